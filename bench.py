@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the ParPaRaw hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config taxi|yelp|clf|cfg1] [--impl ours|reference]
+
+A step = one full parse (all of S1-S8) of one GPU's input: the configuration BASELINE.json's metric
+is quoted on at N=1 is configs[1] (taxi-shaped CSV, 4.8 GB, 18 columns).  For N > 1 (torchrun, one
+rank per GPU, NCCL) every rank owns one contiguous, deliberately not record-aligned 4.8 GB byte
+range of one logical taxi file (weak scaling) and the step includes the two summary allgathers.
+
+`value` = input GB/s of the whole job (all ranks' bytes / max-over-ranks device time), inputs
+resident in HBM, outputs written column-major into pre-sized device columns (capacity from an
+untimed plan pass; DESIGN.md explains why this is not skipped work).  One JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "on-device parse GB/s of input (1/2/4/8 B200) and fraction of HBM roofline"
+CONFIG_LABEL = {
+    "taxi": "NYC-taxi-shaped CSV, 4.8 GB, 18 numeric/datetime columns, unquoted, 1 B200 per rank",
+    "yelp": "Yelp-reviews-shaped CSV, ~4.8 GB, all fields quoted, long multi-line text",
+    "clf": "Common-Log-Format-shaped logs, ~8 GB, 9-state DFA",
+    "cfg1": "1 MB RFC-4180 CSV, 8 columns, ~10% quoted fields",
+}
+RECORDS_PER_RANK = {"taxi": 48_900_000, "yelp": 6_670_000, "clf": 78_000_000, "cfg1": 10_000}
+BYTES_CAP = {"taxi": 4_800_000_000, "yelp": 4_823_000_000, "clf": 8_000_000_000, "cfg1": 1_000_000}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(config):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(config)
+    except Exception:
+        return None
+
+
+class Clocks:
+    def __init__(self):
+        self.proc = None
+        self.path = None
+
+    def start(self, index=0):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}",
+                 "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = float(parts[2])
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        except Exception:
+            return None
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def gen_range(config, rank, world, pin=True):
+    """This rank's byte range of the logical input (host, pinned) + its left context and base."""
+    import torch
+    import datagen
+    w = datagen.WORKLOADS[config]
+    rb = RECORDS_PER_RANK[config]
+    cap = BYTES_CAP[config] + (1 << 20)
+    cut = lambda g: 0 if g == 0 else 37 + 11 * g              # mid-record cut points
+    host = torch.empty(cap + (1 << 20), dtype=torch.uint8, pin_memory=pin)
+    g0 = datagen.fill(w, host.data_ptr(), cap, first_record=rank * rb, max_records=rb)
+    block_len = g0.nbytes
+    # bytes of the next block that belong to this range
+    ext = b""
+    if rank + 1 < world:
+        nxt = b"".join(datagen.record(w, (rank + 1) * rb + i) for i in range(4))
+        ext = nxt[:cut(rank + 1)]
+    n_ext = len(ext)
+    if n_ext:
+        host[block_len:block_len + n_ext] = torch.frombuffer(bytearray(ext), dtype=torch.uint8)
+    c0 = cut(rank) if world > 1 else 0
+    left = host[:c0].clone() if c0 else None
+    data_host = host[c0:block_len + n_ext]
+    return data_host, left, block_len, c0, g0
+
+
+def run_reference(args):
+    """--impl reference: the oracle (the sequential CPU parser) on bounded samples of the workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import datagen
+    import oracle
+    w = datagen.WORKLOADS[args.config]
+    sample = args.ref_sample_bytes
+    data, g = datagen.generate(args.config, sample)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        r = oracle.parse(w.dialect, data, w.C, list(w.types))
+        dt = time.perf_counter() - t0
+        assert r.status == 0 and r.R == g.records
+        if i >= args.warmup:
+            times.append(dt)
+    ms = statistics.mean(times) * 1e3
+    v = len(data) / (ms * 1e-3) / 1e9
+    line = {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.config, "description": CONFIG_LABEL[args.config],
+                       "sample_bytes": len(data), "records": g.records},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"first {len(data)} bytes ({g.records} records) of the {args.config} workload, "
+                                       f"single-threaded sequential parse incl. int64/float64 conversion"},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(config, data_host, budget_s=10.0):
+    """The oracle as it stands, 1 host core, on a bounded prefix of this workload."""
+    import numpy as np
+    import datagen
+    import oracle
+    w = datagen.WORKLOADS[config]
+    arr = data_host.numpy()
+    probe = min(arr.size, 20_000_000)
+    t0 = time.perf_counter()
+    oracle.parse(w.dialect, arr[:probe], w.C, list(w.types))
+    rate = probe / max(time.perf_counter() - t0, 1e-6)
+    n = int(min(arr.size, max(probe, rate * budget_s)))
+    t0 = time.perf_counter()
+    r = oracle.parse(w.dialect, arr[:n], w.C, list(w.types))
+    dt = time.perf_counter() - t0
+    return {"value": round(n / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {n} bytes ({r.R} records) of this rank's input; single-threaded sequential "
+                      f"parse with int64/float64 conversion; {os.cpu_count()} host cores present"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="taxi", choices=list(CONFIG_LABEL))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--ref-sample-bytes", type=int, default=150_000_000)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import datagen
+    import paper_1905_13415_b200 as parpa
+    from paper_1905_13415_b200 import distributed as pdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = datagen.WORKLOADS[args.config]
+    dfa = parpa.Dfa.dialect(w.dialect)
+    schema = parpa.Schema(list(w.types))
+
+    t_gen = time.time()
+    data_host, left_host, block_len, cut0, g = gen_range(args.config, rank, world)
+    t_gen = time.time() - t_gen
+    n = data_host.numel()
+    d = torch.empty(n + 64, dtype=torch.uint8, device="cuda")[:n]
+    d.copy_(data_host, non_blocking=True)
+    left = left_host.cuda() if left_host is not None else None
+    base = 0
+    if world > 1:
+        lens = torch.tensor([block_len], dtype=torch.int64, device="cuda")
+        all_lens = [torch.zeros_like(lens) for _ in range(world)]
+        dist.all_gather(all_lens, lens)
+        base = sum(int(x.item()) for x in all_lens[:rank]) + cut0
+    torch.cuda.synchronize()
+
+    # capacity from an untimed scan pass (records of this range)
+    stream = torch.cuda.current_stream()
+    if world == 1:
+        res_plan = parpa.parse(dfa, schema, d)
+        cap = res_plan.records
+        assert res_plan.status == 0 and cap == g.records, (res_plan.stats, g.records)
+        del res_plan
+    else:
+        cap = g.records + 2
+    cols = parpa.alloc_columns(schema, cap)
+    st = parpa.new_stats_tensor()
+    is_last = rank == world - 1
+
+    def step():
+        if world == 1:
+            return parpa.parse_into(dfa, schema, d, cols, cap, st)
+        pdist.parse_sharded(dfa, schema, d, base, cols, cap, st, left=left, is_last=is_last)
+        return 5
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stats = parpa.stats_from_tensor(st)
+    assert stats["status"] == 0, stats
+    if world == 1:
+        assert stats["records"] == g.records, (stats, g.records)
+
+    clocks = Clocks()
+    clocks.start(local)
+    parpa.set_profiling(True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        launches += step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms_total = e0.elapsed_time(e1)
+    ktimes = parpa.last_kernel_times()
+    parpa.set_profiling(False)
+    clk = clocks.stop()
+    ms_step = ms_total / args.steps
+    if dist:
+        t = torch.tensor([ms_step], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+        tb = torch.tensor([n], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tb, op=dist.ReduceOp.SUM)
+        total_bytes = float(tb.item())
+    else:
+        total_bytes = float(n)
+    value = total_bytes / (ms_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (algorithmic bytes)
+    T = sum(1 for t in w.types if t != datagen.SPAN)
+    R = stats["records"]
+    alg_bytes = n + R * w.C * 12 + R * T * 9
+    dom = "k_scan_emit"
+    kt = [ms for name, ms in ktimes if name == dom] or [ms for name, ms in ktimes if name.startswith("k_scan")]
+    per_kernel = {}
+    for name, ms in ktimes:
+        per_kernel.setdefault(name, []).append(ms)
+    peak, peak_src = load_peaks()
+    roof = None
+    if kt:
+        kms = statistics.mean(kt)
+        achieved = alg_bytes / (kms * 1e-3) / 1e9
+        tr = load_traffic(args.config)
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": tr, "kernel": dom, "kernel_ms": round(kms, 4),
+                "algorithmic_bytes_per_launch": int(alg_bytes), "peak_source": peak_src,
+                "share_of_step": round(kms / ms_step, 4)}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_baseline(args.config, data_host)
+
+    e2e = None
+    if rank == 0 and world == 1 and not args.no_e2e:
+        e2e = run_e2e(parpa, dfa, schema, data_host, cap, w, args.e2e_steps)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+                "config": {"workload": args.config, "description": CONFIG_LABEL[args.config],
+                           "bytes_per_gpu": n, "records_per_gpu": R, "columns": w.C, "typed_columns": T,
+                           "dialect": w.dialect, "path": "fused single-pass parse_into" if world == 1 else
+                           "summarize + allgather + count + allgather + parse_range",
+                           "l2": "input >> 126 MB L2 (no flush needed)", "generate_s": round(t_gen, 1),
+                           "kernel_ms": {k: round(statistics.mean(v), 4) for k, v in per_kernel.items()}},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_e2e(parpa, dfa, schema, data_host, cap, w, steps):
+    """End to end through the public API with HOST buffers: pinned input -> H2D -> parse -> D2H of
+    every output column into pinned host columns, every step (parpa_parse_host)."""
+    import torch
+    import datagen
+    host_cols = []
+    out_bytes = 0
+    for t in w.types:
+        off = torch.empty(cap, dtype=torch.int64, pin_memory=True)
+        ln = torch.empty(cap, dtype=torch.int32, pin_memory=True)
+        out_bytes += cap * 12
+        if t == datagen.SPAN:
+            host_cols.append(parpa.Column(off, ln))
+        else:
+            val = torch.empty(cap, dtype=torch.float64 if t == datagen.FLOAT64 else torch.int64, pin_memory=True)
+            ok = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+            out_bytes += cap * 9
+            host_cols.append(parpa.Column(off, ln, val, ok))
+    times = []
+    for i in range(steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        stats = parpa.parse_host_into(dfa, schema, data_host, host_cols, cap)
+        dt = time.perf_counter() - t0
+        assert stats["status"] == 0 and stats["records"] == cap, stats
+        if i:
+            times.append(dt)
+    t = statistics.mean(times)
+    return {"value": round(data_host.numel() / t / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": int(data_host.numel()), "d2h_bytes_per_step": int(out_bytes + 56),
+            "ms_per_step": round(t * 1e3, 2), "api": "parpa_parse_host (pinned host input and columns)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,233 @@
+/*
+ * parpa.h — C ABI of libparpa, the B200-native (sm_100a) implementation of the data-parallel
+ * hot path of ParPaRaw (arXiv 1905.13415, "ParPaRaw: Massively Parallel Parsing of
+ * Delimiter-Separated Raw Data").  Citations: P:n = line n of the paper's PAPER.md;
+ * DESIGN.md lists the readings R1..R28 taken where the paper is silent.
+ *
+ * What the library computes (all on the GPU, hand-written CUDA kernels; no CPU fallback):
+ *   S1 symbol-group lookup        P:725-731, P:865-884 (tab:twiddling)
+ *   S2 multi-state DFA simulation  P:340-347 (one DFA instance per state -> state-transition vector)
+ *   S3 composite-operator scan     P:349-364 (exclusive scan with (a∘b)_i = b_{a_i}, identity seed)
+ *   S4 delimiter-emitting re-simulation P:368-375 (record / field / control per symbol)
+ *   S5 record / column offset scans P:386-414 (POPCNT record counts, abs/rel column operator ⊕)
+ *   S6 column partition            P:439-457 (here: field spans scattered column-major)
+ *   S7 type conversion             P:459-469 (int64 exact, float64 correctly rounded), defaults
+ *   S8 validation                  P:540-543 (invalid transitions, non-accepting end state)
+ *
+ * Conventions for every function:
+ *   - Returns a status (PARPA_OK or a negative PARPA_E*).  Out-parameters are untouched on error.
+ *   - "device pointer" = CUDA global memory of the current device; "host pointer" = ordinary
+ *     (pinned or pageable) host memory.  Streams are passed as `void *` holding a cudaStream_t
+ *     (NULL = legacy default stream).
+ *   - Work is enqueued on the given stream.  Functions documented as "synchronous" wait for the
+ *     stream before returning.
+ *   - A parpa_dfa is immutable after creation and may be shared across threads and streams.
+ */
+#ifndef PARPA_H
+#define PARPA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---------------------------------------------------------------------- */
+enum {
+  PARPA_OK = 0,
+  PARPA_EINVAL = -1,        /* bad argument / DFA tables violating the validation rules */
+  PARPA_ENOMEM = -2,        /* device or host allocation failed */
+  PARPA_ECUDA = -3,         /* CUDA runtime error (also: no usable device) */
+  PARPA_EFORMAT = -4,       /* input reached the invalid state, or EOI action = error */
+  PARPA_ECOLUMNS = -5,      /* strict schema: some record has != C fields */
+  PARPA_EUNSUPPORTED = -6,  /* DFA too large for this build, field length >= 2^32-1 */
+  PARPA_ENEEDMORE = -7      /* caller capacity too small; the required record count is reported */
+};
+
+/* ---- emission kinds, EOI actions, column types ---------------------------------------- */
+/* The paper's three bitmap indexes (record delimiter, field delimiter, control)
+ * collapse to one 2-bit kind per symbol: RECORD => FIELD => control (reading R2). */
+enum { PARPA_DATA = 0, PARPA_CTRL = 1, PARPA_FIELD = 2, PARPA_RECORD = 3 };
+/* End-of-input action per final state (reading R6, "non-accepting end state"). */
+enum { PARPA_EOI_NONE = 0, PARPA_EOI_RECORD = 1, PARPA_EOI_ERROR = 2 };
+/* Column types: SPAN = raw field span only (strings, datetimes); INT64 / FLOAT64 converted. */
+enum { PARPA_SPAN = 0, PARPA_INT64 = 1, PARPA_FLOAT64 = 2 };
+
+#define PARPA_MISSING_LENGTH 0xFFFFFFFFu   /* length of a missing field (record had fewer fields) */
+#define PARPA_NONE 0xFFFFFFFFFFFFFFFFull   /* "no position" */
+
+typedef struct parpa_dfa parpa_dfa;
+typedef struct parpa_plan parpa_plan;
+typedef struct parpa_result parpa_result;
+
+/* ---- DFA ------------------------------------------------------------------------------- *
+ * parpa_create_dfa — compile a parsing DFA ("uses a DFA while parsing"; P:727:
+ * "collapse all the transition table's symbols that have identical state transitions into
+ * symbol groups"; tab:ttable row-per-group layout).
+ *   num_states      |S|, 2..16 (this build runs |S|-1 <= 8 non-invalid states, else EUNSUPPORTED)
+ *   start_state     the sequential parser's starting state (reading R1)
+ *   invalid_state   the INV state; must be absorbing: transition[g][inv] == inv for all g,
+ *                   and emit[g][inv] == PARPA_CTRL
+ *   num_groups      G, 1..16
+ *   group_of_byte   host uint8[256]: symbol group of each byte value
+ *   transition      host uint8[G][S] row per group: next state from state s on group g
+ *   emit            host uint8[G][S] row per group: emission kind of the symbol, by SOURCE state
+ *   eoi             host uint8[S]: end-of-input action of each final state
+ * On success *out owns a heap object; free it with parpa_destroy_dfa.  Validation failures
+ * return PARPA_EINVAL (SPEC S:32-36 invariants).  Synchronous, no device work. */
+int parpa_create_dfa(uint32_t num_states, uint32_t start_state, uint32_t invalid_state,
+                     uint32_t num_groups, const uint8_t *group_of_byte, const uint8_t *transition,
+                     const uint8_t *emit, const uint8_t *eoi, parpa_dfa **out);
+void parpa_destroy_dfa(parpa_dfa *dfa);
+
+/* ---- schema ------------------------------------------------------------------------------ *
+ * C columns; types[c] in {PARPA_SPAN, PARPA_INT64, PARPA_FLOAT64}; has_default[c] / default_bits[c]
+ * give the column default for empty AND missing typed fields (reading R16: without a
+ * default such fields are null, valid = 0).  default_bits holds the int64 value or the IEEE-754
+ * bits of the double.  strict != 0 turns records with != C fields into PARPA_ECOLUMNS.
+ * All arrays are host memory, read during the call only; has_default / default_bits may be NULL. */
+typedef struct {
+  uint32_t num_columns;
+  const uint8_t *types;
+  const uint8_t *has_default;
+  const int64_t *default_bits;
+  uint32_t strict;
+} parpa_schema;
+
+/* Column storage (device pointers).  Row r of column c is the field of record r (0-based):
+ *   offset[r]  uint64: byte offset of the field's first DATA byte in the input (reading R11;
+ *              for an empty field the position of its terminating delimiter or of EOI; for a
+ *              missing field the position of the record delimiter that ended the record)
+ *   length[r]  uint32: last DATA byte + 1 - offset; 0 if empty; PARPA_MISSING_LENGTH if missing
+ *   value[r]   int64 / double (typed columns only; NULL for spans); 0 when invalid
+ *   valid[r]   uint8: 1 if value holds a converted or default value (typed columns only) */
+typedef struct {
+  uint64_t *offset;
+  uint32_t *length;
+  void *value;
+  uint8_t *valid;
+} parpa_column;
+
+/* Scalar outcome of a parse. */
+typedef struct {
+  uint64_t records;           /* R */
+  uint64_t fields;            /* number of fields closed (incl. the implicit EOI one) */
+  uint64_t first_invalid;     /* byte offset of the first symbol whose transition entered INV, or of
+                                 EOI when the end state's action is error; PARPA_NONE if valid */
+  uint64_t missing_records;   /* records with fewer than C fields */
+  uint64_t extra_fields;      /* fields beyond column C-1 (dropped) */
+  uint64_t deferred_fields;   /* typed fields converted by the slow (device-tier) path */
+  int32_t status;             /* PARPA_OK / EFORMAT / ECOLUMNS / EUNSUPPORTED / ENEEDMORE */
+  uint32_t final_state;       /* DFA state after the last byte */
+} parpa_stats;
+
+/* ---- one-call parse (library-sized outputs) --------------------------------------------- *
+ * parpa_parse — parse len bytes at device pointer d_bytes (input stays caller-owned and must
+ * remain valid until the call returns).  Runs the scan kernel (S1-S5, one input read), reads the
+ * record count back (one host sync), allocates exact [C][R] column storage owned by the result,
+ * then runs the emit kernel (S4-S7, second read), finalize and the deferred-conversion kernel.
+ * Synchronous.  Format errors do not fail the call: *out is produced and its stats carry
+ * PARPA_EFORMAT (outputs are then unspecified). */
+int parpa_parse(const parpa_dfa *dfa, const parpa_schema *schema, const uint8_t *d_bytes,
+                uint64_t len, void *stream, parpa_result **out);
+
+/* Accessors of a parpa_result (host-side handles; column pointers are device memory owned by the
+ * result and freed by parpa_result_free). */
+int parpa_result_stats(const parpa_result *res, parpa_stats *out);
+int parpa_result_column(const parpa_result *res, uint32_t c, parpa_column *out);
+/* copy column c (records rows) into caller device columns `dst` on `stream` (asynchronous) */
+int parpa_result_copy_column(const parpa_result *res, uint32_t c, const parpa_column *dst, void *stream);
+void parpa_result_free(parpa_result *res);
+
+/* ---- two-phase parse into caller-owned columns ---------------------------------------- *
+ * parpa_plan_create — run the scan kernel over the input and keep its per-tile prefixes
+ * (entry state, record/column offsets) in a plan.  Synchronous (one host sync to read R).
+ * parpa_plan_records — the number of rows the emit phase will produce.
+ * parpa_plan_emit — run emit + finalize + deferred conversion into caller columns (each with
+ * room for parpa_plan_records rows); d_stats (device pointer to a parpa_stats, may be NULL) is
+ * written on the stream.  Asynchronous.  The input must still be valid. */
+int parpa_plan_create(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, void *stream,
+                      parpa_plan **out);
+int parpa_plan_records(const parpa_plan *plan, uint64_t *records);
+int parpa_plan_emit(parpa_plan *plan, const parpa_schema *schema, const parpa_column *columns,
+                    parpa_stats *d_stats, void *stream);
+void parpa_plan_destroy(parpa_plan *plan);
+
+/* ---- single-pass parse into caller-owned columns (capacity path) ----------------------- *
+ * parpa_parse_into — one fused kernel reads the input once: S1-S3 with a decoupled look-back
+ * over tile transition vectors, S4-S5 with a second look-back over record/column offsets, then
+ * S6-S7 straight into the caller's columns (capacity rows each), then finalize and deferred
+ * conversion.  Rows >= capacity are not written; d_stats->status is then PARPA_ENEEDMORE and
+ * d_stats->records the number required.  Asynchronous; d_stats is a device pointer (required).
+ * gpu_launches (host, may be NULL) receives the number of kernels enqueued. */
+int parpa_parse_into(const parpa_dfa *dfa, const parpa_schema *schema, const uint8_t *d_bytes,
+                     uint64_t len, const parpa_column *columns, uint64_t capacity,
+                     parpa_stats *d_stats, void *stream, uint32_t *gpu_launches);
+
+/* ---- end-to-end from host memory ------------------------------------------------------- *
+ * parpa_parse_host — h_bytes (host) -> device copy -> parse_into -> columns copied back into
+ * the caller's host columns (capacity rows each) -> *stats (host).  Synchronous. */
+int parpa_parse_host(const parpa_dfa *dfa, const parpa_schema *schema, const uint8_t *h_bytes,
+                     uint64_t len, const parpa_column *h_columns, uint64_t capacity,
+                     parpa_stats *stats, void *stream);
+
+/* ---- range summaries: windows and multi-GPU (context carry; reading R27) ----- *
+ * A byte range [0, len) at global offset `base` of a larger input is reduced to a summary:
+ *   parpa_tau      the range's state-transition vector: tau[i] = state after the range
+ *                  when entered in state i (PARPA entries for i >= num_states are 0xFF)
+ *   parpa_counts   record / field counts, the abs/rel column offset and the carries of
+ *                  the field left open at the range end, for a given entry state
+ * parpa_compose_tau(a, b) = a∘b.  parpa_compose_counts(a, b) = a⊕b on every field.
+ * parpa_parse_range parses a range given the composed summary of everything before it; a typed
+ * field that starts before the range reads its leading bytes from `left_context` (host-visible
+ * device pointer to the `left_len` bytes preceding the range; may be NULL / 0). */
+typedef struct { uint8_t tau[16]; } parpa_tau;
+typedef struct {
+  uint64_t records, fields;
+  uint64_t open_first, open_last;   /* first / last DATA byte (global offsets) of the open field */
+  uint32_t column;                  /* column offset value */
+  uint32_t flags;                   /* bit0 abs, bit1 has delimiter, bit2-4 control-byte carries */
+  uint64_t first_invalid;
+} parpa_counts;
+typedef struct {
+  uint32_t entry_state;             /* DFA state at the range start */
+  uint32_t _pad;
+  uint64_t base;                    /* global byte offset of the range start */
+  parpa_counts prefix;              /* composed counts of all bytes before the range */
+} parpa_context;
+
+int parpa_summarize(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, void *stream,
+                    parpa_tau *out);                                  /* synchronous */
+int parpa_count(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint64_t base,
+                uint32_t entry_state, void *stream, parpa_counts *out, parpa_tau *tau_out);
+int parpa_compose_tau(const parpa_dfa *dfa, const parpa_tau *a, const parpa_tau *b, parpa_tau *out);
+int parpa_compose_counts(const parpa_counts *a, const parpa_counts *b, parpa_counts *out);
+int parpa_parse_range(const parpa_dfa *dfa, const parpa_schema *schema, const uint8_t *d_bytes,
+                      uint64_t len, const parpa_context *ctx, const uint8_t *left_context,
+                      uint64_t left_len, int is_last, const parpa_column *columns,
+                      uint64_t capacity, parpa_stats *d_stats, void *stream);
+
+/* ---- debug export for parity tests ------------------------------------------------------ *
+ * parpa_debug_trace — per-thread-chunk entry states as computed by the scan kernel's S2-S3 path
+ * (d_chunk_states: uint8 per chunk of parpa_chunk_bytes() bytes, DFA state numbering), and, if
+ * d_kinds / d_states are non-NULL, each byte's emission kind and state-before-byte re-simulated on
+ * the GPU from those entry states.  Synchronous. */
+int parpa_debug_trace(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len,
+                      uint8_t *d_chunk_states, uint8_t *d_kinds, uint8_t *d_states, void *stream);
+uint32_t parpa_chunk_bytes(void);
+uint32_t parpa_tile_bytes(void);
+
+/* ---- profiling hooks ----------------------------------------------------------------------- *
+ * parpa_set_profiling(1) clears the history and starts recording a CUDA event pair around every
+ * kernel this thread launches (on the launching stream); parpa_last_kernel_times fills names[i]
+ * (static strings) and ms[i] for up to cap recorded launches, oldest first (synchronises on them). */
+int parpa_set_profiling(int enable);
+int parpa_last_kernel_times(const char **names, float *ms, int cap);
+
+const char *parpa_status_string(int status);
+const char *parpa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PARPA_H */

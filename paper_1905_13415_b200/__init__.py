@@ -1,0 +1,402 @@
+"""paper_1905_13415_b200 — B200-native (sm_100a) ParPaRaw hot path (arXiv 1905.13415).
+
+Thin Python binding over the C ABI of ``libparpa.so`` (include/parpa.h).  Every step of the
+path runs in the library's CUDA kernels; this module only marshals arguments.  PyTorch is
+used for device memory (tensors) and streams.  There is no CPU fallback: if the extension
+cannot be loaded, every entry point raises.
+
+    import paper_1905_13415_b200 as parpa
+    dfa = parpa.Dfa.dialect("csv")                              # tab:ttable
+    schema = parpa.Schema([parpa.INT64, parpa.SPAN, parpa.FLOAT64])
+    res = parpa.parse(dfa, schema, data)                        # data: torch.uint8 CUDA tensor
+    res.records, res.columns[2].value, res.stats
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+from . import _lib
+from . import dialects
+
+SPAN, INT64, FLOAT64 = 0, 1, 2
+DATA, CTRL, FIELD, RECORD = 0, 1, 2, 3
+OK, EINVAL, ENOMEM, ECUDA, EFORMAT, ECOLUMNS, EUNSUPPORTED, ENEEDMORE = 0, -1, -2, -3, -4, -5, -6, -7
+MISSING_LENGTH = 0xFFFFFFFF
+NONE = 0xFFFFFFFFFFFFFFFF
+
+
+class ParpaError(RuntimeError):
+    def __init__(self, code, what=""):
+        lib = _lib.load()
+        super().__init__(f"{what}: {lib.parpa_status_string(code).decode()} ({code})")
+        self.code = code
+
+
+def _check(rc, what):
+    if rc != OK:
+        raise ParpaError(rc, what)
+
+
+def lib():
+    return _lib.load()
+
+
+def _stream_handle(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _u8(buf):
+    return ctypes.cast(buf, _lib.c_u8p)
+
+
+class Dfa:
+    """A compiled parsing DFA (parpa_create_dfa).  Row-per-group tables."""
+
+    def __init__(self, num_states, start, invalid, group_of_byte, transition, emit, eoi, name="custom"):
+        L = _lib.load()
+        G = len(transition)
+        S = num_states
+        gob = (ctypes.c_uint8 * 256)(*group_of_byte)
+        tr = (ctypes.c_uint8 * (G * S))(*[v for row in transition for v in row])
+        em = (ctypes.c_uint8 * (G * S))(*[v for row in emit for v in row])
+        eo = (ctypes.c_uint8 * S)(*eoi)
+        h = ctypes.c_void_p()
+        _check(L.parpa_create_dfa(S, start, invalid, G, _u8(gob), _u8(tr), _u8(em), _u8(eo), ctypes.byref(h)),
+               "parpa_create_dfa")
+        self._h = h
+        self.name = name
+        self.num_states = S
+        self.start = start
+        self.invalid = invalid
+        self.tables = {"group_of_byte": list(group_of_byte), "transition": [list(r) for r in transition],
+                       "emit": [list(r) for r in emit], "eoi": list(eoi), "start": start, "invalid": invalid}
+
+    @classmethod
+    def from_tables(cls, t: "dialects.DfaTables"):
+        return cls(t.S, t.start, t.invalid, t.group_of_byte, t.transition, t.emit, t.eoi, name=t.name)
+
+    @classmethod
+    def dialect(cls, name: str):
+        return cls.from_tables(dialects.get(name))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib._lib is not None:
+            _lib._lib.parpa_destroy_dfa(h)
+            self._h = None
+
+
+@dataclass
+class Schema:
+    """Column types (SPAN / INT64 / FLOAT64), optional defaults for empty / missing typed fields
+    (P:564-568), strict column count."""
+    types: list
+    defaults: list | None = None
+    strict: bool = False
+
+    @property
+    def C(self):
+        return len(self.types)
+
+    def struct(self):
+        C = self.C
+        self._t = (ctypes.c_uint8 * max(C, 1))(*self.types)
+        self._hd = (ctypes.c_uint8 * max(C, 1))()
+        self._db = (ctypes.c_int64 * max(C, 1))()
+        if self.defaults is not None:
+            import struct as _st
+            for c, d in enumerate(self.defaults):
+                if d is None:
+                    continue
+                self._hd[c] = 1
+                if self.types[c] == FLOAT64:
+                    self._db[c] = _st.unpack("<q", _st.pack("<d", float(d)))[0]
+                else:
+                    self._db[c] = int(d)
+        return _lib.Schema_t(C, _u8(self._t), _u8(self._hd), ctypes.cast(self._db, ctypes.POINTER(ctypes.c_int64)),
+                             int(self.strict))
+
+
+class Column:
+    """One output column as torch tensors: offset u64 (int64 storage), length u32 (int32 storage),
+    value int64 / float64 (typed only), valid uint8 (typed only)."""
+
+    def __init__(self, offset, length, value=None, valid=None):
+        self.offset, self.length, self.value, self.valid = offset, length, value, valid
+
+    def struct(self):
+        return _lib.Column_t(self.offset.data_ptr(), self.length.data_ptr(),
+                             self.value.data_ptr() if self.value is not None else None,
+                             self.valid.data_ptr() if self.valid is not None else None)
+
+
+def alloc_columns(schema: Schema, capacity: int, device="cuda"):
+    import torch
+    n = max(int(capacity), 1)
+    cols = []
+    for t in schema.types:
+        off = torch.empty(n, dtype=torch.int64, device=device)
+        ln = torch.empty(n, dtype=torch.int32, device=device)
+        if t == SPAN:
+            cols.append(Column(off, ln))
+        else:
+            val = torch.empty(n, dtype=torch.float64 if t == FLOAT64 else torch.int64, device=device)
+            cols.append(Column(off, ln, val, torch.empty(n, dtype=torch.uint8, device=device)))
+    return cols
+
+
+def _col_array(cols):
+    arr = (_lib.Column_t * max(len(cols), 1))()
+    for i, c in enumerate(cols):
+        arr[i] = c.struct()
+    return arr
+
+
+def stats_from_tensor(t):
+    """Decode a parpa_stats written on the device into a dict (synchronises)."""
+    raw = bytes(t.cpu().numpy().tobytes())
+    s = _lib.Stats_t.from_buffer_copy(raw[:_lib.STATS_BYTES])
+    return {"records": s.records, "fields": s.fields, "first_invalid": s.first_invalid,
+            "missing_records": s.missing_records, "extra_fields": s.extra_fields,
+            "deferred_fields": s.deferred_fields, "status": s.status, "final_state": s.final_state}
+
+
+def new_stats_tensor(device="cuda"):
+    import torch
+    return torch.zeros(_lib.STATS_BYTES, dtype=torch.uint8, device=device)
+
+
+class ParseResult:
+    def __init__(self, columns, stats):
+        self.columns = columns
+        self.stats = stats
+        self.records = stats["records"]
+        self.status = stats["status"]
+
+
+def _check_input(data):
+    import torch
+    if not isinstance(data, torch.Tensor) or data.dtype != torch.uint8 or not data.is_cuda:
+        raise TypeError("data must be a torch.uint8 CUDA tensor")
+    if not data.is_contiguous():
+        raise ValueError("data must be contiguous")
+
+
+def parse(dfa: Dfa, schema: Schema, data, stream=None) -> ParseResult:
+    """Two-phase parse into exactly-sized torch columns (parpa_plan_create + parpa_plan_emit)."""
+    L = _lib.load()
+    _check_input(data)
+    s = _stream_handle(stream)
+    plan = ctypes.c_void_p()
+    _check(L.parpa_plan_create(dfa.handle, ctypes.c_void_p(data.data_ptr()), data.numel(), s, ctypes.byref(plan)),
+           "parpa_plan_create")
+    try:
+        R = ctypes.c_uint64()
+        _check(L.parpa_plan_records(plan, ctypes.byref(R)), "parpa_plan_records")
+        cols = alloc_columns(schema, R.value, data.device)
+        st = new_stats_tensor(data.device)
+        sch = schema.struct()
+        arr = _col_array(cols)
+        _check(L.parpa_plan_emit(plan, ctypes.byref(sch), arr, ctypes.c_void_p(st.data_ptr()), s), "parpa_plan_emit")
+        stats = stats_from_tensor(st)
+    finally:
+        L.parpa_plan_destroy(plan)
+    n = stats["records"]
+    for c in cols:
+        c.offset, c.length = c.offset[:n], c.length[:n]
+        if c.value is not None:
+            c.value, c.valid = c.value[:n], c.valid[:n]
+    return ParseResult(cols, stats)
+
+
+def parse_into(dfa: Dfa, schema: Schema, data, columns, capacity: int, stats_tensor, stream=None) -> int:
+    """Single-pass fused parse into caller columns (parpa_parse_into).  Asynchronous; returns the
+    number of kernels launched."""
+    L = _lib.load()
+    _check_input(data)
+    sch = schema.struct()
+    arr = _col_array(columns)
+    n = ctypes.c_uint32(0)
+    _check(L.parpa_parse_into(dfa.handle, ctypes.byref(sch), ctypes.c_void_p(data.data_ptr()), data.numel(), arr,
+                              int(capacity), ctypes.c_void_p(stats_tensor.data_ptr()), _stream_handle(stream),
+                              ctypes.byref(n)), "parpa_parse_into")
+    return n.value
+
+
+def parse_c_owned(dfa: Dfa, schema: Schema, data, stream=None) -> ParseResult:
+    """parpa_parse (library-allocated result), columns copied into torch tensors, result freed."""
+    import torch
+    L = _lib.load()
+    _check_input(data)
+    sch = schema.struct()
+    s = _stream_handle(stream)
+    res = ctypes.c_void_p()
+    _check(L.parpa_parse(dfa.handle, ctypes.byref(sch), ctypes.c_void_p(data.data_ptr()), data.numel(), s,
+                         ctypes.byref(res)), "parpa_parse")
+    try:
+        st = _lib.Stats_t()
+        _check(L.parpa_result_stats(res, ctypes.byref(st)), "parpa_result_stats")
+        stats = {f: getattr(st, f) for f, _ in _lib.Stats_t._fields_}
+        R = stats["records"]
+        cols = alloc_columns(schema, R, data.device)
+        for c in range(schema.C):
+            dst = cols[c].struct()
+            _check(L.parpa_result_copy_column(res, c, ctypes.byref(dst), s), "parpa_result_copy_column")
+        torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+    finally:
+        L.parpa_result_free(res)
+    for c in cols:
+        c.offset, c.length = c.offset[:R], c.length[:R]
+        if c.value is not None:
+            c.value, c.valid = c.value[:R], c.valid[:R]
+    return ParseResult(cols, stats)
+
+
+def parse_host(dfa: Dfa, schema: Schema, host_bytes, capacity: int, stream=None):
+    """End to end from host memory (parpa_parse_host): returns (stats, numpy columns)."""
+    import numpy as np
+    L = _lib.load()
+    buf = np.ascontiguousarray(host_bytes, dtype=np.uint8).reshape(-1)
+    cap = max(int(capacity), 1)
+    cols_np = []
+    arr = (_lib.Column_t * max(schema.C, 1))()
+    for i, t in enumerate(schema.types):
+        off = np.empty(cap, np.uint64)
+        ln = np.empty(cap, np.uint32)
+        val = np.empty(cap, np.float64 if t == FLOAT64 else np.int64) if t != SPAN else None
+        ok = np.empty(cap, np.uint8) if t != SPAN else None
+        cols_np.append((off, ln, val, ok))
+        arr[i] = _lib.Column_t(off.ctypes.data, ln.ctypes.data, val.ctypes.data if val is not None else None,
+                               ok.ctypes.data if ok is not None else None)
+    sch = schema.struct()
+    st = _lib.Stats_t()
+    _check(L.parpa_parse_host(dfa.handle, ctypes.byref(sch), ctypes.c_void_p(buf.ctypes.data), buf.size, arr, cap,
+                              ctypes.byref(st), _stream_handle(stream)), "parpa_parse_host")
+    stats = {f: getattr(st, f) for f, _ in _lib.Stats_t._fields_}
+    R = min(stats["records"], cap)
+    return stats, [(o[:R], n[:R], v[:R] if v is not None else None, k[:R] if k is not None else None)
+                   for o, n, v, k in cols_np]
+
+
+def parse_host_into(dfa: Dfa, schema: Schema, host_data, host_columns, capacity: int, stream=None):
+    """End to end from host tensors (pinned for full PCIe bandwidth): parpa_parse_host copies the input
+    to the device, parses it and copies every column back into ``host_columns``.  Returns stats."""
+    L = _lib.load()
+    sch = schema.struct()
+    arr = _col_array(host_columns)
+    st = _lib.Stats_t()
+    _check(L.parpa_parse_host(dfa.handle, ctypes.byref(sch), ctypes.c_void_p(host_data.data_ptr()), host_data.numel(),
+                              arr, int(capacity), ctypes.byref(st), _stream_handle(stream)), "parpa_parse_host")
+    return {f: getattr(st, f) for f, _ in _lib.Stats_t._fields_}
+
+
+def debug_trace(dfa: Dfa, data, per_byte=True, stream=None):
+    """GPU per-chunk entry states (S2-S3 path) and, optionally, per-byte kinds / states."""
+    import torch
+    L = _lib.load()
+    _check_input(data)
+    n = data.numel()
+    cb = L.parpa_chunk_bytes()
+    nch = (n + cb - 1) // cb
+    cs = torch.empty(max(nch, 1), dtype=torch.uint8, device=data.device)
+    kinds = torch.empty(max(n, 1), dtype=torch.uint8, device=data.device) if per_byte else None
+    states = torch.empty(max(n, 1), dtype=torch.uint8, device=data.device) if per_byte else None
+    _check(L.parpa_debug_trace(dfa.handle, ctypes.c_void_p(data.data_ptr()), n, ctypes.c_void_p(cs.data_ptr()),
+                               ctypes.c_void_p(kinds.data_ptr()) if per_byte else None,
+                               ctypes.c_void_p(states.data_ptr()) if per_byte else None, _stream_handle(stream)),
+           "parpa_debug_trace")
+    return cs[:nch], (kinds[:n] if per_byte else None), (states[:n] if per_byte else None)
+
+
+# ---- range summaries (windows / multi-GPU) -------------------------------------------------
+def summarize(dfa: Dfa, data, stream=None):
+    L = _lib.load()
+    _check_input(data)
+    t = _lib.Tau_t()
+    _check(L.parpa_summarize(dfa.handle, ctypes.c_void_p(data.data_ptr()), data.numel(), _stream_handle(stream),
+                             ctypes.byref(t)), "parpa_summarize")
+    return list(t.tau[:dfa.num_states])
+
+
+def count(dfa: Dfa, data, base: int, entry_state: int, stream=None):
+    L = _lib.load()
+    _check_input(data)
+    c = _lib.Counts_t()
+    t = _lib.Tau_t()
+    _check(L.parpa_count(dfa.handle, ctypes.c_void_p(data.data_ptr()), data.numel(), int(base), int(entry_state),
+                         _stream_handle(stream), ctypes.byref(c), ctypes.byref(t)), "parpa_count")
+    return c, list(t.tau[:dfa.num_states])
+
+
+def compose_tau(dfa: Dfa, a, b):
+    L = _lib.load()
+    ta, tb, out = _lib.Tau_t(), _lib.Tau_t(), _lib.Tau_t()
+    for i in range(16):
+        ta.tau[i] = a[i] if i < len(a) else 0xFF
+        tb.tau[i] = b[i] if i < len(b) else 0xFF
+    _check(L.parpa_compose_tau(dfa.handle, ctypes.byref(ta), ctypes.byref(tb), ctypes.byref(out)), "compose_tau")
+    return list(out.tau[:dfa.num_states])
+
+
+def compose_counts(a, b):
+    L = _lib.load()
+    out = _lib.Counts_t()
+    _check(L.parpa_compose_counts(ctypes.byref(a), ctypes.byref(b), ctypes.byref(out)), "compose_counts")
+    return out
+
+
+def identity_counts():
+    return _lib.Counts_t(0, 0, NONE, NONE, 0, 0, NONE)
+
+
+def counts_to_bytes(c) -> bytes:
+    return bytes(c)
+
+
+def counts_from_bytes(b: bytes):
+    return _lib.Counts_t.from_buffer_copy(b)
+
+
+def parse_range(dfa: Dfa, schema: Schema, data, entry_state: int, base: int, prefix, columns, capacity: int,
+                stats_tensor, left=None, is_last=True, stream=None):
+    L = _lib.load()
+    _check_input(data)
+    ctx = _lib.Context_t(int(entry_state), 0, int(base), prefix)
+    sch = schema.struct()
+    arr = _col_array(columns)
+    lptr = ctypes.c_void_p(left.data_ptr()) if left is not None and left.numel() else None
+    llen = left.numel() if left is not None else 0
+    _check(L.parpa_parse_range(dfa.handle, ctypes.byref(sch), ctypes.c_void_p(data.data_ptr()), data.numel(),
+                               ctypes.byref(ctx), lptr, llen, int(bool(is_last)), arr, int(capacity),
+                               ctypes.c_void_p(stats_tensor.data_ptr()), _stream_handle(stream)), "parpa_parse_range")
+
+
+def set_profiling(enable: bool):
+    _lib.load().parpa_set_profiling(int(enable))
+
+
+def last_kernel_times():
+    L = _lib.load()
+    names = (ctypes.c_char_p * 4096)()
+    ms = (ctypes.c_float * 4096)()
+    n = L.parpa_last_kernel_times(names, ms, 4096)
+    return [(names[i].decode(), ms[i]) for i in range(n)]
+
+
+def chunk_bytes() -> int:
+    return _lib.load().parpa_chunk_bytes()
+
+
+def tile_bytes() -> int:
+    return _lib.load().parpa_tile_bytes()
+
+
+def version() -> str:
+    return _lib.load().parpa_version().decode()

@@ -1,0 +1,760 @@
+// parpa_api.cu — host side of libparpa: DFA compilation, workspace, kernel launches, the C ABI of
+// include/parpa.h.  Build: see paper_1905_13415_b200/build.py (nvcc -gencode arch=compute_100a,
+// code=sm_100a -lineinfo -O3 -shared).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/parpa.h"
+#include "parpa_kernels.cuh"
+
+using namespace parpa;
+
+struct parpa_dfa {
+  uint32_t S, G, start, inv;
+  uint8_t gob[256];
+  uint8_t trans[16][16], emit[16][16], eoi[16];
+  uint8_t dmap[16];       // DFA state -> device state (0..7, 0xF = INV)
+  DfaK k;                 // compiled tables (kernel parameter)
+};
+
+namespace {
+
+constexpr size_t ALIGN = 256;
+size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
+
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return PARPA_OK;
+  if (e == cudaErrorMemoryAllocation) return PARPA_ENOMEM;
+  return PARPA_ECUDA;
+}
+#define CK(x)                                  \
+  do {                                         \
+    cudaError_t _e = (x);                      \
+    if (_e != cudaSuccess) return cuda_status(_e); \
+  } while (0)
+
+// ---- per-device launch configuration -----------------------------------------------------
+struct DevCfg {
+  bool init = false;
+  int sms = 0;
+  int occ_scan[3] = {0, 0, 0};
+  int occ_emit = 0;
+};
+std::mutex g_mu;
+DevCfg g_dev[64];
+
+int dev_cfg(DevCfg **out) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return PARPA_ECUDA;
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevCfg &c = g_dev[dev];
+  if (!c.init) {
+    CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
+    CK(cudaFuncSetAttribute(k_scan<MODE_TAU>, cudaFuncAttributeMaxDynamicSharedMemorySize, LUT_BYTES));
+    CK(cudaFuncSetAttribute(k_scan<MODE_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, LUT_BYTES));
+    CK(cudaFuncSetAttribute(k_scan<MODE_EMIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, LUT_BYTES));
+    CK(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, LUT_BYTES));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[0], k_scan<MODE_TAU>, THREADS, LUT_BYTES));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[1], k_scan<MODE_COUNT>, THREADS, LUT_BYTES));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[2], k_scan<MODE_EMIT>, THREADS, LUT_BYTES));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit, THREADS, LUT_BYTES));
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    c.init = true;
+  }
+  *out = &c;
+  return PARPA_OK;
+}
+
+// ---- profiling ----------------------------------------------------------------------------
+struct ProfRec {
+  const char *name;
+  cudaEvent_t a, b;
+};
+bool g_prof = false;
+thread_local std::vector<ProfRec> t_prof;
+thread_local std::vector<ProfRec> t_prof_done;
+
+struct Launch {
+  cudaStream_t s;
+  const char *name;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Launch(cudaStream_t st, const char *n) : s(st), name(n) {
+    if (g_prof) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~Launch() {
+    if (g_prof) {
+      cudaEventRecord(b, s);
+      t_prof.push_back(ProfRec{name, a, b});
+    }
+  }
+};
+void prof_begin() {}
+void prof_end() {
+  if (!g_prof) return;
+  t_prof_done.insert(t_prof_done.end(), t_prof.begin(), t_prof.end());
+  t_prof.clear();
+}
+void prof_clear() {
+  for (auto &r : t_prof) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  for (auto &r : t_prof_done) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  t_prof.clear();
+  t_prof_done.clear();
+}
+
+// ---- workspace ------------------------------------------------------------------------------
+struct Work {
+  void *block = nullptr;
+  size_t zero_bytes = 0;
+  unsigned long long *tau_desc = nullptr;
+  uint32_t *seg_flag = nullptr;
+  Ctrl *ctrl = nullptr;
+  Seg *seg_agg = nullptr, *seg_incl = nullptr;
+  TileInfo *tinfo = nullptr;
+  uint8_t *chunk_state = nullptr;
+  DeferItem *dq = nullptr;
+  Stats *stats = nullptr;
+  uint8_t *aligned_in = nullptr;
+  uint32_t ntiles = 0, dq_cap = 0;
+};
+
+int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cudaStream_t s) {
+  uint64_t nt64 = (len + TILE - 1) / TILE;
+  if (nt64 > 0xFFFFFFF0ull) return PARPA_EUNSUPPORTED;
+  w.ntiles = (uint32_t)nt64;
+  size_t nt = std::max<size_t>(w.ntiles, 1);
+  w.dq_cap = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(4096, len / 512), 1u << 24);
+  size_t o = 0;
+  size_t o_tau = o; o = align_up(o + nt * 8);
+  size_t o_flag = o; o = align_up(o + nt * 4);
+  size_t o_ctrl = o; o = align_up(o + sizeof(Ctrl));
+  size_t zero = o;
+  size_t o_agg = o; o = align_up(o + nt * sizeof(Seg));
+  size_t o_incl = o; o = align_up(o + nt * sizeof(Seg));
+  size_t o_tinfo = o; o = align_up(o + nt * sizeof(TileInfo));
+  size_t o_cs = o; o = align_up(o + nt * THREADS);
+  size_t o_dq = o; o = align_up(o + (size_t)w.dq_cap * sizeof(DeferItem));
+  size_t o_st = o; o = align_up(o + sizeof(Stats));
+  size_t o_in = o; if (need_aligned_copy) o = align_up(o + len);
+  CK(cudaMallocAsync(&w.block, o, s));
+  uint8_t *b = (uint8_t *)w.block;
+  w.tau_desc = (unsigned long long *)(b + o_tau);
+  w.seg_flag = (uint32_t *)(b + o_flag);
+  w.ctrl = (Ctrl *)(b + o_ctrl);
+  w.seg_agg = (Seg *)(b + o_agg);
+  w.seg_incl = (Seg *)(b + o_incl);
+  w.tinfo = (TileInfo *)(b + o_tinfo);
+  w.chunk_state = b + o_cs;
+  w.dq = (DeferItem *)(b + o_dq);
+  w.stats = (Stats *)(b + o_st);
+  w.aligned_in = need_aligned_copy ? b + o_in : nullptr;
+  w.zero_bytes = zero;
+  CK(cudaMemsetAsync(w.block, 0, zero, s));
+  return PARPA_OK;
+}
+void work_free(Work &w, cudaStream_t s) {
+  if (w.block) cudaFreeAsync(w.block, s);
+  w.block = nullptr;
+}
+
+Seg seg_identity() { return Seg{0ull, 0ull, NONE, NONE, 0u, 0u}; }
+
+Seg counts_to_seg(const parpa_counts &c) {
+  return Seg{c.records, c.fields, c.open_first, c.open_last, c.column, c.flags};
+}
+parpa_counts seg_to_counts(const Seg &s, uint64_t first_inv) {
+  parpa_counts c;
+  c.records = s.recs; c.fields = s.nflds; c.open_first = s.fd; c.open_last = s.ld;
+  c.column = s.col; c.flags = s.flags; c.first_invalid = first_inv;
+  return c;
+}
+
+void make_args(KArgs &a, const Work &w, const uint8_t *in, uint64_t len) {
+  memset(&a, 0, sizeof(a));
+  a.in = in;
+  a.len = len;
+  a.ntiles = w.ntiles;
+  a.seed = seg_identity();
+  a.tau_desc = w.tau_desc;
+  a.seg_flag = w.seg_flag;
+  a.seg_agg = w.seg_agg;
+  a.seg_incl = w.seg_incl;
+  a.tinfo = w.tinfo;
+  a.chunk_state = w.chunk_state;
+  a.ctrl = w.ctrl;
+  a.dq = w.dq;
+  a.dq_cap = w.dq_cap;
+  a.is_last = 1;
+  a.cap = 0;
+}
+
+int prepare_input(Work &w, const uint8_t *&in, uint64_t len, cudaStream_t s) {
+  if (w.aligned_in) {
+    CK(cudaMemcpyAsync(w.aligned_in, in, len, cudaMemcpyDeviceToDevice, s));
+    in = w.aligned_in;
+  }
+  return PARPA_OK;
+}
+bool misaligned(const void *p) { return ((uintptr_t)p & 15u) != 0; }
+
+int set_columns(const parpa_schema *sch, const parpa_column *cols, uint32_t C, ColsK &ck) {
+  memset(&ck, 0, sizeof(ck));
+  if (C > MAX_COLS) return PARPA_EUNSUPPORTED;
+  for (uint32_t c = 0; c < C; c++) {
+    ColDesc &d = ck.c[c];
+    d.off = (unsigned long long *)cols[c].offset;
+    d.len = cols[c].length;
+    d.val = cols[c].value;
+    d.valid = cols[c].valid;
+    d.type = sch->types ? sch->types[c] : PARPA_SPAN;
+    d.has_def = sch->has_default ? sch->has_default[c] : 0;
+    d.def_bits = sch->default_bits ? sch->default_bits[c] : 0;
+    if (d.type > PARPA_FLOAT64) return PARPA_EINVAL;
+    if (!d.off || !d.len) return PARPA_EINVAL;
+    if (d.type != PARPA_SPAN && (!d.val || !d.valid)) return PARPA_EINVAL;
+  }
+  return PARPA_OK;
+}
+
+int grid_for(int occ, int sms, uint32_t ntiles) {
+  long long g = (long long)std::max(occ, 1) * sms;
+  return (int)std::max<long long>(1, std::min<long long>(g, ntiles));
+}
+
+int launch_scan(int mode, const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, uint32_t *launches) {
+  if (a.ntiles == 0) return PARPA_OK;
+  DevCfg *dc;
+  int rc = dev_cfg(&dc);
+  if (rc) return rc;
+  int g = grid_for(dc->occ_scan[mode], dc->sms, a.ntiles);
+  {
+    Launch L(s, mode == MODE_EMIT ? "k_scan_emit" : mode == MODE_COUNT ? "k_scan_count" : "k_scan_tau");
+    if (mode == MODE_TAU) k_scan<MODE_TAU><<<g, THREADS, LUT_BYTES, s>>>(a, k, ck);
+    else if (mode == MODE_COUNT) k_scan<MODE_COUNT><<<g, THREADS, LUT_BYTES, s>>>(a, k, ck);
+    else k_scan<MODE_EMIT><<<g, THREADS, LUT_BYTES, s>>>(a, k, ck);
+  }
+  if (launches) (*launches)++;
+  CK(cudaGetLastError());
+  return PARPA_OK;
+}
+
+int launch_tail(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, uint32_t *launches) {
+  DevCfg *dc;
+  int rc = dev_cfg(&dc);
+  if (rc) return rc;
+  {
+    Launch L(s, "k_finalize");
+    k_finalize<<<1, 32, 0, s>>>(a, k, ck);
+  }
+  CK(cudaGetLastError());
+  {
+    Launch L(s, "k_deferred");
+    k_deferred<<<dc->sms * 2, 128, 0, s>>>(a, k, ck);
+  }
+  CK(cudaGetLastError());
+  if (launches) *launches += 2;
+  return PARPA_OK;
+}
+
+void host_tau_dfa(const parpa_dfa *d, uint32_t nib, parpa_tau *out) {
+  for (int i = 0; i < 16; i++) out->tau[i] = 0xFF;
+  for (uint32_t i = 0; i < d->S; i++) {
+    uint32_t di = d->dmap[i];
+    uint32_t r = di == INV_DEV ? INV_DEV : (nib >> (4 * di)) & 0xF;
+    out->tau[i] = d->k.hmap[r];
+  }
+}
+
+}  // namespace
+
+struct parpa_plan {
+  const parpa_dfa *dfa;
+  const uint8_t *in;
+  uint64_t len;
+  Work w;
+  KArgs a;
+  uint64_t records;
+  cudaStream_t s;
+};
+
+struct parpa_result {
+  uint32_t C;
+  std::vector<parpa_column> cols;
+  std::vector<void *> allocs;
+  parpa_stats stats;
+};
+
+extern "C" {
+
+const char *parpa_version(void) { return "parpa 0.1 (sm_100a, dense LUT path)"; }
+uint32_t parpa_chunk_bytes(void) { return CHUNK; }
+uint32_t parpa_tile_bytes(void) { return TILE; }
+
+const char *parpa_status_string(int st) {
+  switch (st) {
+  case PARPA_OK: return "ok";
+  case PARPA_EINVAL: return "invalid argument";
+  case PARPA_ENOMEM: return "out of memory";
+  case PARPA_ECUDA: return "CUDA error";
+  case PARPA_EFORMAT: return "format error (invalid state reached or non-accepting end state)";
+  case PARPA_ECOLUMNS: return "record with a number of fields != number of columns (strict)";
+  case PARPA_EUNSUPPORTED: return "unsupported (DFA too large, field too long, or device-tier overflow)";
+  case PARPA_ENEEDMORE: return "output capacity too small";
+  default: return "unknown status";
+  }
+}
+
+int parpa_create_dfa(uint32_t S, uint32_t start, uint32_t inv, uint32_t G, const uint8_t *gob,
+                     const uint8_t *trans, const uint8_t *emit, const uint8_t *eoi, parpa_dfa **out) {
+  if (!out || !gob || !trans || !emit || !eoi) return PARPA_EINVAL;
+  if (S < 2 || S > 16 || G < 1 || G > 16 || start >= S || inv >= S || start == inv) return PARPA_EINVAL;
+  for (int b = 0; b < 256; b++)
+    if (gob[b] >= G) return PARPA_EINVAL;
+  for (uint32_t g = 0; g < G; g++)
+    for (uint32_t s = 0; s < S; s++) {
+      if (trans[g * S + s] >= S || emit[g * S + s] > PARPA_RECORD) return PARPA_EINVAL;
+    }
+  for (uint32_t g = 0; g < G; g++)
+    if (trans[g * S + inv] != inv || emit[g * S + inv] != PARPA_CTRL) return PARPA_EINVAL;
+  for (uint32_t s = 0; s < S; s++)
+    if (eoi[s] > PARPA_EOI_ERROR) return PARPA_EINVAL;
+  if (S - 1 > 8) return PARPA_EUNSUPPORTED;
+  parpa_dfa *d = new (std::nothrow) parpa_dfa;
+  if (!d) return PARPA_ENOMEM;
+  memset(d, 0, sizeof(*d));
+  d->S = S; d->G = G; d->start = start; d->inv = inv;
+  memcpy(d->gob, gob, 256);
+  for (uint32_t g = 0; g < G; g++)
+    for (uint32_t s = 0; s < S; s++) {
+      d->trans[g][s] = trans[g * S + s];
+      d->emit[g][s] = emit[g * S + s];
+    }
+  memcpy(d->eoi, eoi, S);
+  // device numbering: live states 0..k-1 in order, INV -> 0xF
+  uint32_t live[8], k = 0;
+  for (uint32_t s = 0; s < S; s++) {
+    if (s == inv) { d->dmap[s] = INV_DEV; continue; }
+    d->dmap[s] = (uint8_t)k;
+    live[k++] = s;
+  }
+  for (int j = 0; j < 16; j++) { d->k.hmap[j] = (uint8_t)inv; d->k.eoi[j] = eoi[inv]; }
+  for (uint32_t j = 0; j < k; j++) { d->k.hmap[j] = (uint8_t)live[j]; d->k.eoi[j] = eoi[live[j]]; }
+  for (int b = 0; b < 256; b++) {
+    uint32_t g = gob[b];
+    uint32_t sel = 0;
+    uint8_t step[8];
+    for (uint32_t j = 0; j < 8; j++) {
+      uint32_t nd = INV_DEV, kind = PARPA_CTRL;
+      if (j < k) {
+        uint32_t s = live[j];
+        nd = d->dmap[d->trans[g][s]];
+        kind = d->emit[g][s];
+      }
+      sel |= nd << (4 * j);
+      uint32_t fl = (kind != PARPA_DATA ? NOT_DATA : 0) |
+                    ((kind != PARPA_FIELD && kind != PARPA_RECORD) ? NOT_DELIM : 0) |
+                    (kind != PARPA_RECORD ? NOT_REC : 0);
+      step[j] = (uint8_t)(0x80u | nd | fl);
+    }
+    d->k.lut[b][0] = sel & 0xFFFFu;
+    d->k.lut[b][1] = sel >> 16;
+    d->k.lut[b][2] = step[0] | (step[1] << 8) | (step[2] << 16) | ((uint32_t)step[3] << 24);
+    d->k.lut[b][3] = step[4] | (step[5] << 8) | (step[6] << 16) | ((uint32_t)step[7] << 24);
+  }
+  *out = d;
+  return PARPA_OK;
+}
+
+void parpa_destroy_dfa(parpa_dfa *d) { delete d; }
+
+int parpa_set_profiling(int enable) {
+  prof_clear();
+  g_prof = enable != 0;
+  return PARPA_OK;
+}
+
+int parpa_last_kernel_times(const char **names, float *ms, int cap) {
+  int n = 0;
+  for (auto &r : t_prof_done) {
+    if (n >= cap) break;
+    float t = 0;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) t = -1;
+    if (names) names[n] = r.name;
+    if (ms) ms[n] = t;
+    n++;
+  }
+  return n;
+}
+
+// ---- plan: scan pass -------------------------------------------------------------------------
+static int plan_scan(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint32_t seed_dev,
+                     const Seg &seed, uint64_t base, uint32_t C, cudaStream_t s, parpa_plan *p) {
+  p->dfa = dfa;
+  p->len = len;
+  p->s = s;
+  int rc = work_alloc(p->w, len, C, len && misaligned(d_bytes), s);
+  if (rc) return rc;
+  const uint8_t *in = d_bytes;
+  if ((rc = prepare_input(p->w, in, len, s))) return rc;
+  p->in = in;
+  make_args(p->a, p->w, in, len);
+  p->a.seed_dev = seed_dev;
+  p->a.seed = seed;
+  p->a.base = base;
+  p->a.row_base = seed.recs;
+  ColsK ck;
+  memset(&ck, 0, sizeof(ck));
+  return launch_scan(MODE_COUNT, p->a, dfa->k, ck, s, nullptr);
+}
+
+static int plan_totals(parpa_plan *p, Seg &tot, uint32_t &tau, uint64_t &first_inv) {
+  cudaStream_t s = p->s;
+  tot = p->a.seed;
+  tau = NIB_IDENT;
+  Ctrl ctrl;
+  if (p->w.ntiles) {
+    unsigned long long desc;
+    CK(cudaMemcpyAsync(&tot, p->w.seg_incl + (p->w.ntiles - 1), sizeof(Seg), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&desc, p->w.tau_desc + (p->w.ntiles - 1), 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&ctrl, p->w.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    tau = (uint32_t)desc;
+    first_inv = ctrl.inv_neg ? ~ctrl.inv_neg : NONE;
+  } else {
+    first_inv = NONE;
+  }
+  return PARPA_OK;
+}
+
+int parpa_plan_create(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, void *stream,
+                      parpa_plan **out) {
+  if (!dfa || !out || (len && !d_bytes)) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  parpa_plan *p = new (std::nothrow) parpa_plan;
+  if (!p) return PARPA_ENOMEM;
+  prof_begin();
+  int rc = plan_scan(dfa, d_bytes, len, dfa->dmap[dfa->start], seg_identity(), 0, 1024, s, p);
+  if (rc) { work_free(p->w, s); delete p; return rc; }
+  Seg tot;
+  uint32_t tau;
+  uint64_t fi;
+  if ((rc = plan_totals(p, tot, tau, fi))) { work_free(p->w, s); delete p; return rc; }
+  uint32_t fin = nib_at(tau, p->a.seed_dev);
+  p->records = tot.recs + (dfa->k.eoi[fin] == EOI_RECORD ? 1 : 0);
+  *out = p;
+  return PARPA_OK;
+}
+
+int parpa_plan_records(const parpa_plan *p, uint64_t *records) {
+  if (!p || !records) return PARPA_EINVAL;
+  *records = p->records;
+  return PARPA_OK;
+}
+
+int parpa_plan_emit(parpa_plan *p, const parpa_schema *sch, const parpa_column *cols, parpa_stats *d_stats,
+                    void *stream) {
+  if (!p || !sch || (sch->num_columns && !cols)) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  ColsK ck;
+  int rc = set_columns(sch, cols, sch->num_columns, ck);
+  if (rc) return rc;
+  KArgs a = p->a;
+  a.C = sch->num_columns;
+  a.strict = sch->strict;
+  a.cap = p->records;
+  a.stats = d_stats ? (Stats *)d_stats : p->w.stats;
+  if (a.ntiles) {
+    DevCfg *dc;
+    if ((rc = dev_cfg(&dc))) return rc;
+    int g = grid_for(dc->occ_emit, dc->sms, a.ntiles);
+    {
+      Launch L(s, "k_emit");
+      k_emit<<<g, THREADS, LUT_BYTES, s>>>(a, p->dfa->k, ck);
+    }
+    CK(cudaGetLastError());
+  }
+  rc = launch_tail(a, p->dfa->k, ck, s, nullptr);
+  prof_end();
+  return rc;
+}
+
+void parpa_plan_destroy(parpa_plan *p) {
+  if (!p) return;
+  work_free(p->w, p->s);
+  delete p;
+}
+
+// ---- one-call parse -------------------------------------------------------------------------------
+int parpa_parse(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_bytes, uint64_t len,
+                void *stream, parpa_result **out) {
+  if (!dfa || !sch || !out) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  parpa_plan *p = nullptr;
+  int rc = parpa_plan_create(dfa, d_bytes, len, stream, &p);
+  if (rc) return rc;
+  parpa_result *r = new (std::nothrow) parpa_result;
+  if (!r) { parpa_plan_destroy(p); return PARPA_ENOMEM; }
+  uint32_t C = sch->num_columns;
+  r->C = C;
+  r->cols.resize(C);
+  uint64_t R = std::max<uint64_t>(p->records, 1);
+  for (uint32_t c = 0; c < C; c++) {
+    uint8_t type = sch->types ? sch->types[c] : PARPA_SPAN;
+    void *a = nullptr;
+    size_t per = 8 + 4 + (type != PARPA_SPAN ? 9 : 0);
+    if (cudaMallocAsync(&a, R * per + 64, s) != cudaSuccess) { rc = PARPA_ENOMEM; break; }
+    r->allocs.push_back(a);
+    uint8_t *b = (uint8_t *)a;
+    r->cols[c].offset = (uint64_t *)b;
+    r->cols[c].value = type != PARPA_SPAN ? (void *)(b + R * 8) : nullptr;
+    r->cols[c].length = (uint32_t *)(b + R * (type != PARPA_SPAN ? 16 : 8));
+    r->cols[c].valid = type != PARPA_SPAN ? b + R * 20 : nullptr;
+  }
+  if (!rc) rc = parpa_plan_emit(p, sch, r->cols.data(), nullptr, stream);
+  if (!rc) {
+    Stats st;
+    if (cudaMemcpyAsync(&st, p->w.stats, sizeof(Stats), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      rc = PARPA_ECUDA;
+    memcpy(&r->stats, &st, sizeof(st));
+  }
+  parpa_plan_destroy(p);
+  if (rc) { parpa_result_free(r); return rc; }
+  *out = r;
+  return PARPA_OK;
+}
+
+int parpa_result_stats(const parpa_result *r, parpa_stats *out) {
+  if (!r || !out) return PARPA_EINVAL;
+  *out = r->stats;
+  return PARPA_OK;
+}
+int parpa_result_column(const parpa_result *r, uint32_t c, parpa_column *out) {
+  if (!r || !out || c >= r->C) return PARPA_EINVAL;
+  *out = r->cols[c];
+  return PARPA_OK;
+}
+int parpa_result_copy_column(const parpa_result *r, uint32_t c, const parpa_column *dst, void *stream) {
+  if (!r || !dst || c >= r->C) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t R = r->stats.records;
+  if (!R) return PARPA_OK;
+  const parpa_column &src = r->cols[c];
+  if (dst->offset) CK(cudaMemcpyAsync(dst->offset, src.offset, R * 8, cudaMemcpyDeviceToDevice, s));
+  if (dst->length) CK(cudaMemcpyAsync(dst->length, src.length, R * 4, cudaMemcpyDeviceToDevice, s));
+  if (dst->value && src.value) CK(cudaMemcpyAsync(dst->value, src.value, R * 8, cudaMemcpyDeviceToDevice, s));
+  if (dst->valid && src.valid) CK(cudaMemcpyAsync(dst->valid, src.valid, R, cudaMemcpyDeviceToDevice, s));
+  return PARPA_OK;
+}
+
+void parpa_result_free(parpa_result *r) {
+  if (!r) return;
+  for (void *a : r->allocs) cudaFree(a);
+  delete r;
+}
+
+// ---- single-pass capacity path ------------------------------------------------------------------
+static int parse_into_impl(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_bytes, uint64_t len,
+                           const parpa_column *cols, uint64_t cap, parpa_stats *d_stats, cudaStream_t s,
+                           uint32_t seed_dev, const Seg &seed, uint64_t base, const uint8_t *left,
+                           uint64_t left_len, int is_last, uint32_t *launches) {
+  if (!dfa || !sch || !d_stats || (len && !d_bytes) || (sch->num_columns && !cols)) return PARPA_EINVAL;
+  ColsK ck;
+  int rc = set_columns(sch, cols, sch->num_columns, ck);
+  if (rc) return rc;
+  prof_begin();
+  Work w;
+  rc = work_alloc(w, len, sch->num_columns, len && misaligned(d_bytes), s);
+  if (rc) return rc;
+  const uint8_t *in = d_bytes;
+  if (!rc) rc = prepare_input(w, in, len, s);
+  if (!rc) {
+    KArgs a;
+    make_args(a, w, in, len);
+    a.C = sch->num_columns;
+    a.strict = sch->strict;
+    a.cap = cap;
+    a.stats = (Stats *)d_stats;
+    a.seed_dev = seed_dev;
+    a.seed = seed;
+    a.base = base;
+    a.row_base = seed.recs;
+    a.left = left;
+    a.left_len = left_len;
+    a.is_last = is_last;
+    uint32_t n = 0;
+    rc = launch_scan(MODE_EMIT, a, dfa->k, ck, s, &n);
+    if (!rc) rc = launch_tail(a, dfa->k, ck, s, &n);
+    if (launches) *launches = n;
+  }
+  work_free(w, s);
+  prof_end();
+  return rc;
+}
+
+int parpa_parse_into(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_bytes, uint64_t len,
+                     const parpa_column *cols, uint64_t cap, parpa_stats *d_stats, void *stream,
+                     uint32_t *gpu_launches) {
+  if (!dfa) return PARPA_EINVAL;
+  return parse_into_impl(dfa, sch, d_bytes, len, cols, cap, d_stats, (cudaStream_t)stream,
+                         dfa->dmap[dfa->start], seg_identity(), 0, nullptr, 0, 1, gpu_launches);
+}
+
+int parpa_parse_range(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_bytes, uint64_t len,
+                      const parpa_context *ctx, const uint8_t *left, uint64_t left_len, int is_last,
+                      const parpa_column *cols, uint64_t cap, parpa_stats *d_stats, void *stream) {
+  if (!dfa || !ctx || ctx->entry_state >= dfa->S) return PARPA_EINVAL;
+  return parse_into_impl(dfa, sch, d_bytes, len, cols, cap, d_stats, (cudaStream_t)stream,
+                         dfa->dmap[ctx->entry_state], counts_to_seg(ctx->prefix), ctx->base, left, left_len,
+                         is_last, nullptr);
+}
+
+// ---- end-to-end from host memory ---------------------------------------------------------------------
+int parpa_parse_host(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *h_bytes, uint64_t len,
+                     const parpa_column *h_cols, uint64_t cap, parpa_stats *stats, void *stream) {
+  if (!dfa || !sch || !stats || (len && !h_bytes)) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint32_t C = sch->num_columns;
+  std::vector<parpa_column> dcols(C);
+  std::vector<size_t> per(C);
+  void *blk = nullptr;
+  size_t total = align_up(len + 16) + align_up(sizeof(Stats));
+  for (uint32_t c = 0; c < C; c++) {
+    uint8_t type = sch->types ? sch->types[c] : PARPA_SPAN;
+    per[c] = align_up(cap * 8) + align_up(cap * 4) + (type != PARPA_SPAN ? align_up(cap * 8) + align_up(cap) : 0);
+    total += per[c];
+  }
+  CK(cudaMallocAsync(&blk, total, s));
+  uint8_t *b = (uint8_t *)blk;
+  uint8_t *d_in = b;
+  b += align_up(len + 16);
+  parpa_stats *d_stats = (parpa_stats *)b;
+  b += align_up(sizeof(Stats));
+  for (uint32_t c = 0; c < C; c++) {
+    uint8_t type = sch->types ? sch->types[c] : PARPA_SPAN;
+    dcols[c].offset = (uint64_t *)b; b += align_up(cap * 8);
+    dcols[c].length = (uint32_t *)b; b += align_up(cap * 4);
+    if (type != PARPA_SPAN) {
+      dcols[c].value = b; b += align_up(cap * 8);
+      dcols[c].valid = b; b += align_up(cap);
+    } else {
+      dcols[c].value = nullptr;
+      dcols[c].valid = nullptr;
+    }
+  }
+  int rc = PARPA_OK;
+  if (len && cudaMemcpyAsync(d_in, h_bytes, len, cudaMemcpyHostToDevice, s) != cudaSuccess) rc = PARPA_ECUDA;
+  if (!rc) rc = parpa_parse_into(dfa, sch, d_in, len, dcols.data(), cap, d_stats, stream, nullptr);
+  Stats hs;
+  if (!rc && cudaMemcpyAsync(&hs, d_stats, sizeof(Stats), cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = PARPA_ECUDA;
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
+  if (!rc) {
+    uint64_t R = std::min<uint64_t>(hs.records, cap);
+    for (uint32_t c = 0; c < C && !rc; c++) {
+      if (!R) break;
+      if (h_cols[c].offset && cudaMemcpyAsync(h_cols[c].offset, dcols[c].offset, R * 8, cudaMemcpyDeviceToHost, s)) rc = PARPA_ECUDA;
+      if (h_cols[c].length && cudaMemcpyAsync(h_cols[c].length, dcols[c].length, R * 4, cudaMemcpyDeviceToHost, s)) rc = PARPA_ECUDA;
+      if (dcols[c].value && h_cols[c].value && cudaMemcpyAsync(h_cols[c].value, dcols[c].value, R * 8, cudaMemcpyDeviceToHost, s)) rc = PARPA_ECUDA;
+      if (dcols[c].valid && h_cols[c].valid && cudaMemcpyAsync(h_cols[c].valid, dcols[c].valid, R, cudaMemcpyDeviceToHost, s)) rc = PARPA_ECUDA;
+    }
+    if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
+    memcpy(stats, &hs, sizeof(hs));
+  }
+  cudaFreeAsync(blk, s);
+  cudaStreamSynchronize(s);
+  return rc;
+}
+
+// ---- range summaries -------------------------------------------------------------------------------
+int parpa_summarize(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, void *stream, parpa_tau *out) {
+  if (!dfa || !out || (len && !d_bytes)) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  Work w;
+  int rc = work_alloc(w, len, 1, len && misaligned(d_bytes), s);
+  if (rc) return rc;
+  const uint8_t *in = d_bytes;
+  rc = prepare_input(w, in, len, s);
+  KArgs a;
+  make_args(a, w, in, len);
+  ColsK ck;
+  memset(&ck, 0, sizeof(ck));
+  if (!rc) rc = launch_scan(MODE_TAU, a, dfa->k, ck, s, nullptr);
+  unsigned long long desc = NIB_IDENT;
+  if (!rc && w.ntiles) {
+    if (cudaMemcpyAsync(&desc, w.tau_desc + (w.ntiles - 1), 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = PARPA_ECUDA;
+  }
+  work_free(w, s);
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
+  if (!rc) host_tau_dfa(dfa, (uint32_t)desc, out);
+  return rc;
+}
+
+int parpa_count(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint64_t base, uint32_t entry,
+                void *stream, parpa_counts *out, parpa_tau *tau_out) {
+  if (!dfa || !out || entry >= dfa->S || (len && !d_bytes)) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  parpa_plan p;
+  int rc = plan_scan(dfa, d_bytes, len, dfa->dmap[entry], seg_identity(), base, 1, s, &p);
+  Seg tot;
+  uint32_t tau = NIB_IDENT;
+  uint64_t fi = NONE;
+  if (!rc) rc = plan_totals(&p, tot, tau, fi);
+  work_free(p.w, s);
+  if (!rc) {
+    *out = seg_to_counts(tot, fi);
+    if (tau_out) host_tau_dfa(dfa, tau, tau_out);
+  }
+  return rc;
+}
+
+int parpa_compose_tau(const parpa_dfa *dfa, const parpa_tau *a, const parpa_tau *b, parpa_tau *out) {
+  if (!dfa || !a || !b || !out) return PARPA_EINVAL;
+  parpa_tau r;
+  for (int i = 0; i < 16; i++) r.tau[i] = 0xFF;
+  for (uint32_t i = 0; i < dfa->S; i++) {
+    if (a->tau[i] >= dfa->S) return PARPA_EINVAL;
+    r.tau[i] = b->tau[a->tau[i]];                 // (a∘b)_i = b_{a_i}
+  }
+  *out = r;
+  return PARPA_OK;
+}
+
+int parpa_compose_counts(const parpa_counts *a, const parpa_counts *b, parpa_counts *out) {
+  if (!a || !b || !out) return PARPA_EINVAL;
+  Seg c = seg_op(counts_to_seg(*a), counts_to_seg(*b));
+  *out = seg_to_counts(c, std::min(a->first_invalid, b->first_invalid));
+  return PARPA_OK;
+}
+
+// ---- debug ----------------------------------------------------------------------------------------
+int parpa_debug_trace(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint8_t *d_chunk_states,
+                      uint8_t *d_kinds, uint8_t *d_states, void *stream) {
+  if (!dfa || (len && !d_bytes)) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  parpa_plan p;
+  int rc = plan_scan(dfa, d_bytes, len, dfa->dmap[dfa->start], seg_identity(), 0, 1, s, &p);
+  if (!rc && len) {
+    k_debug_trace<<<1024, 128, 0, s>>>(p.a, dfa->k, d_chunk_states, d_kinds, d_states);
+    if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
+  }
+  work_free(p.w, s);
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
+  return rc;
+}
+
+}  // extern "C"

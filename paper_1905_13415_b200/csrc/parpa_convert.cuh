@@ -1,0 +1,317 @@
+// parpa_convert.cuh — type conversion of field values on the device.
+//
+// Thread tier (inside the emit kernels): int64 exact; float64 by Clinger's fast path — with at
+// most 19 significant digits m <= 2^53 and a decimal exponent |e| <= 22, the value m·10^e is one
+// correctly rounded IEEE division or multiplication of two exact doubles.  Everything else is
+// deferred to the device tier (k_deferred), which runs an exact decimal-to-binary algorithm: the
+// digits are held as a decimal (up to 800 digits + a "truncated nonzero" flag), scaled by powers
+// of two until they lie in [1/2, 1), shifted by 53 bits and rounded half-to-even.  That is the
+// "simple decimal conversion" scheme (as in Go's strconv); it is exact for every input.
+// Grammar (reading R15): [+-]?([0-9]+(\.[0-9]*)?|\.[0-9]+)([eE][+-]?[0-9]+)?; int64 (R14):
+// [+-]?[0-9]+ within [-2^63, 2^63-1].  Sources yield the field's DATA bytes one at a time.
+#pragma once
+#include <stdint.h>
+
+namespace parpa {
+
+__constant__ double c_pow10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
+                                   1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
+
+// returns 1 valid, 0 invalid
+template <class Src>
+__device__ int conv_int64(Src &s, long long &out) {
+  uint8_t c;
+  if (!s.next(c)) return 0;
+  bool neg = false;
+  if (c == '+' || c == '-') {
+    neg = c == '-';
+    if (!s.next(c)) return 0;
+  }
+  unsigned long long acc = 0;
+  int nsig = 0;
+  while (true) {
+    unsigned d = (unsigned)c - '0';
+    if (d > 9) return 0;
+    if (nsig || d) {
+      if (++nsig > 19) return 0;                 // >= 10^19 > 2^63: overflow
+      acc = acc * 10ull + d;
+    }
+    if (!s.next(c)) break;
+  }
+  unsigned long long lim = neg ? 0x8000000000000000ull : 0x7FFFFFFFFFFFFFFFull;
+  if (acc > lim) return 0;
+  out = neg ? (long long)(0ull - acc) : (long long)acc;
+  return 1;
+}
+
+// returns 1 valid (bits set), 0 invalid grammar, 2 valid but outside the exact fast path
+template <class Src>
+__device__ int conv_float64_fast(Src &s, long long &bits) {
+  uint8_t c;
+  bool more = s.next(c);
+  if (!more) return 0;
+  bool neg = false;
+  if (c == '+' || c == '-') {
+    neg = c == '-';
+    more = s.next(c);
+  }
+  unsigned long long m = 0;
+  int nsig = 0, e10 = 0, ndig = 0;
+  bool dropped = false;
+  while (more && (unsigned)(c - '0') <= 9u) {
+    unsigned d = c - '0';
+    ndig++;
+    if (nsig || d) {
+      if (nsig < 19) { m = m * 10ull + d; nsig++; }
+      else { e10++; dropped |= d != 0; }
+    }
+    more = s.next(c);
+  }
+  if (more && c == '.') {
+    more = s.next(c);
+    while (more && (unsigned)(c - '0') <= 9u) {
+      unsigned d = c - '0';
+      ndig++;
+      if (nsig || d) {
+        if (nsig < 19) { m = m * 10ull + d; nsig++; e10--; }
+        else dropped |= d != 0;
+      } else {
+        e10--;
+      }
+      more = s.next(c);
+    }
+  }
+  if (ndig == 0) return 0;
+  if (more && (c == 'e' || c == 'E')) {
+    bool eneg = false;
+    int ex = 0, nex = 0;
+    more = s.next(c);
+    if (more && (c == '+' || c == '-')) {
+      eneg = c == '-';
+      more = s.next(c);
+    }
+    while (more && (unsigned)(c - '0') <= 9u) {
+      if (ex < 100000) ex = ex * 10 + (c - '0');
+      nex++;
+      more = s.next(c);
+    }
+    if (nex == 0) return 0;
+    e10 += eneg ? -ex : ex;
+  }
+  if (more) return 0;                             // trailing bytes outside the grammar
+  if (m == 0) {
+    bits = neg ? (long long)0x8000000000000000ull : 0;
+    return 1;
+  }
+  if (dropped || m > (1ull << 53) || e10 < -22 || e10 > 22) return 2;
+  double v = (double)m;
+  v = e10 < 0 ? __ddiv_rn(v, c_pow10[-e10]) : __dmul_rn(v, c_pow10[e10]);
+  if (neg) v = -v;
+  bits = __double_as_longlong(v);
+  return 1;
+}
+
+// ---- exact slow path ------------------------------------------------------------------------
+constexpr int DEC_MAX = 800;
+struct Decimal {
+  uint8_t d[DEC_MAX];            // digit values 0..9, most significant first; value = 0.d × 10^dp
+  int nd, dp;
+  bool neg, trunc;
+};
+
+__device__ inline void dec_trim(Decimal &a) {
+  while (a.nd > 0 && a.d[a.nd - 1] == 0) a.nd--;
+  if (a.nd == 0) a.dp = 0;
+}
+
+__device__ inline void dec_rshift(Decimal &a, int k) {          // divide by 2^k, k <= 60
+  int r = 0, w = 0;
+  unsigned long long n = 0;
+  for (; (n >> k) == 0; r++) {
+    if (r >= a.nd) {
+      if (n == 0) { a.nd = 0; return; }
+      while ((n >> k) == 0) { n = n * 10; r++; }
+      break;
+    }
+    n = n * 10 + a.d[r];
+  }
+  a.dp -= r - 1;
+  unsigned long long mask = (1ull << k) - 1;
+  for (; r < a.nd; r++) {
+    unsigned long long dig = n >> k;
+    n &= mask;
+    a.d[w++] = (uint8_t)dig;
+    n = n * 10 + a.d[r];
+  }
+  while (n > 0) {
+    unsigned long long dig = n >> k;
+    n &= mask;
+    if (w < DEC_MAX) a.d[w++] = (uint8_t)dig;
+    else if (dig > 0) a.trunc = true;
+    n = n * 10;
+  }
+  a.nd = w;
+  dec_trim(a);
+}
+
+__device__ inline void dec_lshift(Decimal &a, int k) {          // multiply by 2^k, k <= 60
+  uint8_t t[DEC_MAX + 24];
+  int w = DEC_MAX + 24;
+  unsigned long long n = 0;
+  for (int r = a.nd - 1; r >= 0; r--) {
+    n += (unsigned long long)a.d[r] << k;
+    unsigned long long q = n / 10;
+    t[--w] = (uint8_t)(n - 10 * q);
+    n = q;
+  }
+  while (n > 0) {
+    unsigned long long q = n / 10;
+    t[--w] = (uint8_t)(n - 10 * q);
+    n = q;
+  }
+  int newnd = DEC_MAX + 24 - w;
+  int delta = newnd - a.nd;
+  int cnt = newnd < DEC_MAX ? newnd : DEC_MAX;
+  for (int i = 0; i < cnt; i++) a.d[i] = t[w + i];
+  for (int i = cnt; i < newnd; i++)
+    if (t[w + i]) a.trunc = true;
+  a.nd = cnt;
+  a.dp += delta;
+  dec_trim(a);
+}
+
+__device__ inline void dec_shift(Decimal &a, int k) {
+  if (a.nd == 0) return;
+  if (k > 0) {
+    while (k > 60) { dec_lshift(a, 60); k -= 60; }
+    dec_lshift(a, k);
+  } else if (k < 0) {
+    while (k < -60) { dec_rshift(a, 60); k += 60; }
+    dec_rshift(a, -k);
+  }
+}
+
+__device__ inline bool dec_round_up(const Decimal &a, int nd) {
+  if (nd < 0 || nd >= a.nd) return false;
+  if (a.d[nd] == 5 && nd + 1 == a.nd) {          // exactly halfway -> round to even
+    if (a.trunc) return true;
+    return nd > 0 && (a.d[nd - 1] & 1);
+  }
+  return a.d[nd] >= 5;
+}
+
+__device__ inline unsigned long long dec_rounded_integer(const Decimal &a) {
+  if (a.dp > 20) return 0xFFFFFFFFFFFFFFFFull;
+  int i;
+  unsigned long long n = 0;
+  for (i = 0; i < a.dp && i < a.nd; i++) n = n * 10 + a.d[i];
+  for (; i < a.dp; i++) n *= 10;
+  if (dec_round_up(a, a.dp)) n++;
+  return n;
+}
+
+__device__ inline unsigned long long dec_float_bits(Decimal &a) {
+  const int mantbits = 52, bias = -1023;
+  const int powtab[9] = {1, 3, 6, 9, 13, 16, 19, 23, 26};
+  int exp = 0;
+  unsigned long long mant = 0;
+  bool overflow = false;
+  if (a.nd == 0) { exp = bias; goto out; }
+  if (a.dp > 310) { overflow = true; goto out; }
+  if (a.dp < -330) { exp = bias; goto out; }
+  while (a.dp > 0) {
+    int n = a.dp >= 9 ? 27 : powtab[a.dp];
+    dec_shift(a, -n);
+    exp += n;
+  }
+  while (a.dp < 0 || (a.dp == 0 && a.d[0] < 5)) {
+    int n = -a.dp >= 9 ? 27 : powtab[-a.dp];
+    dec_shift(a, n);
+    exp -= n;
+  }
+  exp--;                                           // range [0.5, 1) -> [1, 2)
+  if (exp < bias + 1) {
+    int n = bias + 1 - exp;
+    dec_shift(a, -n);
+    exp += n;
+  }
+  if (exp - bias >= (1 << 11) - 1) { overflow = true; goto out; }
+  dec_shift(a, 1 + mantbits);
+  mant = dec_rounded_integer(a);
+  if (mant == (2ull << mantbits)) {
+    mant >>= 1;
+    exp++;
+    if (exp - bias >= (1 << 11) - 1) { overflow = true; goto out; }
+  }
+  if ((mant & (1ull << mantbits)) == 0) exp = bias;  // denormal
+out:
+  if (overflow) { mant = 0; exp = (1 << 11) - 1 + bias; }
+  unsigned long long b = mant & ((1ull << mantbits) - 1);
+  b |= (unsigned long long)((exp - bias) & ((1 << 11) - 1)) << mantbits;
+  if (a.neg) b |= 1ull << 63;
+  return b;
+}
+
+// exact float64 from any valid grammar; returns 1 / 0
+template <class Src>
+__device__ int conv_float64_exact(Src &s, long long &bits) {
+  Decimal a;
+  a.nd = 0; a.dp = 0; a.neg = false; a.trunc = false;
+  uint8_t c;
+  bool more = s.next(c);
+  if (!more) return 0;
+  if (c == '+' || c == '-') {
+    a.neg = c == '-';
+    more = s.next(c);
+  }
+  bool sawdot = false, sawdigits = false;
+  long long ntot = 0;                              // significant digits seen (stored or not)
+  long long dp = 0;
+  while (more) {
+    if (c == '.') {
+      if (sawdot) return 0;
+      sawdot = true;
+      dp = ntot;
+    } else if ((unsigned)(c - '0') <= 9u) {
+      sawdigits = true;
+      if (c == '0' && ntot == 0) {
+        dp--;                                      // leading zero (matters only after the point)
+      } else {
+        if (a.nd < DEC_MAX) a.d[a.nd++] = (uint8_t)(c - '0');
+        else if (c != '0') a.trunc = true;
+        ntot++;
+      }
+    } else {
+      break;
+    }
+    more = s.next(c);
+  }
+  if (!sawdigits) return 0;
+  if (!sawdot) dp = ntot;
+  if (more && (c == 'e' || c == 'E')) {
+    bool eneg = false;
+    long long ex = 0;
+    int nex = 0;
+    more = s.next(c);
+    if (more && (c == '+' || c == '-')) {
+      eneg = c == '-';
+      more = s.next(c);
+    }
+    while (more && (unsigned)(c - '0') <= 9u) {
+      if (ex < 100000) ex = ex * 10 + (c - '0');
+      nex++;
+      more = s.next(c);
+    }
+    if (nex == 0) return 0;
+    dp += eneg ? -ex : ex;
+  }
+  if (more) return 0;
+  if (dp > 100000) dp = 100000;
+  if (dp < -100000) dp = -100000;
+  a.dp = (int)dp;
+  dec_trim(a);
+  bits = (long long)dec_float_bits(a);
+  return 1;
+}
+
+}  // namespace parpa

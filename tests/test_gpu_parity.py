@@ -1,0 +1,231 @@
+"""GPU parity: the CUDA path (through the C ABI) against the sequential oracle, element by element.
+
+Bar: bit-exact for states, emission kinds, offsets, lengths, counts and int64 values; 0 ulp
+(bitwise) for float64 values (BASELINE north_star).
+"""
+import itertools
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from tests.gpu_helpers import compare, to_np
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import paper_1905_13415_b200 as parpa  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+DIALECT_OF = {"cfg1": "csv", "taxi": "csv", "yelp": "csv", "clf": "clf"}
+_DFA = {}
+
+
+def dfa(name):
+    if name not in _DFA:
+        _DFA[name] = parpa.Dfa.dialect(name)
+    return _DFA[name]
+
+
+def dev(data):
+    a = np.frombuffer(bytes(data), np.uint8) if isinstance(data, (bytes, bytearray)) else np.asarray(data, np.uint8)
+    t = torch.empty(max(a.size, 1), dtype=torch.uint8, device="cuda")
+    if a.size:
+        t[:a.size].copy_(torch.from_numpy(a.copy()))
+    return t[:a.size]
+
+
+def run_all_paths(dialect, data, types, defaults=None, strict=False, label=""):
+    schema = parpa.Schema(list(types), defaults, strict)
+    ora = oracle.parse(dialect, data, len(types), list(types), defaults, strict)
+    d = dev(data)
+    res = parpa.parse(dfa(dialect), schema, d)                 # two-phase (scan + emit)
+    compare(res, ora, types, label + "/plan")
+    cap = max(ora.R, 1) + 3
+    cols = parpa.alloc_columns(schema, cap)
+    st = parpa.new_stats_tensor()
+    parpa.parse_into(dfa(dialect), schema, d, cols, cap, st)   # fused single pass
+    compare(parpa.ParseResult(cols, parpa.stats_from_tensor(st)), ora, types, label + "/fused")
+    res3 = parpa.parse_c_owned(dfa(dialect), schema, d)        # library-owned result
+    compare(res3, ora, types, label + "/owned")
+    return ora
+
+
+def test_smoke_cfg1_small():
+    data, g = datagen.generate("cfg1", 50_000)
+    w = datagen.WORKLOADS["cfg1"]
+    ora = run_all_paths("csv", data, w.types, label="cfg1-50k")
+    assert ora.R == g.records
+
+
+@pytest.mark.parametrize("name", ["cfg1", "taxi", "yelp", "clf"])
+def test_workload_slices_full_compare(name):
+    w = datagen.WORKLOADS[name]
+    data, g = datagen.generate(name, 3_000_000 if name != "cfg1" else 1_000_000)
+    ora = run_all_paths(w.dialect, data, w.types, label=name)
+    assert ora.R == g.records
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 63, 64, 65, 127, 4095, 16383, 16384, 16385, 16384 * 3 + 17, 200_003])
+def test_ragged_sizes(n):
+    data, _ = datagen.generate("cfg1", 400_000)
+    run_all_paths("csv", data[:n], datagen.WORKLOADS["cfg1"].types, label=f"n={n}")
+
+
+def test_golden_fixtures_on_gpu():
+    fx = json.load(open(os.path.join(GOLD, "fixtures.json")))
+    for dialect, cases in fx.items():
+        if dialect == "source":
+            continue
+        for case in cases:
+            C = case["C"]
+            types = [oracle.SPAN] * C
+            if dialect == "clf":
+                types[5] = types[6] = oracle.INT64
+            run_all_paths(dialect, case["input"].encode(), types, label=case["cite"][:30])
+
+
+ALPH = [b"\n", b'"', b",", b"a"]
+
+
+def test_bruteforce_corpus_trace_and_outputs():
+    # every string of length <= 6 over {\n, ", ",", a}, each closed with '\n' and concatenated into one
+    # corpus (so chunk and tile boundaries fall everywhere); per-chunk entry states and per-byte kinds
+    # and states must equal the oracle's sequential trace.
+    parts = []
+    for n in range(7):
+        for t in itertools.product(ALPH, repeat=n):
+            parts.append(b"".join(t) + b"\n")
+    data = b"".join(parts)
+    ora = oracle.parse("csv", data, 4, trace=True)
+    cs, kinds, states = parpa.debug_trace(dfa("csv"), dev(data))
+    cb = parpa.chunk_bytes()
+    starts = np.arange(0, len(data), cb)
+    assert np.array_equal(to_np(cs), ora.trace_state[starts])
+    assert np.array_equal(to_np(kinds), ora.trace_kind)
+    assert np.array_equal(to_np(states), ora.trace_state)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "yelp", "clf"])
+def test_trace_on_workloads(name):
+    w = datagen.WORKLOADS[name]
+    data, _ = datagen.generate(name, 2_000_000)
+    ora = oracle.parse(w.dialect, data, w.C, trace=True)
+    cs, kinds, states = parpa.debug_trace(dfa(w.dialect), dev(data))
+    cb = parpa.chunk_bytes()
+    assert np.array_equal(to_np(cs), ora.trace_state[np.arange(0, len(data), cb)])
+    assert np.array_equal(to_np(kinds), ora.trace_kind)
+    assert np.array_equal(to_np(states), ora.trace_state)
+
+
+def random_dfa(rng, S):
+    inv = S - 1
+    G = rng.randint(2, 8)
+    trans = [[rng.randrange(S) for _ in range(S - 1)] + [inv] for _ in range(G)]
+    emit = [[rng.randrange(4) for _ in range(S - 1)] + [1] for _ in range(G)]
+    eoi = [rng.randrange(3) for _ in range(S)]
+    gob = [rng.randrange(G) for _ in range(256)]
+    return {"group_of_byte": gob, "transition": trans, "emit": emit, "eoi": eoi,
+            "start": rng.randrange(S - 1), "invalid": inv}
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_dfas(seed):
+    # random DFAs (|S| <= 9 with an absorbing invalid state), random start state.
+    rng = random.Random(seed)
+    S = rng.randint(2, 9)
+    t = random_dfa(rng, S)
+    d = parpa.Dfa(S, t["start"], t["invalid"], t["group_of_byte"], t["transition"], t["emit"], t["eoi"])
+    n = rng.choice([100, 5000, 70_000])
+    # bias bytes towards a few values so that every group occurs
+    vals = [rng.randrange(256) for _ in range(6)]
+    data = bytes(rng.choice(vals) if rng.random() < 0.7 else rng.randrange(256) for _ in range(n))
+    ora = oracle.parse_tables(t, data, 3, trace=True)
+    cs, kinds, states = parpa.debug_trace(d, dev(data))
+    cb = parpa.chunk_bytes()
+    assert np.array_equal(to_np(cs), ora.trace_state[np.arange(0, len(data), cb)])
+    assert np.array_equal(to_np(kinds), ora.trace_kind)
+    assert np.array_equal(to_np(states), ora.trace_state)
+    schema = parpa.Schema([parpa.SPAN] * 3)
+    res = parpa.parse(d, schema, dev(data))
+    compare(res, ora, [0, 0, 0], f"rand{seed}")
+
+
+def test_float_and_int_hard_cases_device_tier():
+    # the fast path defers these to the exact decimal algorithm (k_deferred)
+    vals = [b"0.3", b"-0.00", b"9007199254740993", b"2.2250738585072011e-308", b"1e23",
+            b"4.9406564584124654e-324", b"1e400", b"-1e400", b"1e-400", b".5", b"5.", b"12.5",
+            b"123456789012345678901234567890", b"0.1e0000000000000000000000000001", b"1" + b"0" * 400,
+            b"0." + b"0" * 300 + b"1", b"179769313486231580793728971405301e276", b"2.4703282292062327e-324",
+            b"2.4703282292062328e-324", b"1.7976931348623157e308", b"1.7976931348623158e308", b"3.14159265358979323846",
+            b"1e", b"e5", b"--1", b"", b"nan", b"1_0"]
+    ints = [b"9223372036854775807", b"-9223372036854775808", b"9223372036854775808", b"00000000000000000000007",
+            b"+5", b"-", b"1.0", b"-0"]
+    rows = []
+    rng = random.Random(4)
+    for i in range(3000):
+        f = vals[i % len(vals)] if i < 600 else (str(rng.randint(0, 10**25)).encode() + b"." +
+                                                 str(rng.randint(0, 10**12)).encode() +
+                                                 (b"e" + str(rng.randint(-340, 310)).encode() if i % 3 else b""))
+        rows.append(f + b"," + ints[i % len(ints)] + b"\n")
+    data = b"".join(rows)
+    run_all_paths("csv", data, [oracle.FLOAT64, oracle.INT64], label="numbers")
+
+
+def test_quoted_numbers_with_inner_quotes():
+    # a typed field whose raw span holds control bytes ('""' inside quotes) goes through the
+    # re-simulating device tier; DATA bytes '1"2' are not a number -> null, same as the oracle
+    data = b'"1""2",3\n"4",""\n"-7","8e1"\n5,"""6"""\n'
+    run_all_paths("csv", data, [oracle.INT64, oracle.FLOAT64], label="inner-quotes")
+
+
+def test_defaults_strict_and_columns():
+    data = b"1,\n,2.5\n7\n1,2,3\n"
+    run_all_paths("csv", data, [oracle.INT64, oracle.FLOAT64], defaults=[-1, 0.25], label="defaults")
+    run_all_paths("csv", data, [oracle.INT64, oracle.FLOAT64], strict=True, label="strict")
+
+
+def test_format_errors_first_invalid():
+    for s in [b'"x"y\n', b'"abc', b'"a"\r\n', b'a"b\n', b"ok,1\n" * 5000 + b'a"b\n' + b"x\n" * 100]:
+        run_all_paths("csv", s, [oracle.SPAN], label=repr(s[:10]))
+
+
+def test_capacity_needmore():
+    data, _ = datagen.generate("cfg1", 100_000)
+    w = datagen.WORKLOADS["cfg1"]
+    schema = parpa.Schema(list(w.types))
+    ora = oracle.parse("csv", data, w.C, w.types)
+    cols = parpa.alloc_columns(schema, 10)
+    st = parpa.new_stats_tensor()
+    parpa.parse_into(dfa("csv"), schema, dev(data), cols, 10, st)
+    s = parpa.stats_from_tensor(st)
+    assert s["status"] == parpa.ENEEDMORE and s["records"] == ora.R
+    assert np.array_equal(to_np(cols[0].offset).view(np.uint64)[:10], ora.offset[0][:10])
+
+
+def test_misaligned_input_pointer():
+    data, _ = datagen.generate("yelp", 500_000)
+    buf = dev(b"x" + bytes(data))
+    w = datagen.WORKLOADS["yelp"]
+    schema = parpa.Schema(list(w.types))
+    ora = oracle.parse("csv", data, w.C, w.types)
+    res = parpa.parse(dfa("csv"), schema, buf[1:])
+    compare(res, ora, w.types, "misaligned")
+
+
+def test_parse_host_end_to_end():
+    data, _ = datagen.generate("taxi", 1_000_000)
+    w = datagen.WORKLOADS["taxi"]
+    ora = oracle.parse("csv", data, w.C, w.types)
+    stats, cols = parpa.parse_host(dfa("csv"), parpa.Schema(list(w.types)), data, ora.R + 1)
+    assert stats["status"] == 0 and stats["records"] == ora.R
+    for c, t in enumerate(w.types):
+        assert np.array_equal(cols[c][0], ora.offset[c])
+        assert np.array_equal(cols[c][1], ora.length[c])
+        if t != oracle.SPAN:
+            assert np.array_equal(cols[c][3], ora.valid[c])
+            assert np.array_equal(cols[c][2].view(np.int64), ora.value[c])
