@@ -106,13 +106,13 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def gen_range(config, rank, world, pin=True):
+def gen_range(config, rank, world, pin=True, records=0):
     """This rank's byte range of the logical input (host, pinned) + its left context and base."""
     import torch
     import datagen
     w = datagen.WORKLOADS[config]
-    rb = RECORDS_PER_RANK[config]
-    cap = BYTES_CAP[config] + (1 << 20)
+    rb = records or RECORDS_PER_RANK[config]
+    cap = BYTES_CAP[config] + (1 << 20) if not records else records * 4096
     cut = lambda g: 0 if g == 0 else 37 + 11 * g              # mid-record cut points
     host = torch.empty(cap + (1 << 20), dtype=torch.uint8, pin_memory=pin)
     g0 = datagen.fill(w, host.data_ptr(), cap, first_record=rank * rb, max_records=rb)
@@ -195,6 +195,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--ref-sample-bytes", type=int, default=150_000_000)
+    ap.add_argument("--records", type=int, default=0, help="override records per rank (profiling runs)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -218,7 +219,7 @@ def main():
     schema = parpa.Schema(list(w.types))
 
     t_gen = time.time()
-    data_host, left_host, block_len, cut0, g = gen_range(args.config, rank, world)
+    data_host, left_host, block_len, cut0, g = gen_range(args.config, rank, world, records=args.records)
     t_gen = time.time() - t_gen
     n = data_host.numel()
     d = torch.empty(n + 64, dtype=torch.uint8, device="cuda")[:n]

@@ -87,10 +87,13 @@ class Dfa:
         return self._h
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib._lib is not None:
-            _lib._lib.parpa_destroy_dfa(h)
-            self._h = None
+        try:
+            h = getattr(self, "_h", None)
+            if h is not None and h.value and _lib._lib is not None:
+                _lib._lib.parpa_destroy_dfa(h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
 
 @dataclass

@@ -58,14 +58,14 @@ int dev_cfg(DevCfg **out) {
   DevCfg &c = g_dev[dev];
   if (!c.init) {
     CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaFuncSetAttribute(k_scan<MODE_TAU>, cudaFuncAttributeMaxDynamicSharedMemorySize, LUT_BYTES));
-    CK(cudaFuncSetAttribute(k_scan<MODE_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, LUT_BYTES));
-    CK(cudaFuncSetAttribute(k_scan<MODE_EMIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, LUT_BYTES));
-    CK(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, LUT_BYTES));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[0], k_scan<MODE_TAU>, THREADS, LUT_BYTES));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[1], k_scan<MODE_COUNT>, THREADS, LUT_BYTES));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[2], k_scan<MODE_EMIT>, THREADS, LUT_BYTES));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit, THREADS, LUT_BYTES));
+    CK(cudaFuncSetAttribute(k_scan<MODE_TAU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ScanCfg<MODE_TAU>::SMEM));
+    CK(cudaFuncSetAttribute(k_scan<MODE_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ScanCfg<MODE_COUNT>::SMEM));
+    CK(cudaFuncSetAttribute(k_scan<MODE_EMIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ScanCfg<MODE_EMIT>::SMEM));
+    CK(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[0], k_scan<MODE_TAU>, ScanCfg<MODE_TAU>::THREADS, ScanCfg<MODE_TAU>::SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[1], k_scan<MODE_COUNT>, ScanCfg<MODE_COUNT>::THREADS, ScanCfg<MODE_COUNT>::SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[2], k_scan<MODE_EMIT>, ScanCfg<MODE_EMIT>::THREADS, ScanCfg<MODE_EMIT>::SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit, EMIT_WARPS * 32, EMIT_SMEM));
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;
@@ -134,7 +134,7 @@ struct Work {
 };
 
 int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cudaStream_t s) {
-  uint64_t nt64 = (len + TILE - 1) / TILE;
+  uint64_t nt64 = (len + PTILE - 1) / PTILE;
   if (nt64 > 0xFFFFFFF0ull) return PARPA_EUNSUPPORTED;
   w.ntiles = (uint32_t)nt64;
   size_t nt = std::max<size_t>(w.ntiles, 1);
@@ -146,8 +146,8 @@ int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cu
   size_t zero = o;
   size_t o_agg = o; o = align_up(o + nt * sizeof(Seg));
   size_t o_incl = o; o = align_up(o + nt * sizeof(Seg));
-  size_t o_tinfo = o; o = align_up(o + nt * sizeof(TileInfo));
-  size_t o_cs = o; o = align_up(o + nt * THREADS);
+  size_t o_tinfo = o; o = align_up(o + nt * CW * sizeof(TileInfo));
+  size_t o_cs = o; o = align_up(o + nt * CW * 32);
   size_t o_dq = o; o = align_up(o + (size_t)w.dq_cap * sizeof(DeferItem));
   size_t o_st = o; o = align_up(o + sizeof(Stats));
   size_t o_in = o; if (need_aligned_copy) o = align_up(o + len);
@@ -231,9 +231,10 @@ int set_columns(const parpa_schema *sch, const parpa_column *cols, uint32_t C, C
   return PARPA_OK;
 }
 
-int grid_for(int occ, int sms, uint32_t ntiles) {
+int grid_for(int occ, int sms, uint32_t ntiles, int warps_per_cta) {
   long long g = (long long)std::max(occ, 1) * sms;
-  return (int)std::max<long long>(1, std::min<long long>(g, ntiles));
+  long long need = ((long long)ntiles + warps_per_cta - 1) / warps_per_cta;
+  return (int)std::max<long long>(1, std::min<long long>(g, need));
 }
 
 int launch_scan(int mode, const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, uint32_t *launches) {
@@ -241,12 +242,18 @@ int launch_scan(int mode, const KArgs &a, const DfaK &k, const ColsK &ck, cudaSt
   DevCfg *dc;
   int rc = dev_cfg(&dc);
   if (rc) return rc;
-  int g = grid_for(dc->occ_scan[mode], dc->sms, a.ntiles);
   {
     Launch L(s, mode == MODE_EMIT ? "k_scan_emit" : mode == MODE_COUNT ? "k_scan_count" : "k_scan_tau");
-    if (mode == MODE_TAU) k_scan<MODE_TAU><<<g, THREADS, LUT_BYTES, s>>>(a, k, ck);
-    else if (mode == MODE_COUNT) k_scan<MODE_COUNT><<<g, THREADS, LUT_BYTES, s>>>(a, k, ck);
-    else k_scan<MODE_EMIT><<<g, THREADS, LUT_BYTES, s>>>(a, k, ck);
+    if (mode == MODE_TAU) {
+      int g = grid_for(dc->occ_scan[0], dc->sms, a.ntiles, 1);
+      k_scan<MODE_TAU><<<g, ScanCfg<MODE_TAU>::THREADS, ScanCfg<MODE_TAU>::SMEM, s>>>(a, k, ck);
+    } else if (mode == MODE_COUNT) {
+      int g = grid_for(dc->occ_scan[1], dc->sms, a.ntiles, 1);
+      k_scan<MODE_COUNT><<<g, ScanCfg<MODE_COUNT>::THREADS, ScanCfg<MODE_COUNT>::SMEM, s>>>(a, k, ck);
+    } else {
+      int g = grid_for(dc->occ_scan[2], dc->sms, a.ntiles, 1);
+      k_scan<MODE_EMIT><<<g, ScanCfg<MODE_EMIT>::THREADS, ScanCfg<MODE_EMIT>::SMEM, s>>>(a, k, ck);
+    }
   }
   if (launches) (*launches)++;
   CK(cudaGetLastError());
@@ -303,7 +310,7 @@ extern "C" {
 
 const char *parpa_version(void) { return "parpa 0.1 (sm_100a, dense LUT path)"; }
 uint32_t parpa_chunk_bytes(void) { return CHUNK; }
-uint32_t parpa_tile_bytes(void) { return TILE; }
+uint32_t parpa_tile_bytes(void) { return PTILE; }
 
 const char *parpa_status_string(int st) {
   switch (st) {
@@ -481,10 +488,10 @@ int parpa_plan_emit(parpa_plan *p, const parpa_schema *sch, const parpa_column *
   if (a.ntiles) {
     DevCfg *dc;
     if ((rc = dev_cfg(&dc))) return rc;
-    int g = grid_for(dc->occ_emit, dc->sms, a.ntiles);
+    int g = grid_for(dc->occ_emit, dc->sms, a.ntiles * CW, EMIT_WARPS);
     {
       Launch L(s, "k_emit");
-      k_emit<<<g, THREADS, LUT_BYTES, s>>>(a, p->dfa->k, ck);
+      k_emit<<<g, EMIT_WARPS * 32, EMIT_SMEM, s>>>(a, p->dfa->k, ck);
     }
     CK(cudaGetLastError());
   }

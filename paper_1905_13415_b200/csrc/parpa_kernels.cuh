@@ -91,7 +91,7 @@ struct KArgs {
   uint32_t *seg_flag;                // [ntiles]
   Seg *seg_agg, *seg_incl;           // [ntiles]
   TileInfo *tinfo;                   // [ntiles]
-  uint8_t *chunk_state;              // [ntiles * THREADS] device entry state of each chunk
+  uint8_t *chunk_state;              // [ntiles * 32] device entry state of each chunk
   Ctrl *ctrl;
   DeferItem *dq;
   uint32_t dq_cap, strict;
@@ -102,7 +102,7 @@ constexpr uint32_t FLAG_AGG = 1, FLAG_INCL = 2;
 
 // ---- shared-memory LUT ------------------------------------------------------------------------
 __device__ __forceinline__ void build_lut(uint8_t *lut, const DfaK &d) {
-  for (int i = threadIdx.x; i < 256 * 32; i += THREADS) {
+  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
     int b = i >> 5, half = (i >> 4) & 1, slot = i & 15;
     uint2 v = half ? make_uint2(d.lut[b][2], d.lut[b][3]) : make_uint2(d.lut[b][0], d.lut[b][1]);
     *reinterpret_cast<uint2 *>(lut + b * 256 + half * 128 + slot * 8) = v;
@@ -202,17 +202,10 @@ __device__ int first_inv_in_chunk(const uint8_t *lut, const uint8_t *p, int nval
   return -1;
 }
 
-// ---- CTA-level τ scan (exclusive per thread, aggregate per tile) ---------------------------------
-struct TauScanSmem {
-  uint32_t wtot[WARPS];
-  uint32_t wpre[WARPS];
-  uint32_t agg;
-  uint32_t prefix;
-  uint32_t tile;
-};
-
-__device__ __forceinline__ uint32_t cta_scan_tau(uint32_t t0, uint32_t t1, TauScanSmem &sm) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// ---- warp-level τ scan (a warp tile = 32 chunks) ------------------------------------------------
+// returns the lane's exclusive prefix; *agg = the warp tile's aggregate
+__device__ __forceinline__ uint32_t warp_scan_tau(uint32_t t0, uint32_t t1, uint32_t &agg) {
+  const int lane = threadIdx.x & 31;
   uint32_t inc = pack_nib(t0, t1), b0 = t0, b1 = t1;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -223,23 +216,26 @@ __device__ __forceinline__ uint32_t cta_scan_tau(uint32_t t0, uint32_t t1, TauSc
       inc = pack_nib(n0, n1);
     }
   }
+  agg = __shfl_sync(0xffffffffu, inc, 31);
   uint32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
-  if (lane == 0) ex = NIB_IDENT;
-  if (lane == 31) sm.wtot[warp] = inc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t p = NIB_IDENT;
-    for (int w = 0; w < WARPS; w++) {
-      sm.wpre[w] = p;
-      p = compose_nib(p, sm.wtot[w]);
-    }
-    sm.agg = p;
-  }
-  __syncthreads();
-  return compose_nib(sm.wpre[warp], ex);
+  return lane == 0 ? NIB_IDENT : ex;
 }
 
-// ---- decoupled look-back over τ (warp 0) ---------------------------------------------------------
+// ---- warp-level SegT scan -----------------------------------------------------------------------
+__device__ __forceinline__ SegT warp_scan_segt(SegT s, SegT &agg) {            // exclusive
+  const int lane = threadIdx.x & 31;
+  SegT inc = s;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    SegT o = shfl_up_segt(inc, d);
+    if (lane >= d) inc = segt_op(o, inc);
+  }
+  agg = shfl_segt(inc, 31);
+  SegT ex = shfl_up_segt(inc, 1);
+  return lane == 0 ? segt_ident() : ex;
+}
+
+// ---- decoupled look-back over τ (one warp) ---------------------------------------------------------
 // returns the exclusive prefix τ_0 ∘ ... ∘ τ_{t-1} of tile t (identity for t == 0)
 __device__ uint32_t lookback_tau(const KArgs &a, uint32_t t) {
   const int lane = threadIdx.x & 31;
@@ -272,56 +268,7 @@ __device__ uint32_t lookback_tau(const KArgs &a, uint32_t t) {
   return acc;
 }
 
-// ---- CTA-level SegT reduce / scan --------------------------------------------------------------
-struct SegScanSmem {
-  SegT wtot[WARPS];
-  SegT wpre[WARPS];
-  SegT agg;
-};
-
-__device__ __forceinline__ SegT cta_reduce_segt(SegT s, SegScanSmem &sm) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    SegT o = shfl_down_segt(s, d);
-    if (lane + d < 32) s = segt_op(s, o);
-  }
-  if (lane == 0) sm.wtot[warp] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    SegT p = segt_ident();
-    for (int w = 0; w < WARPS; w++) p = segt_op(p, sm.wtot[w]);
-    sm.agg = p;
-  }
-  __syncthreads();
-  return sm.agg;
-}
-
-__device__ __forceinline__ SegT cta_scan_segt(SegT s, SegScanSmem &sm) {     // exclusive
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  SegT inc = s;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    SegT o = shfl_up_segt(inc, d);
-    if (lane >= d) inc = segt_op(o, inc);
-  }
-  SegT ex = shfl_up_segt(inc, 1);
-  if (lane == 0) ex = segt_ident();
-  if (lane == 31) sm.wtot[warp] = inc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    SegT p = segt_ident();
-    for (int w = 0; w < WARPS; w++) {
-      sm.wpre[w] = p;
-      p = segt_op(p, sm.wtot[w]);
-    }
-    sm.agg = p;
-  }
-  __syncthreads();
-  return segt_op(sm.wpre[warp], ex);
-}
-
-// ---- decoupled look-back over Seg (warp 0) ---------------------------------------------------------
+// ---- decoupled look-back over Seg (one warp) ---------------------------------------------------------
 __device__ __forceinline__ Seg shfl_down_seg(const Seg &s, int d) {
   Seg o;
   o.recs = __shfl_down_sync(0xffffffffu, s.recs, d);
@@ -372,8 +319,9 @@ __device__ Seg lookback_seg(const KArgs &a, uint32_t t) {
     uint32_t flag = FLAG_INCL;
     if (j >= 0) {
       do {
-        flag = ld_acquire_u32(a.seg_flag + j);
+        flag = ld_relaxed_u32(a.seg_flag + j);       // spin without invalidating L1 every iteration
       } while (flag == 0u);
+      flag = ld_acquire_u32(a.seg_flag + j);         // then one acquire orders the payload loads
       val = ldcg_seg(flag == FLAG_INCL ? a.seg_incl + j : a.seg_agg + j);
     } else if (j == -1) {
       val = a.seed;
@@ -535,128 +483,453 @@ __device__ __forceinline__ void flush_counters(const KArgs &a, EmitCounters &cnt
   if (cnt.unsupported) atomicOr(&a.ctrl->unsupported, 1u);
 }
 
-// ---- the fused scan kernel -------------------------------------------------------------------------
+// ---- per-warp emission (S6+S7): field list in shared memory, then column-wise writes -------------
+// E1: every lane walks its delimiters and appends (first-DATA offset, length | IC) of each field to
+//     the warp's field list at its tile-local field index, and the end index / delimiter position of
+//     each record it closes to the row list.
+// E2: the warp sweeps (column, row) pairs column by column: lanes hold consecutive rows of ONE column,
+//     so the column-major stores coalesce and every lane runs the same converter (no type
+//     divergence).  Digits come from the warp's shared-memory copy of its tile.  This is the paper's
+//     "partition by column, then convert per column" at warp-tile granularity.
+constexpr int WT = 32 * CHUNK;              // bytes per warp tile
+constexpr int FCAP = 512;                   // fields per warp tile handled by E1/E2
+constexpr int RCAP = 128;                   // records per warp tile handled by E1/E2
+struct WarpScratch {
+  uint32_t bytes[2][WT / 4];                // two tiles (stages B and C), 16-byte units swizzled
+  uint2 fields[FCAP];                       // {offset relative to the tile (int32), length | IC << 31}
+  uint32_t rows[RCAP];                      // end field index (low 16) | record delimiter position (high 16)
+};
+constexpr uint32_t FIELD_WRITTEN = 0xFFFFFFFFu;   // length marker: E1 already wrote this field
+
+__device__ __forceinline__ uint32_t swz(uint32_t p) {         // tile byte p -> scratch byte offset
+  uint32_t l = p >> 6, u = (p >> 4) & 3u;
+  return (l << 6) | (((u + (l >> 1)) & 3u) << 4) | (p & 15u);
+}
+__device__ __forceinline__ void stash_chunk(uint32_t *buf, int lane, const uint32_t (&v)[16]) {
+  uint8_t *b = reinterpret_cast<uint8_t *>(buf);
+#pragma unroll
+  for (int u = 0; u < 4; u++)
+    *reinterpret_cast<uint4 *>(b + swz((uint32_t)lane * 64u + 16u * u)) =
+        make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+}
+
+struct TileSrc {                       // raw field bytes: shared-memory tile copy, global before it
+  const KArgs *a;
+  const uint8_t *tb;                   // scratch bytes
+  unsigned long long tbase;            // global position of tile byte 0
+  unsigned long long pos, end;
+  bool ok;
+  __device__ __forceinline__ bool next(uint8_t &c) {
+    if (pos > end) return false;
+    unsigned long long p = pos++;
+    c = p >= tbase ? tb[swz((uint32_t)(p - tbase))] : fetch_byte(*a, p, ok);
+    return true;
+  }
+};
+
+__device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, uint32_t c, unsigned long long row,
+                                            unsigned long long fd, unsigned long long ld, bool ic, bool empty,
+                                            const uint8_t *tb, unsigned long long tbase) {
+  long long v = 0;
+  int ok = 0;
+  if (empty) {
+    if (cd->has_def) { v = cd->def_bits; ok = 1; }
+  } else if (ic) {
+    push_defer(a, fd, ld, row, c, 1u);
+    return;
+  } else {
+    TileSrc src{&a, tb, tbase, fd, ld, true};
+    int res = cd->type == T_INT64 ? conv_int64(src, v) : conv_float64_fast(src, v);
+    if (!src.ok) res = 2;
+    if (res == 2) { push_defer(a, fd, ld, row, c, 0u); return; }
+    ok = res;
+    if (!ok) v = 0;
+  }
+  __stcs(reinterpret_cast<long long *>(cd->val) + row, v);
+  __stcs(cd->valid + row, (uint8_t)ok);
+}
+
+// Per-warp emission of one tile.  st = the lane's chunk-start state (global), sex = the lane's exclusive
+// tile-local summary, agg = the tile summary, prefix = everything before the tile.
+__device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, const uint32_t *tbytes, const Seg &st, SegT sex,
+                          SegT agg, const Seg &prefix, unsigned long long Dm, unsigned long long Fm,
+                          unsigned long long Rm, unsigned long long Vm, unsigned long long tbase_g,
+                          unsigned long long cbase, EmitCounters &cnt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nf = agg.cnt >> 16, nrec = agg.cnt & 0xFFFFu;
+  if (nf > (uint32_t)FCAP || nrec >= (uint32_t)RCAP) {       // warp-uniform: dense tile, direct path
+    emit_chunk(a, cols, st, Dm, Fm, Rm, Vm, cbase, cnt);
+    return;
+  }
+  // ---- E1 ----
+  {
+    unsigned long long Km = Vm & ~Dm & ~Fm;
+    unsigned long long r = st.recs;
+    uint32_t c = st.col;
+    unsigned long long cfd = st.fd, cld = st.ld;
+    uint32_t cfl = st.flags & (F_IC | F_PC | F_PRE);
+    uint32_t k = sex.cnt >> 16, j = sex.cnt & 0xFFFFu;
+    int prev = -1;
+    unsigned long long fm = Fm;
+    while (fm) {
+      int p = lsb64(fm);
+      fm &= fm - 1ull;
+      unsigned long long rng = below(p) & above(prev);
+      int fd, ld;
+      uint32_t fl = open_summary(Dm & rng, Km & rng, fd, ld);
+      unsigned long long sfd = fd < 0 ? NONE : cbase + (unsigned)fd;
+      unsigned long long sld = fd < 0 ? NONE : cbase + (unsigned)ld;
+      if (prev >= 0) { cfd = sfd; cld = sld; cfl = fl; }
+      else open_combine(cfd, cld, cfl, sfd, sld, fl);
+      const unsigned long long dpos = cbase + (unsigned)p;
+      uint2 e;
+      if (cfd == NONE) {
+        e = make_uint2((uint32_t)(dpos - tbase_g), 0u);
+      } else {
+        unsigned long long L = cld + 1 - cfd;
+        long long rel = (long long)cfd - (long long)tbase_g;
+        if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {     // huge / far-away field: write it here
+          emit_field(a, cols, r, c, cfd, cld, cfl, dpos, cnt);
+          e = make_uint2(0u, FIELD_WRITTEN);
+          if (c >= a.C) cnt.extra--;                          // counted again below
+        } else {
+          e = make_uint2((uint32_t)(int32_t)rel, (uint32_t)L | ((cfl & F_IC) ? 0x80000000u : 0u));
+        }
+      }
+      ws->fields[k++] = e;
+      if (c >= a.C) cnt.extra++;
+      if ((Rm >> p) & 1ull) {
+        ws->rows[j++] = k | ((uint32_t)(dpos - tbase_g) << 16);
+        r++;
+        c = 0;
+      } else {
+        c++;
+      }
+      prev = p;
+    }
+  }
+  __syncwarp();
+  // ---- E2 ----
+  const uint8_t *tb = reinterpret_cast<const uint8_t *>(tbytes);
+  const uint32_t last_end = nrec ? (ws->rows[nrec - 1] & 0xFFFFu) : 0u;
+  const uint32_t nrows = nrec + (nf > last_end ? 1u : 0u);
+  const uint32_t c0 = prefix.col;
+  const unsigned long long r0 = prefix.recs;
+  for (uint32_t c = 0; c < a.C; c++) {
+    const ColDesc *cd = cols + c;
+    for (uint32_t jr = lane; jr < nrows; jr += 32) {
+      uint32_t start = jr == 0 ? 0u : (ws->rows[jr - 1] & 0xFFFFu);
+      uint32_t end = jr < nrec ? (ws->rows[jr] & 0xFFFFu) : nf;
+      uint32_t cs = jr == 0 ? c0 : 0u;
+      if (c < cs) continue;                                   // written by an earlier tile
+      uint32_t k = start + (c - cs);
+      unsigned long long row = r0 + jr - a.row_base;
+      if (row >= a.cap) continue;
+      if (k < end) {
+        uint2 e = ws->fields[k];
+        if (e.y == FIELD_WRITTEN) continue;
+        uint32_t len = e.y & 0x7FFFFFFFu;
+        unsigned long long off = tbase_g + (unsigned long long)(long long)(int32_t)e.x;
+        __stcs(cd->off + row, off);
+        __stcs(cd->len + row, len);
+        if (cd->type != T_SPAN)
+          write_value(a, cd, c, row, off, off + len - 1, (e.y >> 31) != 0, len == 0, tb, tbase_g);
+      } else if (jr < nrec) {                                 // record closed with fewer fields
+        if (k == end) cnt.missing++;
+        unsigned long long dpos = tbase_g + (ws->rows[jr] >> 16);
+        __stcs(cd->off + row, dpos);
+        __stcs(cd->len + row, 0xFFFFFFFFu);
+        if (cd->type != T_SPAN) {
+          __stcs(reinterpret_cast<long long *>(cd->val) + row, cd->has_def ? cd->def_bits : 0ll);
+          __stcs(cd->valid + row, (uint8_t)(cd->has_def ? 1 : 0));
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// ---- the fused scan kernel: warp-specialised pipeline over 32 KB tiles -----------------------------
+// CTA = 16 compute warps + 1 look-back warp.  A tile = 16 warp tiles of 2 KB (one 64-byte chunk per
+// lane).  Per iteration i the compute warps run
+//   A(i)   load + S1/S2 (τ per chunk) + warp ∘-scan -> warp aggregates            -> mbarrier A
+//   B(i-1) entry states from the τ prefix, S4 masks, S5 warp summary scan         -> mbarrier B
+//   C(i-2) S6/S7 emission from the record/column prefix
+// while the look-back warp combines the warp aggregates of tile i, publishes them and runs the
+// decoupled look-back over tile τ's (single-pass scan P:250), then does the same for the
+// record/column summaries of tile i-1.  Nothing waits for the current tile's look-back: the chains
+// advance a full pipeline stage behind the compute.  The tile bytes are re-read from L2 (not DRAM)
+// in stages B and C.
+constexpr int CW = 16;                              // compute warps per CTA
+constexpr int PTILE = CW * WT;                      // bytes per look-back tile (32 KB)
+
+struct PipeSmem {
+  uint64_t mbA[2], mbTP[2], mbB[2], mbSP[2];
+  uint32_t tile_id[4];
+  uint32_t wtau[2][CW];                             // warp τ aggregates (nibble form)
+  uint32_t wentry[2][CW];                           // warp entry states (device numbering)
+  SegT wseg[2][CW];                                 // warp summaries (positions warp-tile-local)
+  Seg wpre[2][CW];                                  // warp prefixes (global)
+};
+
 template <int MODE>
-__global__ void __launch_bounds__(THREADS) k_scan(const KArgs a, const DfaK dfa, const ColsK colsk) {
-  extern __shared__ __align__(16) uint8_t lut[];
-  __shared__ TauScanSmem tsm;
-  __shared__ SegScanSmem ssm;
-  __shared__ Seg s_prefix;
+struct ScanCfg {
+  static constexpr int THREADS = (CW + 1) * 32;
+  static constexpr size_t SMEM = LUT_BYTES + sizeof(PipeSmem) + (MODE == MODE_EMIT ? CW * sizeof(WarpScratch) : 0);
+};
+
+// Look-back warp, in two halves per chain so that a tile's aggregate is always published before this
+// warp blocks in any look-back (publishing never waits; look-backs only wait on smaller tiles, so the
+// smallest blocked look-back always makes progress — no cross-CTA cycles).
+struct LbTau { uint32_t wex, agg; };
+struct LbSeg { SegT wex; Seg agg; };
+
+__device__ __forceinline__ LbTau lb_tau_publish(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t) {
+  const int lane = threadIdx.x & 31;
+  uint32_t w = lane < CW ? sm.wtau[slot][lane] : NIB_IDENT;
+  LbTau r;
+  r.wex = warp_scan_tau(spread16(w), spread16(w >> 16), r.agg);
+  if (lane == 0) st_relaxed_u64(a.tau_desc + t, ((unsigned long long)(t == 0 ? FLAG_INCL : FLAG_AGG) << 32) | r.agg);
+  return r;
+}
+__device__ __forceinline__ void lb_tau_finish(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t, const LbTau &r) {
+  const int lane = threadIdx.x & 31;
+  uint32_t prefix = NIB_IDENT;
+  if (t != 0) {
+    prefix = lookback_tau(a, t);
+    if (lane == 0) st_relaxed_u64(a.tau_desc + t, ((unsigned long long)FLAG_INCL << 32) | compose_nib(prefix, r.agg));
+  }
+  const uint32_t tile_entry = nib_at(prefix, a.seed_dev);
+  if (lane < CW) {
+    uint32_t e = nib_at(r.wex, tile_entry);
+    sm.wentry[slot][lane] = e;
+    a.tinfo[(unsigned long long)t * CW + lane].entry = e;
+  }
+}
+__device__ __forceinline__ LbSeg lb_seg_publish(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t) {
+  const int lane = threadIdx.x & 31;
+  SegT w = lane < CW ? segt_shift(sm.wseg[slot][lane], (uint32_t)lane * WT) : segt_ident();
+  SegT sagg;
+  LbSeg r;
+  r.wex = warp_scan_segt(w, sagg);
+  r.agg = segt_to_seg(sagg, a.base + (unsigned long long)t * PTILE);
+  if (lane == 0) {
+    if (t == 0) {
+      stcg_seg(a.seg_incl, seg_op(a.seed, r.agg));
+      st_release_u32(a.seg_flag, FLAG_INCL);
+    } else {
+      stcg_seg(a.seg_agg + t, r.agg);
+      st_release_u32(a.seg_flag + t, FLAG_AGG);
+    }
+  }
+  return r;
+}
+__device__ __forceinline__ void lb_seg_finish(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t, const LbSeg &r) {
+  const int lane = threadIdx.x & 31;
+  Seg prefix = a.seed;
+  if (t != 0) {
+    prefix = lookback_seg(a, t);
+    if (lane == 0) {
+      stcg_seg(a.seg_incl + t, seg_op(prefix, r.agg));
+      st_release_u32(a.seg_flag + t, FLAG_INCL);
+    }
+  }
+  if (lane < CW) {
+    Seg wp = seg_op(prefix, segt_to_seg(r.wex, a.base + (unsigned long long)t * PTILE));
+    sm.wpre[slot][lane] = wp;
+    a.tinfo[(unsigned long long)t * CW + lane].excl = wp;
+  }
+}
+
+template <int MODE>
+__global__ void __maxnreg__(120) k_scan(const KArgs a, const DfaK dfa, const ColsK colsk) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t *lut = smem;
+  PipeSmem &sm = *reinterpret_cast<PipeSmem *>(smem + LUT_BYTES);
+  WarpScratch *scratch = reinterpret_cast<WarpScratch *>(smem + LUT_BYTES + sizeof(PipeSmem));
   __shared__ ColDesc s_cols[MODE == MODE_EMIT ? MAX_COLS : 1];
   build_lut(lut, dfa);
   if (MODE == MODE_EMIT)
-    for (int c = threadIdx.x; c < (int)a.C; c += THREADS) s_cols[c] = colsk.c[c];
-  const int tid = threadIdx.x, lane = tid & 31;
+    for (int c = threadIdx.x; c < (int)a.C; c += blockDim.x) s_cols[c] = colsk.c[c];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; s++) {
+      mbar_init(&sm.mbA[s], CW);
+      mbar_init(&sm.mbTP[s], 1);
+      mbar_init(&sm.mbB[s], CW);
+      mbar_init(&sm.mbSP[s], 1);
+    }
+  }
+  __syncthreads();                                          // the only CTA-wide barrier
+  if (warp == CW) {
+    // ================= look-back warp =================
+    bool prev_valid = false;
+    uint32_t t_prev = 0;
+    for (uint32_t i = 0;; i++) {
+      LbSeg rs;
+      const bool do_seg = MODE != MODE_TAU && i >= 1;
+      if (do_seg) {                                          // publish tile i-1's summary aggregate
+        mbar_wait(&sm.mbB[(i - 1) & 1], ((i - 1) >> 1) & 1);
+        if (prev_valid) rs = lb_seg_publish(a, sm, (i - 1) & 1, t_prev);
+      }
+      mbar_wait(&sm.mbA[i & 1], (i >> 1) & 1);
+      const uint32_t t = sm.tile_id[i & 3];
+      const bool valid = t < a.ntiles;
+      if (valid) {                                           // publish tile i's τ aggregate, then chase
+        LbTau rt = lb_tau_publish(a, sm, i & 1, t);
+        lb_tau_finish(a, sm, i & 1, t, rt);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.mbTP[i & 1]);
+      }
+      if (do_seg && prev_valid) {
+        lb_seg_finish(a, sm, (i - 1) & 1, t_prev, rs);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.mbSP[(i - 1) & 1]);
+      }
+      if (!valid) break;
+      prev_valid = valid;
+      t_prev = t;
+    }
+    return;
+  }
+  // ================= compute warps =================
+  WarpScratch *ws = scratch + warp;
   const uint32_t laneoff = (uint32_t)(lane & 15) * 8u;
   EmitCounters cnt{0ull, 0ull, 0u};
-  __syncthreads();
-  while (true) {
-    if (tid == 0) tsm.tile = atomicAdd(&a.ctrl->ticket, 1u);
-    __syncthreads();
-    const uint32_t t = tsm.tile;
-    if (t >= a.ntiles) break;
-    const unsigned long long tstart = (unsigned long long)t * TILE;
-    const unsigned long long cstart = tstart + (unsigned long long)tid * CHUNK;
-    int nvalid = cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
-    uint32_t v[16];
-    load_chunk(a.in + cstart, nvalid, v);
-    uint32_t t0, t1;
-    if (nvalid == CHUNK) chunk_tau<true>(lut, v, nvalid, laneoff, t0, t1);
-    else chunk_tau<false>(lut, v, nvalid, laneoff, t0, t1);
-    uint32_t ex = cta_scan_tau(t0, t1, tsm);
-    // publish the tile aggregate, look back, publish the inclusive prefix
-    if (tid < 32) {
-      uint32_t prefix = NIB_IDENT;
-      if (t == 0) {
-        if (tid == 0) st_relaxed_u64(a.tau_desc, ((unsigned long long)FLAG_INCL << 32) | tsm.agg);
-      } else {
-        if (tid == 0) st_relaxed_u64(a.tau_desc + t, ((unsigned long long)FLAG_AGG << 32) | tsm.agg);
-        prefix = lookback_tau(a, t);
-        if (tid == 0)
-          st_relaxed_u64(a.tau_desc + t, ((unsigned long long)FLAG_INCL << 32) | compose_nib(prefix, tsm.agg));
-      }
-      if (tid == 0) tsm.prefix = prefix;
+  // stage registers: A = tile i (bytes, prefetched one iteration ahead), B = tile i-1 (bytes,
+  // lane-exclusive τ), C = tile i-2 (masks, summary scan; its bytes are in ws->bytes[(i-2)&1])
+  uint32_t vA[16], vB[16];
+  int nvA = 0, nvB = 0;
+  uint32_t tA = 0xFFFFFFFFu, exB = NIB_IDENT;
+  unsigned long long wtB = 0, wtC = 0;
+  bool validA = false, validB = false, validC = false;
+  unsigned long long DmC = 0, FmC = 0, RmC = 0, VmC = 0;
+  SegT sexC = segt_ident(), saggC = segt_ident();
+  // prologue: claim and load tile 0
+  if (warp == 0 && lane == 0) sm.tile_id[0] = atomicAdd(&a.ctrl->ticket, 1u);
+  named_bar_sync(1, CW * 32);
+  tA = sm.tile_id[0];
+  validA = tA < a.ntiles;
+  if (validA) {
+    const unsigned long long cstart = ((unsigned long long)tA * CW + warp) * WT + (unsigned long long)lane * CHUNK;
+    nvA = cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
+    load_chunk(a.in + cstart, nvA, vA);
+  }
+  for (uint32_t i = 0;; i++) {
+    // ---- claim tile i+1 and issue its loads (they land while A/B/C below compute) ----
+    if (warp == 0 && lane == 0) sm.tile_id[(i + 1) & 3] = atomicAdd(&a.ctrl->ticket, 1u);
+    named_bar_sync(1, CW * 32);
+    const uint32_t tN = sm.tile_id[(i + 1) & 3];
+    const bool validN = tN < a.ntiles;
+    uint32_t vN[16];
+    int nvN = 0;
+    if (validN) {
+      const unsigned long long cstart = ((unsigned long long)tN * CW + warp) * WT + (unsigned long long)lane * CHUNK;
+      nvN = cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
+      load_chunk(a.in + cstart, nvN, vN);
     }
-    __syncthreads();
-    if (MODE == MODE_TAU) continue;
-    const uint32_t tile_entry = nib_at(tsm.prefix, a.seed_dev);
-    const uint32_t entry = nib_at(ex, tile_entry);
-    a.chunk_state[(unsigned long long)t * THREADS + tid] = (uint8_t)entry;
-    unsigned long long Dm, Fm, Rm;
-    uint32_t fin;
-    if (nvalid == CHUNK) fin = chunk_masks<true>(lut, v, nvalid, laneoff, entry, Dm, Fm, Rm);
-    else fin = chunk_masks<false>(lut, v, nvalid, laneoff, entry, Dm, Fm, Rm);
-    if (fin == INV_DEV && entry != INV_DEV && nvalid > 0) {
-      int p = first_inv_in_chunk(lut, a.in + cstart, nvalid, laneoff, entry);
-      if (p >= 0) atomicMax(&a.ctrl->inv_neg, ~(a.base + cstart + (unsigned)p));
+    // ---- A(i): τ of the chunk, warp scan ----
+    uint32_t exA = NIB_IDENT;
+    const unsigned long long wtA = (unsigned long long)tA * CW + warp;
+    if (validA) {
+      uint32_t t0, t1, agg;
+      if (nvA == CHUNK) chunk_tau<true>(lut, vA, nvA, laneoff, t0, t1);
+      else chunk_tau<false>(lut, vA, nvA, laneoff, t0, t1);
+      exA = warp_scan_tau(t0, t1, agg);
+      if (lane == 0) sm.wtau[i & 1][warp] = agg;
     }
-    const unsigned long long Vm = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull);
-    SegT s = chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)tid * CHUNK);
-    SegT sex;
-    if (MODE == MODE_EMIT) sex = cta_scan_segt(s, ssm);
-    else cta_reduce_segt(s, ssm);
-    if (tid < 32) {
-      Seg agg = segt_to_seg(ssm.agg, a.base + tstart);
-      Seg prefix;
-      if (t == 0) {
-        prefix = a.seed;
-        if (tid == 0) {
-          stcg_seg(a.seg_incl, seg_op(prefix, agg));
-          st_release_u32(a.seg_flag, FLAG_INCL);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.mbA[i & 1]);
+    // TAU-only mode: stay at most one tile ahead of the look-back warp (mbarrier phases, smem slots)
+    if (MODE == MODE_TAU && i >= 1 && validB) mbar_wait(&sm.mbTP[(i - 1) & 1], ((i - 1) >> 1) & 1);
+    // ---- B(i-1): entry states, masks, summary scan ----
+    if (MODE != MODE_TAU && i >= 1) {
+      if (validB) {
+        if (MODE == MODE_EMIT) stash_chunk(ws->bytes[(i - 1) & 1], lane, vB);
+        mbar_wait(&sm.mbTP[(i - 1) & 1], ((i - 1) >> 1) & 1);
+        const uint32_t entry = nib_at(exB, sm.wentry[(i - 1) & 1][warp]);
+        a.chunk_state[wtB * 32 + lane] = (uint8_t)entry;
+        unsigned long long Dm, Fm, Rm;
+        uint32_t fin;
+        if (nvB == CHUNK) fin = chunk_masks<true>(lut, vB, nvB, laneoff, entry, Dm, Fm, Rm);
+        else fin = chunk_masks<false>(lut, vB, nvB, laneoff, entry, Dm, Fm, Rm);
+        const unsigned long long cstart = wtB * WT + (unsigned long long)lane * CHUNK;
+        if (fin == INV_DEV && entry != INV_DEV && nvB > 0) {
+          int p = first_inv_in_chunk(lut, a.in + cstart, nvB, laneoff, entry);
+          if (p >= 0) atomicMax(&a.ctrl->inv_neg, ~(a.base + cstart + (unsigned)p));
         }
-      } else {
-        if (tid == 0) {
-          stcg_seg(a.seg_agg + t, agg);
-          st_release_u32(a.seg_flag + t, FLAG_AGG);
-        }
-        prefix = lookback_seg(a, t);
-        if (tid == 0) {
-          stcg_seg(a.seg_incl + t, seg_op(prefix, agg));
-          st_release_u32(a.seg_flag + t, FLAG_INCL);
-        }
+        const unsigned long long Vm = nvB >= 64 ? ~0ull : ((1ull << nvB) - 1ull);
+        SegT sagg;
+        const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
+        if (lane == 0) sm.wseg[(i - 1) & 1][warp] = sagg;
+        DmC = Dm; FmC = Fm; RmC = Rm; VmC = Vm; sexC = sex; saggC = sagg;
       }
-      if (tid == 0) {
-        s_prefix = prefix;
-        a.tinfo[t].excl = prefix;
-        a.tinfo[t].entry = tile_entry;
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sm.mbB[(i - 1) & 1]);
     }
-    __syncthreads();
-    if (MODE == MODE_EMIT) {
-      Seg st = seg_op(s_prefix, segt_to_seg(sex, a.base + tstart));
-      emit_chunk(a, s_cols, st, Dm, Fm, Rm, Vm, a.base + cstart, cnt);
+    // ---- C(i-2): emission ----
+    if (MODE == MODE_EMIT && i >= 2 && validC) {
+      mbar_wait(&sm.mbSP[(i - 2) & 1], ((i - 2) >> 1) & 1);
+      const Seg wprefix = sm.wpre[(i - 2) & 1][warp];
+      const unsigned long long cstart = wtC * WT + (unsigned long long)lane * CHUNK;
+      const Seg st = seg_op(wprefix, segt_to_seg(sexC, a.base + wtC * WT));
+      emit_tile(a, s_cols, ws, ws->bytes[(i - 2) & 1], st, sexC, saggC, wprefix, DmC, FmC, RmC, VmC,
+                a.base + wtC * WT, a.base + cstart, cnt);
     }
+    const bool done = MODE == MODE_EMIT ? (i >= 2 && !validC) : (i >= 1 && !validB);
+    if (done) break;
+    // ---- rotate the pipeline ----
+    validC = validB;
+    wtC = wtB;
+    validB = validA;
+    wtB = wtA;
+    exB = exA;
+    nvB = nvA;
+#pragma unroll
+    for (int k = 0; k < 16; k++) vB[k] = vA[k];
+    validA = validN;
+    tA = tN;
+    nvA = nvN;
+#pragma unroll
+    for (int k = 0; k < 16; k++) vA[k] = vN[k];
   }
   flush_counters(a, cnt);
 }
 
-// ---- two-phase emit kernel -------------------------------------------------------------------------
-__global__ void __launch_bounds__(THREADS) k_emit(const KArgs a, const DfaK dfa, const ColsK colsk) {
-  extern __shared__ __align__(16) uint8_t lut[];
-  __shared__ SegScanSmem ssm;
+// ---- two-phase emit kernel (per warp tile, from the stored prefixes; no look-back) ------------------
+constexpr int EMIT_WARPS = 16;
+constexpr size_t EMIT_SMEM = LUT_BYTES + EMIT_WARPS * sizeof(WarpScratch);
+
+__global__ void __launch_bounds__(EMIT_WARPS * 32, 1) k_emit(const KArgs a, const DfaK dfa, const ColsK colsk) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t *lut = smem;
   __shared__ ColDesc s_cols[MAX_COLS];
   build_lut(lut, dfa);
-  for (int c = threadIdx.x; c < (int)a.C; c += THREADS) s_cols[c] = colsk.c[c];
-  const int tid = threadIdx.x, lane = tid & 31;
+  for (int c = threadIdx.x; c < (int)a.C; c += blockDim.x) s_cols[c] = colsk.c[c];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpScratch *ws = reinterpret_cast<WarpScratch *>(smem + LUT_BYTES) + warp;
   const uint32_t laneoff = (uint32_t)(lane & 15) * 8u;
   EmitCounters cnt{0ull, 0ull, 0u};
   __syncthreads();
-  for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-    const unsigned long long tstart = (unsigned long long)t * TILE;
-    const unsigned long long cstart = tstart + (unsigned long long)tid * CHUNK;
-    int nvalid = cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
+  const uint32_t gw = blockIdx.x * EMIT_WARPS + warp, nw = gridDim.x * EMIT_WARPS;
+  const uint32_t nwt = a.ntiles * CW;
+  for (uint32_t t = gw; t < nwt; t += nw) {
+    const unsigned long long tstart = (unsigned long long)t * WT;
+    const unsigned long long cstart = tstart + (unsigned long long)lane * CHUNK;
+    const int nvalid = cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
     uint32_t v[16];
     load_chunk(a.in + cstart, nvalid, v);
-    const uint32_t entry = a.chunk_state[(unsigned long long)t * THREADS + tid];
+    stash_chunk(ws->bytes[0], lane, v);
+    const uint32_t entry = a.chunk_state[(unsigned long long)t * 32 + lane];
     unsigned long long Dm, Fm, Rm;
     if (nvalid == CHUNK) chunk_masks<true>(lut, v, nvalid, laneoff, entry, Dm, Fm, Rm);
     else chunk_masks<false>(lut, v, nvalid, laneoff, entry, Dm, Fm, Rm);
     const unsigned long long Vm = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull);
-    SegT s = chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)tid * CHUNK);
-    SegT sex = cta_scan_segt(s, ssm);
-    Seg st = seg_op(a.tinfo[t].excl, segt_to_seg(sex, a.base + tstart));
-    emit_chunk(a, s_cols, st, Dm, Fm, Rm, Vm, a.base + cstart, cnt);
-    __syncthreads();
+    SegT sagg;
+    const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
+    const Seg prefix = a.tinfo[t].excl;
+    const Seg st = seg_op(prefix, segt_to_seg(sex, a.base + tstart));
+    emit_tile(a, s_cols, ws, ws->bytes[0], st, sex, sagg, prefix, Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
   }
   flush_counters(a, cnt);
 }

@@ -1,0 +1,117 @@
+"""GPU: range summaries and sharded parsing (the multi-GPU path) on one GPU with "virtual ranks".
+
+The input is cut at arbitrary byte positions (inside quoted fields, on delimiters, at ±1 of them);
+each range is summarised on the GPU (parpa_summarize / parpa_count), the summaries are composed on
+the host exactly as distributed.exchange does across ranks, every range is parsed with
+parpa_parse_range, and the concatenated rows must equal the oracle's single-shot parse."""
+import random
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+from tests.gpu_helpers import to_np
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+import paper_1905_13415_b200 as parpa  # noqa: E402
+from paper_1905_13415_b200 import distributed as pdist  # noqa: E402
+
+
+def dev(a):
+    t = torch.empty(max(len(a), 1) + 16, dtype=torch.uint8, device="cuda")
+    if len(a):
+        t[:len(a)].copy_(torch.from_numpy(np.frombuffer(bytes(a), np.uint8).copy()))
+    return t[:len(a)]
+
+
+def sharded_parse(dialect, data, types, cuts, left_bytes=4096):
+    """Parse every range as its own "rank" and assemble the global columns.  Columns stay sharded
+    (SURVEY §8e): the record straddling cut g has its columns < col(g) on rank g-1 (local row
+    R_local) and the rest on rank g (local row 0)."""
+    dfa = parpa.Dfa.dialect(dialect)
+    schema = parpa.Schema(list(types))
+    G = len(cuts) - 1
+    taus, counts = [], []
+    for g in range(G):
+        taus.append(parpa.summarize(dfa, dev(data[cuts[g]:cuts[g + 1]])))
+    for g in range(G):
+        e = pdist.entry_state(dfa, taus, g)
+        c, tau2 = parpa.count(dfa, dev(data[cuts[g]:cuts[g + 1]]), cuts[g], e)
+        assert tau2 == taus[g]
+        counts.append(c)
+    C = len(types)
+    out = [[[] for _ in range(4)] for _ in range(C)]
+    for g in range(G):
+        e = pdist.entry_state(dfa, taus, g)
+        prefix = pdist.prefix_counts(counts, g)
+        after = pdist.prefix_counts(counts, g + 1)
+        lo, hi = cuts[g], cuts[g + 1]
+        cap = (hi - lo) + 2
+        cols = parpa.alloc_columns(schema, cap)
+        st = parpa.new_stats_tensor()
+        left = dev(data[max(0, lo - left_bytes):lo]) if lo else None
+        last = g == G - 1
+        parpa.parse_range(dfa, schema, dev(data[lo:hi]), e, lo, prefix, cols, cap, st, left=left, is_last=last)
+        s = parpa.stats_from_tensor(st)
+        assert s["status"] in (0, parpa.ECOLUMNS), s
+        n = s["records"]
+        c_in, c_out = prefix.column, after.column
+        for c in range(C):
+            rows = list(range(n + (0 if last else 1)))
+            keep = []
+            for r in rows:
+                ok = True
+                if r == 0 and c < c_in:
+                    ok = False                 # closed on an earlier rank
+                if r == n and not last and c >= c_out:
+                    ok = False                 # closed on a later rank
+                if ok:
+                    keep.append(r)
+            arrs = [cols[c].offset, cols[c].length, cols[c].value, cols[c].valid]
+            views = [np.uint64, np.uint32, np.int64, None]
+            for i in range(4):
+                if arrs[i] is None:
+                    continue
+                a = to_np(arrs[i])
+                a = a.view(views[i]) if views[i] is not None else a
+                out[c][i].append(a[keep])
+    return [tuple(np.concatenate(x[i]) if x[i] else None for i in range(4)) for x in out]
+
+
+@pytest.mark.parametrize("name,G,seed", [("cfg1", 2, 0), ("cfg1", 5, 1), ("yelp", 3, 2), ("clf", 4, 3),
+                                         ("taxi", 3, 4)])
+def test_virtual_ranks_equal_single_shot(name, G, seed):
+    w = datagen.WORKLOADS[name]
+    data, _ = datagen.generate(name, 1_500_000)
+    data = bytes(data)
+    ora = oracle.parse(w.dialect, data, w.C, list(w.types))
+    rng = random.Random(seed)
+    inner = sorted(rng.sample(range(1, len(data) - 1), G - 1))
+    # nudge one cut onto a delimiter and one just after, and keep 16-byte alignment of nothing in particular
+    cuts = [0] + inner + [len(data)]
+    cols = sharded_parse(w.dialect, data, w.types, cuts)
+    for c, t in enumerate(w.types):
+        off, ln, val, ok = cols[c]
+        assert np.array_equal(off, ora.offset[c]), (name, c)
+        assert np.array_equal(ln, ora.length[c]), (name, c)
+        if t != oracle.SPAN:
+            assert np.array_equal(ok, ora.valid[c]), (name, c)
+            assert np.array_equal(val, ora.value[c]), (name, c)
+
+
+def test_cuts_at_delimiters_and_inside_quotes():
+    data = b'1,"Hello, World\nHow are you?",3\n' * 400 + b'x,"a""b",7\n' * 300
+    types = [oracle.SPAN, oracle.SPAN, oracle.INT64]
+    ora = oracle.parse("csv", data, 3, types)
+    special = [i for i in range(1, len(data) - 1) if data[i] in b',\n"']
+    rng = random.Random(9)
+    for trial in range(6):
+        picks = sorted(set(rng.sample(special, 3) + [rng.choice(special) + 1]))
+        cuts = [0] + picks + [len(data)]
+        cols = sharded_parse("csv", data, types, cuts)
+        for c in range(3):
+            assert np.array_equal(cols[c][0], ora.offset[c])
+            assert np.array_equal(cols[c][1], ora.length[c])
+        assert np.array_equal(cols[2][2], ora.value[2])
