@@ -225,6 +225,8 @@ int parpa_set_profiling(int enable);
 int parpa_last_kernel_times(const char **names, float *ms, int cap);
 
 const char *parpa_status_string(int status);
+/* text of the last CUDA runtime error seen by this thread ("" if none) */
+const char *parpa_last_error(void);
 const char *parpa_version(void);
 
 #ifdef __cplusplus

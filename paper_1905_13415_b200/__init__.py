@@ -29,7 +29,8 @@ NONE = 0xFFFFFFFFFFFFFFFF
 class ParpaError(RuntimeError):
     def __init__(self, code, what=""):
         lib = _lib.load()
-        super().__init__(f"{what}: {lib.parpa_status_string(code).decode()} ({code})")
+        detail = lib.parpa_last_error().decode() if code == -3 else ""
+        super().__init__(f"{what}: {lib.parpa_status_string(code).decode()} ({code}) {detail}")
         self.code = code
 
 

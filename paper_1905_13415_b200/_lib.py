@@ -54,6 +54,7 @@ EXPORTS = [
     "parpa_parse_into", "parpa_parse_host", "parpa_summarize", "parpa_count", "parpa_compose_tau",
     "parpa_compose_counts", "parpa_parse_range", "parpa_debug_trace", "parpa_chunk_bytes", "parpa_tile_bytes",
     "parpa_set_profiling", "parpa_last_kernel_times", "parpa_status_string", "parpa_version",
+    "parpa_last_error",
 ]
 
 
@@ -109,5 +110,6 @@ def load(build_if_missing: bool = True):
         lib.parpa_status_string.restype = ctypes.c_char_p
         lib.parpa_status_string.argtypes = [ctypes.c_int]
         lib.parpa_version.restype = ctypes.c_char_p
+        lib.parpa_last_error.restype = ctypes.c_char_p
         _lib = lib
         return lib

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -29,8 +30,10 @@ namespace {
 constexpr size_t ALIGN = 256;
 size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
+thread_local char t_last_error[256] = "";
 int cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return PARPA_OK;
+  snprintf(t_last_error, sizeof(t_last_error), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
   if (e == cudaErrorMemoryAllocation) return PARPA_ENOMEM;
   return PARPA_ECUDA;
 }
@@ -66,6 +69,20 @@ int dev_cfg(DevCfg **out) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[1], k_scan<MODE_COUNT>, ScanCfg<MODE_COUNT>::THREADS, ScanCfg<MODE_COUNT>::SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[2], k_scan<MODE_EMIT>, ScanCfg<MODE_EMIT>::THREADS, ScanCfg<MODE_EMIT>::SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit, EMIT_WARPS * 32, EMIT_SMEM));
+    if (getenv("PARPA_DEBUG")) {
+      auto show = [](const char *n, const void *f) {
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, f) == cudaSuccess)
+          fprintf(stderr, "[parpa] %s: regs=%d maxThreads=%d static_smem=%zu local=%zu maxDynSmem=%d\n", n, fa.numRegs,
+                  fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.localSizeBytes, fa.maxDynamicSharedSizeBytes);
+      };
+      show("k_scan<TAU>", (const void *)k_scan<MODE_TAU>);
+      show("k_scan<COUNT>", (const void *)k_scan<MODE_COUNT>);
+      show("k_scan<EMIT>", (const void *)k_scan<MODE_EMIT>);
+      show("k_emit", (const void *)k_emit);
+      fprintf(stderr, "[parpa] occ tau=%d count=%d emit=%d k_emit=%d sms=%d smem(emit)=%zu\n", c.occ_scan[0],
+              c.occ_scan[1], c.occ_scan[2], c.occ_emit, c.sms, (size_t)ScanCfg<MODE_EMIT>::SMEM);
+    }
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;
@@ -122,9 +139,9 @@ struct Work {
   void *block = nullptr;
   size_t zero_bytes = 0;
   unsigned long long *tau_desc = nullptr;
-  uint32_t *seg_flag = nullptr;
+  uint4 *seg_desc = nullptr;
   Ctrl *ctrl = nullptr;
-  Seg *seg_agg = nullptr, *seg_incl = nullptr;
+  Seg *seg_incl = nullptr;
   TileInfo *tinfo = nullptr;
   uint8_t *chunk_state = nullptr;
   DeferItem *dq = nullptr;
@@ -141,10 +158,9 @@ int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cu
   w.dq_cap = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(4096, len / 512), 1u << 24);
   size_t o = 0;
   size_t o_tau = o; o = align_up(o + nt * 8);
-  size_t o_flag = o; o = align_up(o + nt * 4);
+  size_t o_flag = o; o = align_up(o + nt * 16);
   size_t o_ctrl = o; o = align_up(o + sizeof(Ctrl));
   size_t zero = o;
-  size_t o_agg = o; o = align_up(o + nt * sizeof(Seg));
   size_t o_incl = o; o = align_up(o + nt * sizeof(Seg));
   size_t o_tinfo = o; o = align_up(o + nt * CW * sizeof(TileInfo));
   size_t o_cs = o; o = align_up(o + nt * CW * 32);
@@ -154,9 +170,8 @@ int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cu
   CK(cudaMallocAsync(&w.block, o, s));
   uint8_t *b = (uint8_t *)w.block;
   w.tau_desc = (unsigned long long *)(b + o_tau);
-  w.seg_flag = (uint32_t *)(b + o_flag);
+  w.seg_desc = (uint4 *)(b + o_flag);
   w.ctrl = (Ctrl *)(b + o_ctrl);
-  w.seg_agg = (Seg *)(b + o_agg);
   w.seg_incl = (Seg *)(b + o_incl);
   w.tinfo = (TileInfo *)(b + o_tinfo);
   w.chunk_state = b + o_cs;
@@ -191,8 +206,7 @@ void make_args(KArgs &a, const Work &w, const uint8_t *in, uint64_t len) {
   a.ntiles = w.ntiles;
   a.seed = seg_identity();
   a.tau_desc = w.tau_desc;
-  a.seg_flag = w.seg_flag;
-  a.seg_agg = w.seg_agg;
+  a.seg_desc = w.seg_desc;
   a.seg_incl = w.seg_incl;
   a.tinfo = w.tinfo;
   a.chunk_state = w.chunk_state;
@@ -308,6 +322,7 @@ struct parpa_result {
 
 extern "C" {
 
+const char *parpa_last_error(void) { return t_last_error; }
 const char *parpa_version(void) { return "parpa 0.1 (sm_100a, dense LUT path)"; }
 uint32_t parpa_chunk_bytes(void) { return CHUNK; }
 uint32_t parpa_tile_bytes(void) { return PTILE; }
@@ -605,7 +620,32 @@ static int parse_into_impl(const parpa_dfa *dfa, const parpa_schema *sch, const 
     a.left_len = left_len;
     a.is_last = is_last;
     uint32_t n = 0;
+    unsigned long long *prof = nullptr;
+    const bool dbg = getenv("PARPA_DEBUG") != nullptr;
+    if (dbg && cudaMallocAsync(&prof, 4096 * 16 * 8, s) == cudaSuccess) {
+      cudaMemsetAsync(prof, 0, 4096 * 16 * 8, s);
+      a.prof = prof;
+    }
     rc = launch_scan(MODE_EMIT, a, dfa->k, ck, s, &n);
+    if (prof) {
+      std::vector<unsigned long long> h(4096 * 16);
+      cudaMemcpyAsync(h.data(), prof, h.size() * 8, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      const char *nm[] = {"ticket", "A", "wait_TP", "B", "wait_SP", "C", "lbT_wait", "lbT_work", "lbS_wait",
+                          "lbS_work", "iters"};
+      double tot[16] = {0};
+      int nb = 0;
+      for (int b = 0; b < 4096; b++) {
+        if (!h[b * 16 + P_ITERS]) continue;
+        nb++;
+        for (int k = 0; k < P_NPROF; k++) tot[k] += (double)h[b * 16 + k];
+      }
+      fprintf(stderr, "[parpa] per-CTA mean cycles over %d CTAs:", nb);
+      for (int k = 0; k < P_NPROF; k++) fprintf(stderr, " %s=%.3g", nm[k], nb ? tot[k] / nb : 0.0);
+      fprintf(stderr, "\n");
+      cudaFreeAsync(prof, s);
+      a.prof = nullptr;
+    }
     if (!rc) rc = launch_tail(a, dfa->k, ck, s, &n);
     if (launches) *launches = n;
   }

@@ -27,7 +27,9 @@
 namespace parpa {
 
 constexpr int CHUNK = 64;                  // bytes per thread ("chunk")
-constexpr int TILE = CHUNK * 32;           // one warp tile = 2 KB; the unit of the decoupled look-back
+constexpr int WT = CHUNK * 32;             // one warp tile = 2 KB (a lane per 64-byte chunk)
+constexpr int CW = 14;                     // compute warps per CTA (+2 look-back warps = 512 threads)
+constexpr int PTILE = CW * WT;             // bytes per look-back tile (28 KB)
 constexpr int LUT_BYTES = 256 * 256;       // 64 KB shared-memory LUT
 constexpr uint32_t NIB_IDENT = 0x76543210u;
 constexpr uint32_t INV_DEV = 0xFu;

@@ -88,15 +88,20 @@ struct KArgs {
   unsigned long long row_base;       // global record index of local row 0
   unsigned long long cap;            // rows per column
   unsigned long long *tau_desc;      // [ntiles] (flag << 32) | nibble τ
-  uint32_t *seg_flag;                // [ntiles]
-  Seg *seg_agg, *seg_incl;           // [ntiles]
+  uint4 *seg_desc;                   // [ntiles] {SegT aggregate (tile-local), flag}: one 16-byte word
+  Seg *seg_incl;                     // [ntiles] inclusive prefix (valid once the flag says so)
   TileInfo *tinfo;                   // [ntiles]
   uint8_t *chunk_state;              // [ntiles * 32] device entry state of each chunk
   Ctrl *ctrl;
   DeferItem *dq;
   uint32_t dq_cap, strict;
   Stats *stats;
+  unsigned long long *prof;          // optional [gridDim][16] cycle counters (PARPA_DEBUG)
 };
+enum { P_TICKET, P_A, P_WAIT_TP, P_B, P_WAIT_SP, P_C, P_LBT_WAIT, P_LBT_WORK, P_LBS_WAIT, P_LBS_WORK, P_ITERS, P_NPROF };
+#define PROF_T0(x) unsigned long long x = a.prof ? clock64() : 0ull
+#define PROF_ADD(slot, t0) do { if (a.prof && (threadIdx.x & 31) == 0) { unsigned long long _n = clock64(); \
+  atomicAdd(a.prof + blockIdx.x * 16 + (slot), _n - (t0)); (t0) = _n; } } while (0)
 
 constexpr uint32_t FLAG_AGG = 1, FLAG_INCL = 2;
 
@@ -189,6 +194,88 @@ __device__ __forceinline__ uint32_t chunk_masks(const uint8_t *lut, const uint32
   return x & 0xFu;
 }
 
+// ---- 4-way ILP variants: the chunk is cut into four 16-byte quarters with independent chains ----
+// Pass 1 computes one τ per quarter (four independent PRMT chains) and composes them; pass 2 starts
+// each quarter from its own entry state, derived from the entry state and the quarter τ's, so its
+// four state chains are independent too.  qt[q] = nibble τ of quarter q (q = 0..2 needed later).
+template <bool FULL>
+__device__ __forceinline__ void chunk_tau4(const uint8_t *lut, const uint32_t (&v)[16], int nvalid,
+                                           uint32_t laneoff, uint32_t &t0, uint32_t &t1, uint32_t (&qt)[3]) {
+  uint32_t a0[4], a1[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) { a0[q] = 0x83828180u; a1[q] = 0x87868584u; }
+#pragma unroll
+  for (int i = 15; i >= 0; --i) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int b = 16 * q + i;
+      if (!FULL && b >= nvalid) continue;
+      uint32_t addr = prmt(v[b >> 2], laneoff, 0x5504u | ((uint32_t)(b & 3) << 4));
+      uint2 e = *reinterpret_cast<const uint2 *>(lut + addr);
+      uint32_t n0 = prmt(a0[q], a1[q], e.x);
+      uint32_t n1 = prmt(a0[q], a1[q], e.y);
+      a0[q] = n0;
+      a1[q] = n1;
+    }
+  }
+  uint32_t n[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) n[q] = pack_nib(a0[q], a1[q]);
+  qt[0] = n[0]; qt[1] = n[1]; qt[2] = n[2];
+  // chunk τ = n0 ∘ n1 ∘ n2 ∘ n3 (byte form for the warp scan): source = later, selector = earlier
+  uint32_t x0 = prmt(a0[3], a1[3], n[2]), x1 = prmt(a0[3], a1[3], n[2] >> 16);      // n2 ∘ n3
+  uint32_t y0 = prmt(a0[1], a1[1], n[0]), y1 = prmt(a0[1], a1[1], n[0] >> 16);      // n0 ∘ n1
+  uint32_t y = pack_nib(y0, y1);
+  t0 = prmt(x0, x1, y);                                                               // (n0∘n1)∘(n2∘n3)
+  t1 = prmt(x0, x1, y >> 16);
+}
+
+template <bool FULL>
+__device__ __forceinline__ uint32_t chunk_masks4(const uint8_t *lut, const uint32_t (&v)[16], int nvalid,
+                                                 uint32_t laneoff, uint32_t entry, const uint32_t (&qt)[3],
+                                                 unsigned long long &Dm, unsigned long long &Fm,
+                                                 unsigned long long &Rm) {
+  uint32_t x[4];
+  x[0] = 0x80u | entry;
+  x[1] = 0x80u | nib_at(qt[0], x[0] & 0xFu);
+  x[2] = 0x80u | nib_at(qt[1], x[1] & 0xFu);
+  x[3] = 0x80u | nib_at(qt[2], x[2] & 0xFu);
+  uint32_t d[2] = {0, 0}, f[2] = {0, 0}, r[2] = {0, 0};
+#pragma unroll
+  for (int ww = 0; ww < 4; ww++) {
+    uint32_t xs[4][4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int w = 4 * q + ww, b = 4 * w + k;
+        if (FULL || b < nvalid) {
+          uint32_t addr = prmt(v[w], laneoff, 0x5504u | ((uint32_t)k << 4));
+          uint2 st = *reinterpret_cast<const uint2 *>(lut + addr + 128);
+          x[q] = prmt(st.x, st.y, x[q]);
+          xs[q][k] = x[q];
+        } else {
+          xs[q][k] = 0xFFu;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int w = 4 * q + ww;
+      uint32_t pk = prmt(prmt(xs[q][0], xs[q][1], 0x0040u), prmt(xs[q][2], xs[q][3], 0x0040u), 0x5410u);
+      uint32_t npk = ~pk;
+      const int h = w >> 3, sh = 4 * (w & 7);
+      d[h] |= gather4(npk, 0x10101010u, 0x10204080u) << sh;
+      f[h] |= gather4(npk, 0x20202020u, 0x08102040u) << sh;
+      r[h] |= gather4(npk, 0x40404040u, 0x04081020u) << sh;
+    }
+  }
+  Dm = (unsigned long long)d[0] | ((unsigned long long)d[1] << 32);
+  Fm = (unsigned long long)f[0] | ((unsigned long long)f[1] << 32);
+  Rm = (unsigned long long)r[0] | ((unsigned long long)r[1] << 32);
+  return x[3] & 0xFu;
+}
+
 // scalar re-walk (rare): position of the first byte whose transition enters INV
 __device__ int first_inv_in_chunk(const uint8_t *lut, const uint8_t *p, int nvalid, uint32_t laneoff,
                                   uint32_t entry) {
@@ -235,35 +322,49 @@ __device__ __forceinline__ SegT warp_scan_segt(SegT s, SegT &agg) {            /
   return lane == 0 ? segt_ident() : ex;
 }
 
-// ---- decoupled look-back over τ (one warp) ---------------------------------------------------------
-// returns the exclusive prefix τ_0 ∘ ... ∘ τ_{t-1} of tile t (identity for t == 0)
+// ---- decoupled look-back over τ (one warp) -----------------------------------------------------
+// Window = 8 descriptors per lane = 256 tiles per memory round trip (all loads in flight at once),
+// combined per lane as a depth-3 tree and across lanes with shuffles.  Returns τ_0 ∘ ... ∘ τ_{t-1}.
+constexpr int LB_PER_LANE = 8;
 __device__ uint32_t lookback_tau(const KArgs &a, uint32_t t) {
   const int lane = threadIdx.x & 31;
   uint32_t acc = NIB_IDENT;
   long long base = (long long)t - 1;
   while (true) {
-    long long j = base - lane;
-    uint32_t val = NIB_IDENT, flag = FLAG_INCL;
-    if (j >= 0) {
-      unsigned long long dsc;
-      do {
-        dsc = ld_relaxed_u64(a.tau_desc + j);
-      } while ((dsc >> 32) == 0u);
-      flag = (uint32_t)(dsc >> 32);
-      val = (uint32_t)dsc;
-    }
-    unsigned m = __ballot_sync(0xffffffffu, flag == FLAG_INCL);
-    int k = m ? __ffs(m) - 1 : 31;
-    uint32_t w = lane <= k ? val : NIB_IDENT;
+    uint32_t v[LB_PER_LANE];
+    bool incl = false;
+    int kstar = LB_PER_LANE - 1;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {       // w <- w_{lane+d..} ∘ w   (farther tiles first)
+    for (int k = 0; k < LB_PER_LANE; k++) {
+      long long j = base - (long long)lane * LB_PER_LANE - k;
+      unsigned long long d = ((unsigned long long)FLAG_INCL << 32) | NIB_IDENT;
+      if (j >= 0) {
+        do {
+          d = ld_relaxed_u64(a.tau_desc + j);
+        } while ((d >> 32) == 0u);
+      }
+      v[k] = (uint32_t)d;
+      if (!incl && (d >> 32) == FLAG_INCL) { incl = true; kstar = k; }
+    }
+#pragma unroll
+    for (int k = 0; k < LB_PER_LANE; k++)
+      if (k > kstar) v[k] = NIB_IDENT;
+    // depth-3 tree: farther tiles first
+    uint32_t p0 = compose_nib(v[1], v[0]), p1 = compose_nib(v[3], v[2]);
+    uint32_t p2 = compose_nib(v[5], v[4]), p3 = compose_nib(v[7], v[6]);
+    uint32_t w = compose_nib(compose_nib(p3, p2), compose_nib(p1, p0));
+    unsigned m = __ballot_sync(0xffffffffu, incl);
+    int L = m ? __ffs(m) - 1 : 31;
+    if (lane > L) w = NIB_IDENT;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
       uint32_t o = __shfl_down_sync(0xffffffffu, w, d);
       if (lane + d < 32) w = compose_nib(o, w);
     }
     w = __shfl_sync(0xffffffffu, w, 0);
     acc = compose_nib(w, acc);
     if (m) break;
-    base -= 32;
+    base -= 32 * LB_PER_LANE;
   }
   return acc;
 }
@@ -308,36 +409,65 @@ __device__ __forceinline__ void stcg_seg(Seg *p, const Seg &s) {
   __stcg(&p->flags, s.flags);
 }
 
-// returns seed ∘ Seg_0 ∘ ... ∘ Seg_{t-1}
+__device__ __forceinline__ uint4 ld_relaxed_v4(const uint4 *p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_v4(uint4 *p, uint4 v) {
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+
+// returns seed ∘ Seg_0 ∘ ... ∘ Seg_{t-1}; window of 256 tiles per round trip (16-byte descriptors)
 __device__ Seg lookback_seg(const KArgs &a, uint32_t t) {
   const int lane = threadIdx.x & 31;
   Seg acc = seg_ident();
   long long base = (long long)t - 1;
   while (true) {
-    long long j = base - lane;
-    Seg val = seg_ident();
-    uint32_t flag = FLAG_INCL;
-    if (j >= 0) {
-      do {
-        flag = ld_relaxed_u32(a.seg_flag + j);       // spin without invalidating L1 every iteration
-      } while (flag == 0u);
-      flag = ld_acquire_u32(a.seg_flag + j);         // then one acquire orders the payload loads
-      val = ldcg_seg(flag == FLAG_INCL ? a.seg_incl + j : a.seg_agg + j);
-    } else if (j == -1) {
-      val = a.seed;
-    }
-    unsigned m = __ballot_sync(0xffffffffu, flag == FLAG_INCL);
-    int k = m ? __ffs(m) - 1 : 31;
-    Seg w = lane <= k ? val : seg_ident();
+    uint4 d[LB_PER_LANE];
+    bool incl = false;
+    int kstar = LB_PER_LANE - 1;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      Seg o = shfl_down_seg(w, d);
-      if (lane + d < 32) w = seg_op(o, w);
+    for (int k = 0; k < LB_PER_LANE; k++) {
+      long long j = base - (long long)lane * LB_PER_LANE - k;
+      d[k] = make_uint4(0u, 0u, 0xFFFFFFFFu, j == -1 ? FLAG_INCL : (j < -1 ? FLAG_INCL : 0u));
+      if (j >= 0) {
+        do {
+          d[k] = ld_relaxed_v4(a.seg_desc + j);
+        } while (d[k].w == 0u);
+      }
+      if (!incl && d[k].w == FLAG_INCL) { incl = true; kstar = k; }
+    }
+    Seg v[LB_PER_LANE];
+    if (incl) __threadfence();                         // acquire side for the inclusive payload below
+#pragma unroll
+    for (int k = 0; k < LB_PER_LANE; k++) {
+      long long j = base - (long long)lane * LB_PER_LANE - k;
+      if (k > kstar) {
+        v[k] = seg_ident();
+      } else if (k == kstar && incl) {
+        v[k] = j >= 0 ? ldcg_seg(a.seg_incl + j) : (j == -1 ? a.seed : seg_ident());
+      } else {
+        v[k] = segt_to_seg(SegT{d[k].x, d[k].y, d[k].z}, a.base + (unsigned long long)j * PTILE);
+      }
+    }
+    Seg p0 = seg_op(v[1], v[0]), p1 = seg_op(v[3], v[2]);
+    Seg p2 = seg_op(v[5], v[4]), p3 = seg_op(v[7], v[6]);
+    Seg w = seg_op(seg_op(p3, p2), seg_op(p1, p0));
+    unsigned m = __ballot_sync(0xffffffffu, incl);
+    int L = m ? __ffs(m) - 1 : 31;
+    if (lane > L) w = seg_ident();
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      Seg o = shfl_down_seg(w, dd);
+      if (lane + dd < 32) w = seg_op(o, w);
     }
     w = shfl_seg(w, 0);
     acc = seg_op(w, acc);
     if (m) break;
-    base -= 32;
+    base -= 32 * LB_PER_LANE;
   }
   return acc;
 }
@@ -491,7 +621,6 @@ __device__ __forceinline__ void flush_counters(const KArgs &a, EmitCounters &cnt
 //     so the column-major stores coalesce and every lane runs the same converter (no type
 //     divergence).  Digits come from the warp's shared-memory copy of its tile.  This is the paper's
 //     "partition by column, then convert per column" at warp-tile granularity.
-constexpr int WT = 32 * CHUNK;              // bytes per warp tile
 constexpr int FCAP = 512;                   // fields per warp tile handled by E1/E2
 constexpr int RCAP = 128;                   // records per warp tile handled by E1/E2
 struct WarpScratch {
@@ -615,9 +744,15 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   const uint32_t nrows = nrec + (nf > last_end ? 1u : 0u);
   const uint32_t c0 = prefix.col;
   const unsigned long long r0 = prefix.recs;
-  for (uint32_t c = 0; c < a.C; c++) {
+  // (column, row) items flattened over the lanes, column-major: consecutive lanes hold consecutive
+  // rows of one column (coalesced stores); a warp touches at most two columns per step.
+  const uint32_t total = a.C * nrows;
+  const float rcp = nrows ? 1.0f / (float)nrows : 0.f;
+  for (uint32_t it = lane; it < total; it += 32) {
+    uint32_t c = __float2uint_rz(((float)it + 0.5f) * rcp);
+    uint32_t jr = it - c * nrows;
     const ColDesc *cd = cols + c;
-    for (uint32_t jr = lane; jr < nrows; jr += 32) {
+    {
       uint32_t start = jr == 0 ? 0u : (ws->rows[jr - 1] & 0xFFFFu);
       uint32_t end = jr < nrec ? (ws->rows[jr] & 0xFFFFu) : nf;
       uint32_t cs = jr == 0 ? c0 : 0u;
@@ -660,93 +795,116 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
 // record/column summaries of tile i-1.  Nothing waits for the current tile's look-back: the chains
 // advance a full pipeline stage behind the compute.  The tile bytes are re-read from L2 (not DRAM)
 // in stages B and C.
-constexpr int CW = 16;                              // compute warps per CTA
-constexpr int PTILE = CW * WT;                      // bytes per look-back tile (32 KB)
 
 struct PipeSmem {
   uint64_t mbA[2], mbTP[2], mbB[2], mbSP[2];
   uint32_t tile_id[4];
+  uint32_t tile_id2[4];                             // tile of stage B, for the record/column warp
   uint32_t wtau[2][CW];                             // warp τ aggregates (nibble form)
   uint32_t wentry[2][CW];                           // warp entry states (device numbering)
   SegT wseg[2][CW];                                 // warp summaries (positions warp-tile-local)
   Seg wpre[2][CW];                                  // warp prefixes (global)
+  uint32_t cntA[2], cntB[2];                        // arrival counters: the last warp publishes
+  uint32_t wexT[2][32];                             // per-warp exclusive τ within the tile
+  uint32_t aggT[2];                                 // tile τ aggregate
+  SegT wexS[2][32];                                 // per-warp exclusive summary within the tile
+  SegT saggS[2];                                    // tile summary aggregate (tile-local positions)
 };
 
+constexpr size_t SCRATCH_OFF = (LUT_BYTES + sizeof(PipeSmem) + 127) / 128 * 128;
 template <int MODE>
 struct ScanCfg {
-  static constexpr int THREADS = (CW + 1) * 32;
-  static constexpr size_t SMEM = LUT_BYTES + sizeof(PipeSmem) + (MODE == MODE_EMIT ? CW * sizeof(WarpScratch) : 0);
+  static constexpr int THREADS = (CW + 2) * 32;
+  static constexpr size_t SMEM = SCRATCH_OFF + (MODE == MODE_EMIT ? CW * sizeof(WarpScratch) : 0);
 };
 
 // Look-back warp, in two halves per chain so that a tile's aggregate is always published before this
 // warp blocks in any look-back (publishing never waits; look-backs only wait on smaller tiles, so the
 // smallest blocked look-back always makes progress — no cross-CTA cycles).
-struct LbTau { uint32_t wex, agg; };
-struct LbSeg { SegT wex; Seg agg; };
-
-__device__ __forceinline__ LbTau lb_tau_publish(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t) {
+// Aggregate publication is done by the LAST compute warp to finish a stage (smem arrival counter),
+// right when the tile's data is complete — never behind a look-back.  The look-back warps only chase.
+__device__ __forceinline__ void publish_tau(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t) {
   const int lane = threadIdx.x & 31;
   uint32_t w = lane < CW ? sm.wtau[slot][lane] : NIB_IDENT;
-  LbTau r;
-  r.wex = warp_scan_tau(spread16(w), spread16(w >> 16), r.agg);
-  if (lane == 0) st_relaxed_u64(a.tau_desc + t, ((unsigned long long)(t == 0 ? FLAG_INCL : FLAG_AGG) << 32) | r.agg);
-  return r;
+  uint32_t agg;
+  uint32_t wex = warp_scan_tau(spread16(w), spread16(w >> 16), agg);
+  sm.wexT[slot][lane] = wex;
+  if (lane == 0) {
+    sm.aggT[slot] = agg;
+    st_relaxed_u64(a.tau_desc + t, ((unsigned long long)(t == 0 ? FLAG_INCL : FLAG_AGG) << 32) | agg);
+  }
 }
-__device__ __forceinline__ void lb_tau_finish(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t, const LbTau &r) {
+__device__ __forceinline__ void publish_seg(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t) {
+  const int lane = threadIdx.x & 31;
+  SegT w = lane < CW ? segt_shift(sm.wseg[slot][lane], (uint32_t)lane * WT) : segt_ident();
+  SegT sagg;
+  SegT wex = warp_scan_segt(w, sagg);
+  sm.wexS[slot][lane] = wex;
+  if (lane == 0) {
+    sm.saggS[slot] = sagg;
+    if (t == 0) {
+      stcg_seg(a.seg_incl, seg_op(a.seed, segt_to_seg(sagg, a.base)));
+      __threadfence();
+      st_relaxed_v4(a.seg_desc, make_uint4(sagg.cnt, sagg.colf, sagg.pos, FLAG_INCL));
+    } else {
+      st_relaxed_v4(a.seg_desc + t, make_uint4(sagg.cnt, sagg.colf, sagg.pos, FLAG_AGG));
+    }
+  }
+}
+__device__ __forceinline__ void lb_tau_finish(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t) {
   const int lane = threadIdx.x & 31;
   uint32_t prefix = NIB_IDENT;
   if (t != 0) {
     prefix = lookback_tau(a, t);
-    if (lane == 0) st_relaxed_u64(a.tau_desc + t, ((unsigned long long)FLAG_INCL << 32) | compose_nib(prefix, r.agg));
+    if (lane == 0)
+      st_relaxed_u64(a.tau_desc + t, ((unsigned long long)FLAG_INCL << 32) | compose_nib(prefix, sm.aggT[slot]));
   }
   const uint32_t tile_entry = nib_at(prefix, a.seed_dev);
   if (lane < CW) {
-    uint32_t e = nib_at(r.wex, tile_entry);
+    uint32_t e = nib_at(sm.wexT[slot][lane], tile_entry);
     sm.wentry[slot][lane] = e;
     a.tinfo[(unsigned long long)t * CW + lane].entry = e;
   }
 }
-__device__ __forceinline__ LbSeg lb_seg_publish(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t) {
+__device__ __forceinline__ void lb_seg_finish(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t) {
   const int lane = threadIdx.x & 31;
-  SegT w = lane < CW ? segt_shift(sm.wseg[slot][lane], (uint32_t)lane * WT) : segt_ident();
-  SegT sagg;
-  LbSeg r;
-  r.wex = warp_scan_segt(w, sagg);
-  r.agg = segt_to_seg(sagg, a.base + (unsigned long long)t * PTILE);
-  if (lane == 0) {
-    if (t == 0) {
-      stcg_seg(a.seg_incl, seg_op(a.seed, r.agg));
-      st_release_u32(a.seg_flag, FLAG_INCL);
-    } else {
-      stcg_seg(a.seg_agg + t, r.agg);
-      st_release_u32(a.seg_flag + t, FLAG_AGG);
-    }
-  }
-  return r;
-}
-__device__ __forceinline__ void lb_seg_finish(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t, const LbSeg &r) {
-  const int lane = threadIdx.x & 31;
+  const unsigned long long tb = a.base + (unsigned long long)t * PTILE;
   Seg prefix = a.seed;
   if (t != 0) {
     prefix = lookback_seg(a, t);
     if (lane == 0) {
-      stcg_seg(a.seg_incl + t, seg_op(prefix, r.agg));
-      st_release_u32(a.seg_flag + t, FLAG_INCL);
+      SegT sagg = sm.saggS[slot];
+      stcg_seg(a.seg_incl + t, seg_op(prefix, segt_to_seg(sagg, tb)));
+      __threadfence();
+      st_relaxed_v4(a.seg_desc + t, make_uint4(sagg.cnt, sagg.colf, sagg.pos, FLAG_INCL));
     }
   }
   if (lane < CW) {
-    Seg wp = seg_op(prefix, segt_to_seg(r.wex, a.base + (unsigned long long)t * PTILE));
+    Seg wp = seg_op(prefix, segt_to_seg(sm.wexS[slot][lane], tb));
     sm.wpre[slot][lane] = wp;
     a.tinfo[(unsigned long long)t * CW + lane].excl = wp;
   }
 }
 
+// the last warp to arrive at a stage publishes the tile aggregate
+__device__ __forceinline__ bool last_arrival(uint32_t *cnt) {
+  uint32_t old = 0;
+  if ((threadIdx.x & 31) == 0) {
+    __threadfence_block();
+    old = atomicAdd(cnt, 1u);
+    if (old == CW - 1) atomicExch(cnt, 0u);
+  }
+  old = __shfl_sync(0xffffffffu, old, 0);
+  if (old == CW - 1) __threadfence_block();
+  return old == CW - 1;
+}
+
 template <int MODE>
-__global__ void __maxnreg__(120) k_scan(const KArgs a, const DfaK dfa, const ColsK colsk) {
-  extern __shared__ __align__(16) uint8_t smem[];
+__global__ void __launch_bounds__(ScanCfg<MODE>::THREADS, 1) k_scan(const KArgs a, const DfaK dfa, const ColsK colsk) {
+  extern __shared__ __align__(128) uint8_t smem[];
   uint8_t *lut = smem;
   PipeSmem &sm = *reinterpret_cast<PipeSmem *>(smem + LUT_BYTES);
-  WarpScratch *scratch = reinterpret_cast<WarpScratch *>(smem + LUT_BYTES + sizeof(PipeSmem));
+  WarpScratch *scratch = reinterpret_cast<WarpScratch *>(smem + SCRATCH_OFF);
   __shared__ ColDesc s_cols[MODE == MODE_EMIT ? MAX_COLS : 1];
   build_lut(lut, dfa);
   if (MODE == MODE_EMIT)
@@ -754,6 +912,7 @@ __global__ void __maxnreg__(120) k_scan(const KArgs a, const DfaK dfa, const Col
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; s++) {
+      sm.cntA[s] = sm.cntB[s] = 0;
       mbar_init(&sm.mbA[s], CW);
       mbar_init(&sm.mbTP[s], 1);
       mbar_init(&sm.mbB[s], CW);
@@ -761,34 +920,35 @@ __global__ void __maxnreg__(120) k_scan(const KArgs a, const DfaK dfa, const Col
     }
   }
   __syncthreads();                                          // the only CTA-wide barrier
-  if (warp == CW) {
-    // ================= look-back warp =================
-    bool prev_valid = false;
-    uint32_t t_prev = 0;
-    for (uint32_t i = 0;; i++) {
-      LbSeg rs;
-      const bool do_seg = MODE != MODE_TAU && i >= 1;
-      if (do_seg) {                                          // publish tile i-1's summary aggregate
-        mbar_wait(&sm.mbB[(i - 1) & 1], ((i - 1) >> 1) & 1);
-        if (prev_valid) rs = lb_seg_publish(a, sm, (i - 1) & 1, t_prev);
-      }
-      mbar_wait(&sm.mbA[i & 1], (i >> 1) & 1);
-      const uint32_t t = sm.tile_id[i & 3];
-      const bool valid = t < a.ntiles;
-      if (valid) {                                           // publish tile i's τ aggregate, then chase
-        LbTau rt = lb_tau_publish(a, sm, i & 1, t);
-        lb_tau_finish(a, sm, i & 1, t, rt);
+  if (warp >= CW) {
+    // ================= look-back warps =================
+    // warp CW: the τ chain (S3); warp CW+1: the record/column chain (S5).  Each publishes a tile's
+    // aggregate before it can block in that tile's look-back, and neither waits on the other, so the
+    // smallest blocked look-back in the grid always progresses.
+    if (warp == CW) {
+      PROF_T0(pt);
+      for (uint32_t i = 0;; i++) {
+        mbar_wait(&sm.mbA[i & 1], (i >> 1) & 1);
+        PROF_ADD(P_LBT_WAIT, pt);
+        const uint32_t t = sm.tile_id[i & 3];
+        if (t >= a.ntiles) break;
+        lb_tau_finish(a, sm, i & 1, t);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.mbTP[i & 1]);
+        PROF_ADD(P_LBT_WORK, pt);
       }
-      if (do_seg && prev_valid) {
-        lb_seg_finish(a, sm, (i - 1) & 1, t_prev, rs);
+    } else if (MODE != MODE_TAU) {
+      PROF_T0(pt);
+      for (uint32_t i = 0;; i++) {
+        mbar_wait(&sm.mbB[i & 1], (i >> 1) & 1);             // stage B of tile i done (or tile invalid)
+        PROF_ADD(P_LBS_WAIT, pt);
+        const uint32_t t = sm.tile_id2[i & 3];
+        if (t >= a.ntiles) break;
+        lb_seg_finish(a, sm, i & 1, t);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.mbSP[(i - 1) & 1]);
+        if (lane == 0) mbar_arrive(&sm.mbSP[i & 1]);
+        PROF_ADD(P_LBS_WORK, pt);
       }
-      if (!valid) break;
-      prev_valid = valid;
-      t_prev = t;
     }
     return;
   }
@@ -801,6 +961,7 @@ __global__ void __maxnreg__(120) k_scan(const KArgs a, const DfaK dfa, const Col
   uint32_t vA[16], vB[16];
   int nvA = 0, nvB = 0;
   uint32_t tA = 0xFFFFFFFFu, exB = NIB_IDENT;
+  uint32_t qtB[3] = {NIB_IDENT, NIB_IDENT, NIB_IDENT};
   unsigned long long wtB = 0, wtC = 0;
   bool validA = false, validB = false, validC = false;
   unsigned long long DmC = 0, FmC = 0, RmC = 0, VmC = 0;
@@ -815,10 +976,15 @@ __global__ void __maxnreg__(120) k_scan(const KArgs a, const DfaK dfa, const Col
     nvA = cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
     load_chunk(a.in + cstart, nvA, vA);
   }
+  const bool prof0 = a.prof && warp == 0;
+  unsigned long long pt = prof0 ? clock64() : 0ull;
+#define CPROF(slot) do { if (prof0 && lane == 0) { unsigned long long _n = clock64(); \
+  atomicAdd(a.prof + blockIdx.x * 16 + (slot), _n - pt); pt = _n; } } while (0)
   for (uint32_t i = 0;; i++) {
     // ---- claim tile i+1 and issue its loads (they land while A/B/C below compute) ----
     if (warp == 0 && lane == 0) sm.tile_id[(i + 1) & 3] = atomicAdd(&a.ctrl->ticket, 1u);
     named_bar_sync(1, CW * 32);
+    CPROF(P_TICKET);
     const uint32_t tN = sm.tile_id[(i + 1) & 3];
     const bool validN = tN < a.ntiles;
     uint32_t vN[16];
@@ -830,29 +996,36 @@ __global__ void __maxnreg__(120) k_scan(const KArgs a, const DfaK dfa, const Col
     }
     // ---- A(i): τ of the chunk, warp scan ----
     uint32_t exA = NIB_IDENT;
+    uint32_t qtA[3] = {NIB_IDENT, NIB_IDENT, NIB_IDENT};
     const unsigned long long wtA = (unsigned long long)tA * CW + warp;
     if (validA) {
       uint32_t t0, t1, agg;
-      if (nvA == CHUNK) chunk_tau<true>(lut, vA, nvA, laneoff, t0, t1);
-      else chunk_tau<false>(lut, vA, nvA, laneoff, t0, t1);
+      if (nvA == CHUNK) chunk_tau4<true>(lut, vA, nvA, laneoff, t0, t1, qtA);
+      else chunk_tau4<false>(lut, vA, nvA, laneoff, t0, t1, qtA);
       exA = warp_scan_tau(t0, t1, agg);
       if (lane == 0) sm.wtau[i & 1][warp] = agg;
+      __syncwarp();
+      if (last_arrival(&sm.cntA[i & 1])) publish_tau(a, sm, i & 1, (uint32_t)tA);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.mbA[i & 1]);
+    CPROF(P_A);
     // TAU-only mode: stay at most one tile ahead of the look-back warp (mbarrier phases, smem slots)
     if (MODE == MODE_TAU && i >= 1 && validB) mbar_wait(&sm.mbTP[(i - 1) & 1], ((i - 1) >> 1) & 1);
     // ---- B(i-1): entry states, masks, summary scan ----
     if (MODE != MODE_TAU && i >= 1) {
+      if (warp == 0 && lane == 0) sm.tile_id2[(i - 1) & 3] = validB ? (uint32_t)(wtB / CW) : 0xFFFFFFFFu;
       if (validB) {
         if (MODE == MODE_EMIT) stash_chunk(ws->bytes[(i - 1) & 1], lane, vB);
+        CPROF(P_B);
         mbar_wait(&sm.mbTP[(i - 1) & 1], ((i - 1) >> 1) & 1);
+        CPROF(P_WAIT_TP);
         const uint32_t entry = nib_at(exB, sm.wentry[(i - 1) & 1][warp]);
         a.chunk_state[wtB * 32 + lane] = (uint8_t)entry;
         unsigned long long Dm, Fm, Rm;
         uint32_t fin;
-        if (nvB == CHUNK) fin = chunk_masks<true>(lut, vB, nvB, laneoff, entry, Dm, Fm, Rm);
-        else fin = chunk_masks<false>(lut, vB, nvB, laneoff, entry, Dm, Fm, Rm);
+        if (nvB == CHUNK) fin = chunk_masks4<true>(lut, vB, nvB, laneoff, entry, qtB, Dm, Fm, Rm);
+        else fin = chunk_masks4<false>(lut, vB, nvB, laneoff, entry, qtB, Dm, Fm, Rm);
         const unsigned long long cstart = wtB * WT + (unsigned long long)lane * CHUNK;
         if (fin == INV_DEV && entry != INV_DEV && nvB > 0) {
           int p = first_inv_in_chunk(lut, a.in + cstart, nvB, laneoff, entry);
@@ -863,19 +1036,27 @@ __global__ void __maxnreg__(120) k_scan(const KArgs a, const DfaK dfa, const Col
         const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
         if (lane == 0) sm.wseg[(i - 1) & 1][warp] = sagg;
         DmC = Dm; FmC = Fm; RmC = Rm; VmC = Vm; sexC = sex; saggC = sagg;
+        __syncwarp();
+        if (last_arrival(&sm.cntB[(i - 1) & 1])) publish_seg(a, sm, (i - 1) & 1, (uint32_t)(wtB / CW));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sm.mbB[(i - 1) & 1]);
+      CPROF(P_B);
     }
+    // COUNT mode: stay at most two tiles ahead of the record/column warp
+    if (MODE == MODE_COUNT && i >= 2 && validC) mbar_wait(&sm.mbSP[(i - 2) & 1], ((i - 2) >> 1) & 1);
     // ---- C(i-2): emission ----
     if (MODE == MODE_EMIT && i >= 2 && validC) {
       mbar_wait(&sm.mbSP[(i - 2) & 1], ((i - 2) >> 1) & 1);
+      CPROF(P_WAIT_SP);
       const Seg wprefix = sm.wpre[(i - 2) & 1][warp];
       const unsigned long long cstart = wtC * WT + (unsigned long long)lane * CHUNK;
       const Seg st = seg_op(wprefix, segt_to_seg(sexC, a.base + wtC * WT));
       emit_tile(a, s_cols, ws, ws->bytes[(i - 2) & 1], st, sexC, saggC, wprefix, DmC, FmC, RmC, VmC,
                 a.base + wtC * WT, a.base + cstart, cnt);
+      CPROF(P_C);
     }
+    if (prof0 && lane == 0) atomicAdd(a.prof + blockIdx.x * 16 + P_ITERS, 1ull);
     const bool done = MODE == MODE_EMIT ? (i >= 2 && !validC) : (i >= 1 && !validB);
     if (done) break;
     // ---- rotate the pipeline ----
@@ -884,6 +1065,7 @@ __global__ void __maxnreg__(120) k_scan(const KArgs a, const DfaK dfa, const Col
     validB = validA;
     wtB = wtA;
     exB = exA;
+    qtB[0] = qtA[0]; qtB[1] = qtA[1]; qtB[2] = qtA[2];
     nvB = nvA;
 #pragma unroll
     for (int k = 0; k < 16; k++) vB[k] = vA[k];
