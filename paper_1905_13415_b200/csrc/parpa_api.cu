@@ -632,16 +632,16 @@ static int parse_into_impl(const parpa_dfa *dfa, const parpa_schema *sch, const 
       cudaMemcpyAsync(h.data(), prof, h.size() * 8, cudaMemcpyDeviceToHost, s);
       cudaStreamSynchronize(s);
       const char *nm[] = {"ticket", "A", "wait_TP", "B", "wait_SP", "C", "lbT_wait", "lbT_work", "lbS_wait",
-                          "lbS_work", "iters"};
+                          "lbS_work", "iters", "lbT_windows", "lbT_spins", "lbS_windows", "lbS_spins"};
       double tot[16] = {0};
       int nb = 0;
       for (int b = 0; b < 4096; b++) {
         if (!h[b * 16 + P_ITERS]) continue;
         nb++;
-        for (int k = 0; k < P_NPROF; k++) tot[k] += (double)h[b * 16 + k];
+        for (int k = 0; k < 15; k++) tot[k] += (double)h[b * 16 + k];
       }
       fprintf(stderr, "[parpa] per-CTA mean cycles over %d CTAs:", nb);
-      for (int k = 0; k < P_NPROF; k++) fprintf(stderr, " %s=%.3g", nm[k], nb ? tot[k] / nb : 0.0);
+      for (int k = 0; k < 15; k++) fprintf(stderr, " %s=%.3g", nm[k], nb ? tot[k] / nb : 0.0);
       fprintf(stderr, "\n");
       cudaFreeAsync(prof, s);
       a.prof = nullptr;

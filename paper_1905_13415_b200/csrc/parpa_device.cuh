@@ -254,9 +254,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
-      "r"(parity)
+      "r"(parity), "r"(1000000u)                            /* suspend up to 1 ms: sleep, don't poll */
       : "memory");
 }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {

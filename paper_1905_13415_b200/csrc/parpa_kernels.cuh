@@ -330,26 +330,40 @@ __device__ uint32_t lookback_tau(const KArgs &a, uint32_t t) {
   const int lane = threadIdx.x & 31;
   uint32_t acc = NIB_IDENT;
   long long base = (long long)t - 1;
+  unsigned long long nwin = 0, nspin = 0;
   while (true) {
+    unsigned long long d[LB_PER_LANE];
+#pragma unroll
+    for (int k = 0; k < LB_PER_LANE; k++) {                  // all loads in flight at once
+      long long j = base - (long long)lane * LB_PER_LANE - k;
+      d[k] = j >= 0 ? ld_relaxed_u64(a.tau_desc + j) : (((unsigned long long)FLAG_INCL << 32) | NIB_IDENT);
+    }
+    nwin++;
+    while (true) {                                            // re-poll only the unpublished ones
+      bool missing = false;
+#pragma unroll
+      for (int k = 0; k < LB_PER_LANE; k++) {
+        long long j = base - (long long)lane * LB_PER_LANE - k;
+        if ((d[k] >> 32) == 0u) {
+          d[k] = ld_relaxed_u64(a.tau_desc + j);
+          missing = true;
+        }
+      }
+      if (!__any_sync(0xffffffffu, missing)) break;
+      nspin++;
+      __nanosleep(64);
+    }
     uint32_t v[LB_PER_LANE];
     bool incl = false;
     int kstar = LB_PER_LANE - 1;
 #pragma unroll
     for (int k = 0; k < LB_PER_LANE; k++) {
-      long long j = base - (long long)lane * LB_PER_LANE - k;
-      unsigned long long d = ((unsigned long long)FLAG_INCL << 32) | NIB_IDENT;
-      if (j >= 0) {
-        do {
-          d = ld_relaxed_u64(a.tau_desc + j);
-        } while ((d >> 32) == 0u);
-      }
-      v[k] = (uint32_t)d;
-      if (!incl && (d >> 32) == FLAG_INCL) { incl = true; kstar = k; }
+      v[k] = (uint32_t)d[k];
+      if (!incl && (d[k] >> 32) == FLAG_INCL) { incl = true; kstar = k; }
     }
 #pragma unroll
     for (int k = 0; k < LB_PER_LANE; k++)
       if (k > kstar) v[k] = NIB_IDENT;
-    // depth-3 tree: farther tiles first
     uint32_t p0 = compose_nib(v[1], v[0]), p1 = compose_nib(v[3], v[2]);
     uint32_t p2 = compose_nib(v[5], v[4]), p3 = compose_nib(v[7], v[6]);
     uint32_t w = compose_nib(compose_nib(p3, p2), compose_nib(p1, p0));
@@ -357,14 +371,18 @@ __device__ uint32_t lookback_tau(const KArgs &a, uint32_t t) {
     int L = m ? __ffs(m) - 1 : 31;
     if (lane > L) w = NIB_IDENT;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      uint32_t o = __shfl_down_sync(0xffffffffu, w, d);
-      if (lane + d < 32) w = compose_nib(o, w);
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      uint32_t o = __shfl_down_sync(0xffffffffu, w, dd);
+      if (lane + dd < 32) w = compose_nib(o, w);
     }
     w = __shfl_sync(0xffffffffu, w, 0);
     acc = compose_nib(w, acc);
     if (m) break;
     base -= 32 * LB_PER_LANE;
+  }
+  if (a.prof && lane == 0) {
+    atomicAdd(a.prof + blockIdx.x * 16 + 11, nwin);
+    atomicAdd(a.prof + blockIdx.x * 16 + 12, nspin);
   }
   return acc;
 }
@@ -425,21 +443,34 @@ __device__ Seg lookback_seg(const KArgs &a, uint32_t t) {
   const int lane = threadIdx.x & 31;
   Seg acc = seg_ident();
   long long base = (long long)t - 1;
+  unsigned long long nwin = 0, nspin = 0;
   while (true) {
     uint4 d[LB_PER_LANE];
+#pragma unroll
+    for (int k = 0; k < LB_PER_LANE; k++) {                  // all loads in flight at once
+      long long j = base - (long long)lane * LB_PER_LANE - k;
+      d[k] = j >= 0 ? ld_relaxed_v4(a.seg_desc + j) : make_uint4(0u, 0u, 0xFFFFFFFFu, FLAG_INCL);
+    }
+    nwin++;
+    while (true) {
+      bool missing = false;
+#pragma unroll
+      for (int k = 0; k < LB_PER_LANE; k++) {
+        long long j = base - (long long)lane * LB_PER_LANE - k;
+        if (d[k].w == 0u) {
+          d[k] = ld_relaxed_v4(a.seg_desc + j);
+          missing = true;
+        }
+      }
+      if (!__any_sync(0xffffffffu, missing)) break;
+      nspin++;
+      __nanosleep(64);
+    }
     bool incl = false;
     int kstar = LB_PER_LANE - 1;
 #pragma unroll
-    for (int k = 0; k < LB_PER_LANE; k++) {
-      long long j = base - (long long)lane * LB_PER_LANE - k;
-      d[k] = make_uint4(0u, 0u, 0xFFFFFFFFu, j == -1 ? FLAG_INCL : (j < -1 ? FLAG_INCL : 0u));
-      if (j >= 0) {
-        do {
-          d[k] = ld_relaxed_v4(a.seg_desc + j);
-        } while (d[k].w == 0u);
-      }
+    for (int k = 0; k < LB_PER_LANE; k++)
       if (!incl && d[k].w == FLAG_INCL) { incl = true; kstar = k; }
-    }
     Seg v[LB_PER_LANE];
     if (incl) __threadfence();                         // acquire side for the inclusive payload below
 #pragma unroll
@@ -468,6 +499,10 @@ __device__ Seg lookback_seg(const KArgs &a, uint32_t t) {
     acc = seg_op(w, acc);
     if (m) break;
     base -= 32 * LB_PER_LANE;
+  }
+  if (a.prof && lane == 0) {
+    atomicAdd(a.prof + blockIdx.x * 16 + 13, nwin);
+    atomicAdd(a.prof + blockIdx.x * 16 + 14, nspin);
   }
   return acc;
 }
