@@ -6,7 +6,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libparpa.so")
+LIB_PATH = os.environ.get("PARPA_LIB") or os.path.join(HERE, "libparpa.so")  # PARPA_LIB: A/B builds
 
 c_u8p = ctypes.POINTER(ctypes.c_uint8)
 
@@ -65,7 +65,7 @@ def load(build_if_missing: bool = True):
     with _lock:
         if _lib is not None:
             return _lib
-        if build_if_missing:
+        if build_if_missing and not os.environ.get("PARPA_LIB"):
             from . import build as _build
             try:
                 _build.build()

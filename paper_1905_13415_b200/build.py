@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libparpa.so")
 SOURCES = ["parpa_api.cu"]
-HEADERS = ["parpa_device.cuh", "parpa_kernels.cuh", "parpa_convert.cuh"]
+HEADERS = ["parpa_device.cuh", "parpa_kernels.cuh", "parpa_passes.cuh", "parpa_convert.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 

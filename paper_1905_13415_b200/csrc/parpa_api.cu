@@ -47,8 +47,7 @@ int cuda_status(cudaError_t e) {
 struct DevCfg {
   bool init = false;
   int sms = 0;
-  int occ_scan[3] = {0, 0, 0};
-  int occ_emit = 0;
+  int occ_pass1 = 0, occ_pass2 = 0, occ_emit = 0;
 };
 std::mutex g_mu;
 DevCfg g_dev[64];
@@ -61,13 +60,11 @@ int dev_cfg(DevCfg **out) {
   DevCfg &c = g_dev[dev];
   if (!c.init) {
     CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaFuncSetAttribute(k_scan<MODE_TAU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ScanCfg<MODE_TAU>::SMEM));
-    CK(cudaFuncSetAttribute(k_scan<MODE_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ScanCfg<MODE_COUNT>::SMEM));
-    CK(cudaFuncSetAttribute(k_scan<MODE_EMIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ScanCfg<MODE_EMIT>::SMEM));
+    CK(cudaFuncSetAttribute(k_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, LUT_BYTES));
+    CK(cudaFuncSetAttribute(k_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, LUT_BYTES));
     CK(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[0], k_scan<MODE_TAU>, ScanCfg<MODE_TAU>::THREADS, ScanCfg<MODE_TAU>::SMEM));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[1], k_scan<MODE_COUNT>, ScanCfg<MODE_COUNT>::THREADS, ScanCfg<MODE_COUNT>::SMEM));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_scan[2], k_scan<MODE_EMIT>, ScanCfg<MODE_EMIT>::THREADS, ScanCfg<MODE_EMIT>::SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass1, k_pass1, PASS_WARPS * 32, LUT_BYTES));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass2, k_pass2, PASS_WARPS * 32, LUT_BYTES));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit, EMIT_WARPS * 32, EMIT_SMEM));
     if (getenv("PARPA_DEBUG")) {
       auto show = [](const char *n, const void *f) {
@@ -76,12 +73,12 @@ int dev_cfg(DevCfg **out) {
           fprintf(stderr, "[parpa] %s: regs=%d maxThreads=%d static_smem=%zu local=%zu maxDynSmem=%d\n", n, fa.numRegs,
                   fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.localSizeBytes, fa.maxDynamicSharedSizeBytes);
       };
-      show("k_scan<TAU>", (const void *)k_scan<MODE_TAU>);
-      show("k_scan<COUNT>", (const void *)k_scan<MODE_COUNT>);
-      show("k_scan<EMIT>", (const void *)k_scan<MODE_EMIT>);
+      show("k_pass1", (const void *)k_pass1);
+      show("k_tau_scan", (const void *)k_tau_scan);
+      show("k_pass2", (const void *)k_pass2);
+      show("k_seg_scan", (const void *)k_seg_scan);
       show("k_emit", (const void *)k_emit);
-      fprintf(stderr, "[parpa] occ tau=%d count=%d emit=%d k_emit=%d sms=%d smem(emit)=%zu\n", c.occ_scan[0],
-              c.occ_scan[1], c.occ_scan[2], c.occ_emit, c.sms, (size_t)ScanCfg<MODE_EMIT>::SMEM);
+      fprintf(stderr, "[parpa] occ pass1=%d pass2=%d emit=%d sms=%d\n", c.occ_pass1, c.occ_pass2, c.occ_emit, c.sms);
     }
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -137,48 +134,65 @@ void prof_clear() {
 // ---- workspace ------------------------------------------------------------------------------
 struct Work {
   void *block = nullptr;
-  size_t zero_bytes = 0;
   unsigned long long *tau_desc = nullptr;
-  uint4 *seg_desc = nullptr;
+  uint32_t *bflag = nullptr;
   Ctrl *ctrl = nullptr;
-  Seg *seg_incl = nullptr;
+  uint32_t *lex = nullptr, *wtau = nullptr, *tot_tau = nullptr;
+  uint8_t *wentry = nullptr;
+  uint4 *wseg = nullptr;
+  Seg *bagg = nullptr, *bincl = nullptr, *tot_seg = nullptr;
   TileInfo *tinfo = nullptr;
   uint8_t *chunk_state = nullptr;
   DeferItem *dq = nullptr;
   Stats *stats = nullptr;
   uint8_t *aligned_in = nullptr;
-  uint32_t ntiles = 0, dq_cap = 0;
+  uint32_t ntiles = 0, nblk = 0, dq_cap = 0;
 };
 
+// One cudaMallocAsync block per call: the look-back descriptors and control words (zeroed), then the
+// per-warp-tile and per-chunk arrays (written before they are read; no clearing needed).
 int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cudaStream_t s) {
-  uint64_t nt64 = (len + PTILE - 1) / PTILE;
-  if (nt64 > 0xFFFFFFF0ull) return PARPA_EUNSUPPORTED;
+  uint64_t nt64 = (len + WT - 1) / WT;
+  if (nt64 > 0x07FFFFFFull) return PARPA_EUNSUPPORTED;       // chunk index must fit 32 bits
   w.ntiles = (uint32_t)nt64;
-  size_t nt = std::max<size_t>(w.ntiles, 1);
+  w.nblk = (uint32_t)((nt64 + SCAN_TILE - 1) / SCAN_TILE);
+  size_t nt = std::max<size_t>(w.ntiles, 1), nb = std::max<size_t>(w.nblk, 1);
   w.dq_cap = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(4096, len / 512), 1u << 24);
   size_t o = 0;
-  size_t o_tau = o; o = align_up(o + nt * 8);
-  size_t o_flag = o; o = align_up(o + nt * 16);
+  size_t o_tau = o; o = align_up(o + nb * 8);
+  size_t o_flag = o; o = align_up(o + nb * 4);
   size_t o_ctrl = o; o = align_up(o + sizeof(Ctrl));
   size_t zero = o;
-  size_t o_incl = o; o = align_up(o + nt * sizeof(Seg));
-  size_t o_tinfo = o; o = align_up(o + nt * CW * sizeof(TileInfo));
-  size_t o_cs = o; o = align_up(o + nt * CW * 32);
+  size_t o_lex = o; o = align_up(o + nt * 32 * 4);
+  size_t o_wtau = o; o = align_up(o + nt * 4);
+  size_t o_went = o; o = align_up(o + nt);
+  size_t o_wseg = o; o = align_up(o + nt * 16);
+  size_t o_bagg = o; o = align_up(o + nb * sizeof(Seg));
+  size_t o_binc = o; o = align_up(o + nb * sizeof(Seg));
+  size_t o_tot = o; o = align_up(o + sizeof(Seg) + 16);
+  size_t o_tinfo = o; o = align_up(o + nt * sizeof(TileInfo));
+  size_t o_cs = o; o = align_up(o + nt * 32);
   size_t o_dq = o; o = align_up(o + (size_t)w.dq_cap * sizeof(DeferItem));
   size_t o_st = o; o = align_up(o + sizeof(Stats));
   size_t o_in = o; if (need_aligned_copy) o = align_up(o + len);
   CK(cudaMallocAsync(&w.block, o, s));
   uint8_t *b = (uint8_t *)w.block;
   w.tau_desc = (unsigned long long *)(b + o_tau);
-  w.seg_desc = (uint4 *)(b + o_flag);
+  w.bflag = (uint32_t *)(b + o_flag);
   w.ctrl = (Ctrl *)(b + o_ctrl);
-  w.seg_incl = (Seg *)(b + o_incl);
+  w.lex = (uint32_t *)(b + o_lex);
+  w.wtau = (uint32_t *)(b + o_wtau);
+  w.wentry = b + o_went;
+  w.wseg = (uint4 *)(b + o_wseg);
+  w.bagg = (Seg *)(b + o_bagg);
+  w.bincl = (Seg *)(b + o_binc);
+  w.tot_seg = (Seg *)(b + o_tot);
+  w.tot_tau = (uint32_t *)(b + o_tot + sizeof(Seg));
   w.tinfo = (TileInfo *)(b + o_tinfo);
   w.chunk_state = b + o_cs;
   w.dq = (DeferItem *)(b + o_dq);
   w.stats = (Stats *)(b + o_st);
   w.aligned_in = need_aligned_copy ? b + o_in : nullptr;
-  w.zero_bytes = zero;
   CK(cudaMemsetAsync(w.block, 0, zero, s));
   return PARPA_OK;
 }
@@ -205,9 +219,16 @@ void make_args(KArgs &a, const Work &w, const uint8_t *in, uint64_t len) {
   a.len = len;
   a.ntiles = w.ntiles;
   a.seed = seg_identity();
+  a.lex = w.lex;
+  a.wtau = w.wtau;
+  a.wentry = w.wentry;
+  a.wseg = w.wseg;
   a.tau_desc = w.tau_desc;
-  a.seg_desc = w.seg_desc;
-  a.seg_incl = w.seg_incl;
+  a.bflag = w.bflag;
+  a.bagg = w.bagg;
+  a.bincl = w.bincl;
+  a.tot_tau = w.tot_tau;
+  a.tot_seg = w.tot_seg;
   a.tinfo = w.tinfo;
   a.chunk_state = w.chunk_state;
   a.ctrl = w.ctrl;
@@ -251,26 +272,52 @@ int grid_for(int occ, int sms, uint32_t ntiles, int warps_per_cta) {
   return (int)std::max<long long>(1, std::min<long long>(g, need));
 }
 
-int launch_scan(int mode, const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, uint32_t *launches) {
+// S1-S5: pass 1, τ scan (MODE_TAU stops here), pass 2, record/column scan.
+int launch_passes(int mode, const KArgs &a, const DfaK &k, cudaStream_t s, uint32_t *launches) {
+  if (a.ntiles == 0) return PARPA_OK;
+  DevCfg *dc;
+  int rc = dev_cfg(&dc);
+  if (rc) return rc;
+  const uint32_t nblk = (a.ntiles + SCAN_TILE - 1) / SCAN_TILE;
+  {
+    Launch L(s, "k_pass1");
+    k_pass1<<<grid_for(dc->occ_pass1, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, LUT_BYTES, s>>>(a, k);
+  }
+  CK(cudaGetLastError());
+  {
+    Launch L(s, "k_tau_scan");
+    k_tau_scan<<<nblk, SCAN_THREADS, 0, s>>>(a);
+  }
+  CK(cudaGetLastError());
+  uint32_t n = 2;
+  if (mode != MODE_TAU) {
+    {
+      Launch L(s, "k_pass2");
+      k_pass2<<<grid_for(dc->occ_pass2, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, LUT_BYTES, s>>>(a, k);
+    }
+    CK(cudaGetLastError());
+    {
+      Launch L(s, "k_seg_scan");
+      k_seg_scan<<<nblk, SCAN_THREADS, 0, s>>>(a);
+    }
+    CK(cudaGetLastError());
+    n += 2;
+  }
+  if (launches) *launches += n;
+  return PARPA_OK;
+}
+
+int launch_emit(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, uint32_t *launches) {
   if (a.ntiles == 0) return PARPA_OK;
   DevCfg *dc;
   int rc = dev_cfg(&dc);
   if (rc) return rc;
   {
-    Launch L(s, mode == MODE_EMIT ? "k_scan_emit" : mode == MODE_COUNT ? "k_scan_count" : "k_scan_tau");
-    if (mode == MODE_TAU) {
-      int g = grid_for(dc->occ_scan[0], dc->sms, a.ntiles, 1);
-      k_scan<MODE_TAU><<<g, ScanCfg<MODE_TAU>::THREADS, ScanCfg<MODE_TAU>::SMEM, s>>>(a, k, ck);
-    } else if (mode == MODE_COUNT) {
-      int g = grid_for(dc->occ_scan[1], dc->sms, a.ntiles, 1);
-      k_scan<MODE_COUNT><<<g, ScanCfg<MODE_COUNT>::THREADS, ScanCfg<MODE_COUNT>::SMEM, s>>>(a, k, ck);
-    } else {
-      int g = grid_for(dc->occ_scan[2], dc->sms, a.ntiles, 1);
-      k_scan<MODE_EMIT><<<g, ScanCfg<MODE_EMIT>::THREADS, ScanCfg<MODE_EMIT>::SMEM, s>>>(a, k, ck);
-    }
+    Launch L(s, "k_emit");
+    k_emit<<<grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s>>>(a, k, ck);
   }
-  if (launches) (*launches)++;
   CK(cudaGetLastError());
+  if (launches) (*launches)++;
   return PARPA_OK;
 }
 
@@ -325,7 +372,7 @@ extern "C" {
 const char *parpa_last_error(void) { return t_last_error; }
 const char *parpa_version(void) { return "parpa 0.1 (sm_100a, dense LUT path)"; }
 uint32_t parpa_chunk_bytes(void) { return CHUNK; }
-uint32_t parpa_tile_bytes(void) { return PTILE; }
+uint32_t parpa_tile_bytes(void) { return WT; }
 
 const char *parpa_status_string(int st) {
   switch (st) {
@@ -439,9 +486,7 @@ static int plan_scan(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len,
   p->a.seed = seed;
   p->a.base = base;
   p->a.row_base = seed.recs;
-  ColsK ck;
-  memset(&ck, 0, sizeof(ck));
-  return launch_scan(MODE_COUNT, p->a, dfa->k, ck, s, nullptr);
+  return launch_passes(MODE_COUNT, p->a, dfa->k, s, nullptr);
 }
 
 static int plan_totals(parpa_plan *p, Seg &tot, uint32_t &tau, uint64_t &first_inv) {
@@ -450,12 +495,10 @@ static int plan_totals(parpa_plan *p, Seg &tot, uint32_t &tau, uint64_t &first_i
   tau = NIB_IDENT;
   Ctrl ctrl;
   if (p->w.ntiles) {
-    unsigned long long desc;
-    CK(cudaMemcpyAsync(&tot, p->w.seg_incl + (p->w.ntiles - 1), sizeof(Seg), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&desc, p->w.tau_desc + (p->w.ntiles - 1), 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&tot, p->w.tot_seg, sizeof(Seg), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&tau, p->w.tot_tau, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&ctrl, p->w.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    tau = (uint32_t)desc;
     first_inv = ctrl.inv_neg ? ~ctrl.inv_neg : NONE;
   } else {
     first_inv = NONE;
@@ -500,17 +543,8 @@ int parpa_plan_emit(parpa_plan *p, const parpa_schema *sch, const parpa_column *
   a.strict = sch->strict;
   a.cap = p->records;
   a.stats = d_stats ? (Stats *)d_stats : p->w.stats;
-  if (a.ntiles) {
-    DevCfg *dc;
-    if ((rc = dev_cfg(&dc))) return rc;
-    int g = grid_for(dc->occ_emit, dc->sms, a.ntiles * CW, EMIT_WARPS);
-    {
-      Launch L(s, "k_emit");
-      k_emit<<<g, EMIT_WARPS * 32, EMIT_SMEM, s>>>(a, p->dfa->k, ck);
-    }
-    CK(cudaGetLastError());
-  }
-  rc = launch_tail(a, p->dfa->k, ck, s, nullptr);
+  rc = launch_emit(a, p->dfa->k, ck, s, nullptr);
+  if (!rc) rc = launch_tail(a, p->dfa->k, ck, s, nullptr);
   prof_end();
   return rc;
 }
@@ -620,32 +654,8 @@ static int parse_into_impl(const parpa_dfa *dfa, const parpa_schema *sch, const 
     a.left_len = left_len;
     a.is_last = is_last;
     uint32_t n = 0;
-    unsigned long long *prof = nullptr;
-    const bool dbg = getenv("PARPA_DEBUG") != nullptr;
-    if (dbg && cudaMallocAsync(&prof, 4096 * 16 * 8, s) == cudaSuccess) {
-      cudaMemsetAsync(prof, 0, 4096 * 16 * 8, s);
-      a.prof = prof;
-    }
-    rc = launch_scan(MODE_EMIT, a, dfa->k, ck, s, &n);
-    if (prof) {
-      std::vector<unsigned long long> h(4096 * 16);
-      cudaMemcpyAsync(h.data(), prof, h.size() * 8, cudaMemcpyDeviceToHost, s);
-      cudaStreamSynchronize(s);
-      const char *nm[] = {"ticket", "A", "wait_TP", "B", "wait_SP", "C", "lbT_wait", "lbT_work", "lbS_wait",
-                          "lbS_work", "iters", "lbT_windows", "lbT_spins", "lbS_windows", "lbS_spins"};
-      double tot[16] = {0};
-      int nb = 0;
-      for (int b = 0; b < 4096; b++) {
-        if (!h[b * 16 + P_ITERS]) continue;
-        nb++;
-        for (int k = 0; k < 15; k++) tot[k] += (double)h[b * 16 + k];
-      }
-      fprintf(stderr, "[parpa] per-CTA mean cycles over %d CTAs:", nb);
-      for (int k = 0; k < 15; k++) fprintf(stderr, " %s=%.3g", nm[k], nb ? tot[k] / nb : 0.0);
-      fprintf(stderr, "\n");
-      cudaFreeAsync(prof, s);
-      a.prof = nullptr;
-    }
+    rc = launch_passes(MODE_COUNT, a, dfa->k, s, &n);
+    if (!rc) rc = launch_emit(a, dfa->k, ck, s, &n);
     if (!rc) rc = launch_tail(a, dfa->k, ck, s, &n);
     if (launches) *launches = n;
   }
@@ -738,12 +748,10 @@ int parpa_summarize(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, 
   rc = prepare_input(w, in, len, s);
   KArgs a;
   make_args(a, w, in, len);
-  ColsK ck;
-  memset(&ck, 0, sizeof(ck));
-  if (!rc) rc = launch_scan(MODE_TAU, a, dfa->k, ck, s, nullptr);
-  unsigned long long desc = NIB_IDENT;
+  if (!rc) rc = launch_passes(MODE_TAU, a, dfa->k, s, nullptr);
+  uint32_t desc = NIB_IDENT;
   if (!rc && w.ntiles) {
-    if (cudaMemcpyAsync(&desc, w.tau_desc + (w.ntiles - 1), 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = PARPA_ECUDA;
+    if (cudaMemcpyAsync(&desc, w.tot_tau, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = PARPA_ECUDA;
   }
   work_free(w, s);
   if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;

@@ -258,6 +258,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
       "r"(parity), "r"(1000000u)                            /* suspend up to 1 ms: sleep, don't poll */
       : "memory");
+  // lanes can leave the suspend loop separately; without this the warp stays split into halves
+  // that execute the following stage twice (measured: 2x instructions at 16 threads/issue)
+  __syncwarp();
 }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

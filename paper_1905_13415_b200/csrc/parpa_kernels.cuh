@@ -56,14 +56,15 @@ struct ColsK {                      // column descriptors, passed by value (kern
 };
 
 struct Ctrl {
-  unsigned int ticket;
+  unsigned int ticket;               // block tickets of k_tau_scan
+  unsigned int ticket2;              // block tickets of k_seg_scan
   unsigned int n_defer;
   unsigned int defer_overflow;
   unsigned int unsupported;
   unsigned long long inv_neg;        // ~(first invalid byte position), 0 = none (atomicMax)
   unsigned long long n_missing;
   unsigned long long n_extra;
-  unsigned long long pad[3];
+  unsigned long long pad[2];
 };
 
 struct TileInfo {
@@ -87,9 +88,16 @@ struct KArgs {
   Seg seed;                          // composed prefix of everything before the range
   unsigned long long row_base;       // global record index of local row 0
   unsigned long long cap;            // rows per column
-  unsigned long long *tau_desc;      // [ntiles] (flag << 32) | nibble τ
-  uint4 *seg_desc;                   // [ntiles] {SegT aggregate (tile-local), flag}: one 16-byte word
-  Seg *seg_incl;                     // [ntiles] inclusive prefix (valid once the flag says so)
+  // ntiles = warp tiles (WT bytes each); nblk = scan blocks (SCAN_TILE warp tiles each)
+  uint32_t *lex;                     // [ntiles * 32] lane-exclusive τ within its warp tile (nibble form)
+  uint32_t *wtau;                    // [ntiles] warp-tile τ aggregate
+  uint8_t *wentry;                   // [ntiles] entry state of each warp tile (device numbering)
+  uint4 *wseg;                       // [ntiles] warp-tile SegT aggregate {cnt, colf, pos, 0}
+  unsigned long long *tau_desc;      // [nblk] decoupled look-back descriptors (flag << 32) | nibble τ
+  uint32_t *bflag;                   // [nblk] Seg look-back flags
+  Seg *bagg, *bincl;                 // [nblk] block aggregate / inclusive prefix (valid once flagged)
+  uint32_t *tot_tau;                 // τ of the whole range (nibble form, seed not applied)
+  Seg *tot_seg;                      // seed ∘ Seg of the whole range
   TileInfo *tinfo;                   // [ntiles]
   uint8_t *chunk_state;              // [ntiles * 32] device entry state of each chunk
   Ctrl *ctrl;
@@ -438,75 +446,6 @@ __device__ __forceinline__ void st_relaxed_v4(uint4 *p, uint4 v) {
                "r"(v.w) : "memory");
 }
 
-// returns seed ∘ Seg_0 ∘ ... ∘ Seg_{t-1}; window of 256 tiles per round trip (16-byte descriptors)
-__device__ Seg lookback_seg(const KArgs &a, uint32_t t) {
-  const int lane = threadIdx.x & 31;
-  Seg acc = seg_ident();
-  long long base = (long long)t - 1;
-  unsigned long long nwin = 0, nspin = 0;
-  while (true) {
-    uint4 d[LB_PER_LANE];
-#pragma unroll
-    for (int k = 0; k < LB_PER_LANE; k++) {                  // all loads in flight at once
-      long long j = base - (long long)lane * LB_PER_LANE - k;
-      d[k] = j >= 0 ? ld_relaxed_v4(a.seg_desc + j) : make_uint4(0u, 0u, 0xFFFFFFFFu, FLAG_INCL);
-    }
-    nwin++;
-    while (true) {
-      bool missing = false;
-#pragma unroll
-      for (int k = 0; k < LB_PER_LANE; k++) {
-        long long j = base - (long long)lane * LB_PER_LANE - k;
-        if (d[k].w == 0u) {
-          d[k] = ld_relaxed_v4(a.seg_desc + j);
-          missing = true;
-        }
-      }
-      if (!__any_sync(0xffffffffu, missing)) break;
-      nspin++;
-      __nanosleep(64);
-    }
-    bool incl = false;
-    int kstar = LB_PER_LANE - 1;
-#pragma unroll
-    for (int k = 0; k < LB_PER_LANE; k++)
-      if (!incl && d[k].w == FLAG_INCL) { incl = true; kstar = k; }
-    Seg v[LB_PER_LANE];
-    if (incl) __threadfence();                         // acquire side for the inclusive payload below
-#pragma unroll
-    for (int k = 0; k < LB_PER_LANE; k++) {
-      long long j = base - (long long)lane * LB_PER_LANE - k;
-      if (k > kstar) {
-        v[k] = seg_ident();
-      } else if (k == kstar && incl) {
-        v[k] = j >= 0 ? ldcg_seg(a.seg_incl + j) : (j == -1 ? a.seed : seg_ident());
-      } else {
-        v[k] = segt_to_seg(SegT{d[k].x, d[k].y, d[k].z}, a.base + (unsigned long long)j * PTILE);
-      }
-    }
-    Seg p0 = seg_op(v[1], v[0]), p1 = seg_op(v[3], v[2]);
-    Seg p2 = seg_op(v[5], v[4]), p3 = seg_op(v[7], v[6]);
-    Seg w = seg_op(seg_op(p3, p2), seg_op(p1, p0));
-    unsigned m = __ballot_sync(0xffffffffu, incl);
-    int L = m ? __ffs(m) - 1 : 31;
-    if (lane > L) w = seg_ident();
-#pragma unroll
-    for (int dd = 1; dd < 32; dd <<= 1) {
-      Seg o = shfl_down_seg(w, dd);
-      if (lane + dd < 32) w = seg_op(o, w);
-    }
-    w = shfl_seg(w, 0);
-    acc = seg_op(w, acc);
-    if (m) break;
-    base -= 32 * LB_PER_LANE;
-  }
-  if (a.prof && lane == 0) {
-    atomicAdd(a.prof + blockIdx.x * 16 + 13, nwin);
-    atomicAdd(a.prof + blockIdx.x * 16 + 14, nspin);
-  }
-  return acc;
-}
-
 // ---- S6+S7: field emission ---------------------------------------------------------------------
 struct EmitCounters {
   unsigned long long missing, extra;
@@ -819,299 +758,9 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   __syncwarp();
 }
 
-// ---- the fused scan kernel: warp-specialised pipeline over 32 KB tiles -----------------------------
-// CTA = 16 compute warps + 1 look-back warp.  A tile = 16 warp tiles of 2 KB (one 64-byte chunk per
-// lane).  Per iteration i the compute warps run
-//   A(i)   load + S1/S2 (τ per chunk) + warp ∘-scan -> warp aggregates            -> mbarrier A
-//   B(i-1) entry states from the τ prefix, S4 masks, S5 warp summary scan         -> mbarrier B
-//   C(i-2) S6/S7 emission from the record/column prefix
-// while the look-back warp combines the warp aggregates of tile i, publishes them and runs the
-// decoupled look-back over tile τ's (single-pass scan P:250), then does the same for the
-// record/column summaries of tile i-1.  Nothing waits for the current tile's look-back: the chains
-// advance a full pipeline stage behind the compute.  The tile bytes are re-read from L2 (not DRAM)
-// in stages B and C.
-
-struct PipeSmem {
-  uint64_t mbA[2], mbTP[2], mbB[2], mbSP[2];
-  uint32_t tile_id[4];
-  uint32_t tile_id2[4];                             // tile of stage B, for the record/column warp
-  uint32_t wtau[2][CW];                             // warp τ aggregates (nibble form)
-  uint32_t wentry[2][CW];                           // warp entry states (device numbering)
-  SegT wseg[2][CW];                                 // warp summaries (positions warp-tile-local)
-  Seg wpre[2][CW];                                  // warp prefixes (global)
-  uint32_t cntA[2], cntB[2];                        // arrival counters: the last warp publishes
-  uint32_t wexT[2][32];                             // per-warp exclusive τ within the tile
-  uint32_t aggT[2];                                 // tile τ aggregate
-  SegT wexS[2][32];                                 // per-warp exclusive summary within the tile
-  SegT saggS[2];                                    // tile summary aggregate (tile-local positions)
-};
-
-constexpr size_t SCRATCH_OFF = (LUT_BYTES + sizeof(PipeSmem) + 127) / 128 * 128;
-template <int MODE>
-struct ScanCfg {
-  static constexpr int THREADS = (CW + 2) * 32;
-  static constexpr size_t SMEM = SCRATCH_OFF + (MODE == MODE_EMIT ? CW * sizeof(WarpScratch) : 0);
-};
-
-// Look-back warp, in two halves per chain so that a tile's aggregate is always published before this
-// warp blocks in any look-back (publishing never waits; look-backs only wait on smaller tiles, so the
-// smallest blocked look-back always makes progress — no cross-CTA cycles).
-// Aggregate publication is done by the LAST compute warp to finish a stage (smem arrival counter),
-// right when the tile's data is complete — never behind a look-back.  The look-back warps only chase.
-__device__ __forceinline__ void publish_tau(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t) {
-  const int lane = threadIdx.x & 31;
-  uint32_t w = lane < CW ? sm.wtau[slot][lane] : NIB_IDENT;
-  uint32_t agg;
-  uint32_t wex = warp_scan_tau(spread16(w), spread16(w >> 16), agg);
-  sm.wexT[slot][lane] = wex;
-  if (lane == 0) {
-    sm.aggT[slot] = agg;
-    st_relaxed_u64(a.tau_desc + t, ((unsigned long long)(t == 0 ? FLAG_INCL : FLAG_AGG) << 32) | agg);
-  }
-}
-__device__ __forceinline__ void publish_seg(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t) {
-  const int lane = threadIdx.x & 31;
-  SegT w = lane < CW ? segt_shift(sm.wseg[slot][lane], (uint32_t)lane * WT) : segt_ident();
-  SegT sagg;
-  SegT wex = warp_scan_segt(w, sagg);
-  sm.wexS[slot][lane] = wex;
-  if (lane == 0) {
-    sm.saggS[slot] = sagg;
-    if (t == 0) {
-      stcg_seg(a.seg_incl, seg_op(a.seed, segt_to_seg(sagg, a.base)));
-      __threadfence();
-      st_relaxed_v4(a.seg_desc, make_uint4(sagg.cnt, sagg.colf, sagg.pos, FLAG_INCL));
-    } else {
-      st_relaxed_v4(a.seg_desc + t, make_uint4(sagg.cnt, sagg.colf, sagg.pos, FLAG_AGG));
-    }
-  }
-}
-__device__ __forceinline__ void lb_tau_finish(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t) {
-  const int lane = threadIdx.x & 31;
-  uint32_t prefix = NIB_IDENT;
-  if (t != 0) {
-    prefix = lookback_tau(a, t);
-    if (lane == 0)
-      st_relaxed_u64(a.tau_desc + t, ((unsigned long long)FLAG_INCL << 32) | compose_nib(prefix, sm.aggT[slot]));
-  }
-  const uint32_t tile_entry = nib_at(prefix, a.seed_dev);
-  if (lane < CW) {
-    uint32_t e = nib_at(sm.wexT[slot][lane], tile_entry);
-    sm.wentry[slot][lane] = e;
-    a.tinfo[(unsigned long long)t * CW + lane].entry = e;
-  }
-}
-__device__ __forceinline__ void lb_seg_finish(const KArgs &a, PipeSmem &sm, uint32_t slot, uint32_t t) {
-  const int lane = threadIdx.x & 31;
-  const unsigned long long tb = a.base + (unsigned long long)t * PTILE;
-  Seg prefix = a.seed;
-  if (t != 0) {
-    prefix = lookback_seg(a, t);
-    if (lane == 0) {
-      SegT sagg = sm.saggS[slot];
-      stcg_seg(a.seg_incl + t, seg_op(prefix, segt_to_seg(sagg, tb)));
-      __threadfence();
-      st_relaxed_v4(a.seg_desc + t, make_uint4(sagg.cnt, sagg.colf, sagg.pos, FLAG_INCL));
-    }
-  }
-  if (lane < CW) {
-    Seg wp = seg_op(prefix, segt_to_seg(sm.wexS[slot][lane], tb));
-    sm.wpre[slot][lane] = wp;
-    a.tinfo[(unsigned long long)t * CW + lane].excl = wp;
-  }
-}
-
-// the last warp to arrive at a stage publishes the tile aggregate
-__device__ __forceinline__ bool last_arrival(uint32_t *cnt) {
-  uint32_t old = 0;
-  if ((threadIdx.x & 31) == 0) {
-    __threadfence_block();
-    old = atomicAdd(cnt, 1u);
-    if (old == CW - 1) atomicExch(cnt, 0u);
-  }
-  old = __shfl_sync(0xffffffffu, old, 0);
-  if (old == CW - 1) __threadfence_block();
-  return old == CW - 1;
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(ScanCfg<MODE>::THREADS, 1) k_scan(const KArgs a, const DfaK dfa, const ColsK colsk) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t *lut = smem;
-  PipeSmem &sm = *reinterpret_cast<PipeSmem *>(smem + LUT_BYTES);
-  WarpScratch *scratch = reinterpret_cast<WarpScratch *>(smem + SCRATCH_OFF);
-  __shared__ ColDesc s_cols[MODE == MODE_EMIT ? MAX_COLS : 1];
-  build_lut(lut, dfa);
-  if (MODE == MODE_EMIT)
-    for (int c = threadIdx.x; c < (int)a.C; c += blockDim.x) s_cols[c] = colsk.c[c];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; s++) {
-      sm.cntA[s] = sm.cntB[s] = 0;
-      mbar_init(&sm.mbA[s], CW);
-      mbar_init(&sm.mbTP[s], 1);
-      mbar_init(&sm.mbB[s], CW);
-      mbar_init(&sm.mbSP[s], 1);
-    }
-  }
-  __syncthreads();                                          // the only CTA-wide barrier
-  if (warp >= CW) {
-    // ================= look-back warps =================
-    // warp CW: the τ chain (S3); warp CW+1: the record/column chain (S5).  Each publishes a tile's
-    // aggregate before it can block in that tile's look-back, and neither waits on the other, so the
-    // smallest blocked look-back in the grid always progresses.
-    if (warp == CW) {
-      PROF_T0(pt);
-      for (uint32_t i = 0;; i++) {
-        mbar_wait(&sm.mbA[i & 1], (i >> 1) & 1);
-        PROF_ADD(P_LBT_WAIT, pt);
-        const uint32_t t = sm.tile_id[i & 3];
-        if (t >= a.ntiles) break;
-        lb_tau_finish(a, sm, i & 1, t);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.mbTP[i & 1]);
-        PROF_ADD(P_LBT_WORK, pt);
-      }
-    } else if (MODE != MODE_TAU) {
-      PROF_T0(pt);
-      for (uint32_t i = 0;; i++) {
-        mbar_wait(&sm.mbB[i & 1], (i >> 1) & 1);             // stage B of tile i done (or tile invalid)
-        PROF_ADD(P_LBS_WAIT, pt);
-        const uint32_t t = sm.tile_id2[i & 3];
-        if (t >= a.ntiles) break;
-        lb_seg_finish(a, sm, i & 1, t);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sm.mbSP[i & 1]);
-        PROF_ADD(P_LBS_WORK, pt);
-      }
-    }
-    return;
-  }
-  // ================= compute warps =================
-  WarpScratch *ws = scratch + warp;
-  const uint32_t laneoff = (uint32_t)(lane & 15) * 8u;
-  EmitCounters cnt{0ull, 0ull, 0u};
-  // stage registers: A = tile i (bytes, prefetched one iteration ahead), B = tile i-1 (bytes,
-  // lane-exclusive τ), C = tile i-2 (masks, summary scan; its bytes are in ws->bytes[(i-2)&1])
-  uint32_t vA[16], vB[16];
-  int nvA = 0, nvB = 0;
-  uint32_t tA = 0xFFFFFFFFu, exB = NIB_IDENT;
-  uint32_t qtB[3] = {NIB_IDENT, NIB_IDENT, NIB_IDENT};
-  unsigned long long wtB = 0, wtC = 0;
-  bool validA = false, validB = false, validC = false;
-  unsigned long long DmC = 0, FmC = 0, RmC = 0, VmC = 0;
-  SegT sexC = segt_ident(), saggC = segt_ident();
-  // prologue: claim and load tile 0
-  if (warp == 0 && lane == 0) sm.tile_id[0] = atomicAdd(&a.ctrl->ticket, 1u);
-  named_bar_sync(1, CW * 32);
-  tA = sm.tile_id[0];
-  validA = tA < a.ntiles;
-  if (validA) {
-    const unsigned long long cstart = ((unsigned long long)tA * CW + warp) * WT + (unsigned long long)lane * CHUNK;
-    nvA = cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
-    load_chunk(a.in + cstart, nvA, vA);
-  }
-  const bool prof0 = a.prof && warp == 0;
-  unsigned long long pt = prof0 ? clock64() : 0ull;
-#define CPROF(slot) do { if (prof0 && lane == 0) { unsigned long long _n = clock64(); \
-  atomicAdd(a.prof + blockIdx.x * 16 + (slot), _n - pt); pt = _n; } } while (0)
-  for (uint32_t i = 0;; i++) {
-    // ---- claim tile i+1 and issue its loads (they land while A/B/C below compute) ----
-    if (warp == 0 && lane == 0) sm.tile_id[(i + 1) & 3] = atomicAdd(&a.ctrl->ticket, 1u);
-    named_bar_sync(1, CW * 32);
-    CPROF(P_TICKET);
-    const uint32_t tN = sm.tile_id[(i + 1) & 3];
-    const bool validN = tN < a.ntiles;
-    uint32_t vN[16];
-    int nvN = 0;
-    if (validN) {
-      const unsigned long long cstart = ((unsigned long long)tN * CW + warp) * WT + (unsigned long long)lane * CHUNK;
-      nvN = cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
-      load_chunk(a.in + cstart, nvN, vN);
-    }
-    // ---- A(i): τ of the chunk, warp scan ----
-    uint32_t exA = NIB_IDENT;
-    uint32_t qtA[3] = {NIB_IDENT, NIB_IDENT, NIB_IDENT};
-    const unsigned long long wtA = (unsigned long long)tA * CW + warp;
-    if (validA) {
-      uint32_t t0, t1, agg;
-      if (nvA == CHUNK) chunk_tau4<true>(lut, vA, nvA, laneoff, t0, t1, qtA);
-      else chunk_tau4<false>(lut, vA, nvA, laneoff, t0, t1, qtA);
-      exA = warp_scan_tau(t0, t1, agg);
-      if (lane == 0) sm.wtau[i & 1][warp] = agg;
-      __syncwarp();
-      if (last_arrival(&sm.cntA[i & 1])) publish_tau(a, sm, i & 1, (uint32_t)tA);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.mbA[i & 1]);
-    CPROF(P_A);
-    // TAU-only mode: stay at most one tile ahead of the look-back warp (mbarrier phases, smem slots)
-    if (MODE == MODE_TAU && i >= 1 && validB) mbar_wait(&sm.mbTP[(i - 1) & 1], ((i - 1) >> 1) & 1);
-    // ---- B(i-1): entry states, masks, summary scan ----
-    if (MODE != MODE_TAU && i >= 1) {
-      if (warp == 0 && lane == 0) sm.tile_id2[(i - 1) & 3] = validB ? (uint32_t)(wtB / CW) : 0xFFFFFFFFu;
-      if (validB) {
-        if (MODE == MODE_EMIT) stash_chunk(ws->bytes[(i - 1) & 1], lane, vB);
-        CPROF(P_B);
-        mbar_wait(&sm.mbTP[(i - 1) & 1], ((i - 1) >> 1) & 1);
-        CPROF(P_WAIT_TP);
-        const uint32_t entry = nib_at(exB, sm.wentry[(i - 1) & 1][warp]);
-        a.chunk_state[wtB * 32 + lane] = (uint8_t)entry;
-        unsigned long long Dm, Fm, Rm;
-        uint32_t fin;
-        if (nvB == CHUNK) fin = chunk_masks4<true>(lut, vB, nvB, laneoff, entry, qtB, Dm, Fm, Rm);
-        else fin = chunk_masks4<false>(lut, vB, nvB, laneoff, entry, qtB, Dm, Fm, Rm);
-        const unsigned long long cstart = wtB * WT + (unsigned long long)lane * CHUNK;
-        if (fin == INV_DEV && entry != INV_DEV && nvB > 0) {
-          int p = first_inv_in_chunk(lut, a.in + cstart, nvB, laneoff, entry);
-          if (p >= 0) atomicMax(&a.ctrl->inv_neg, ~(a.base + cstart + (unsigned)p));
-        }
-        const unsigned long long Vm = nvB >= 64 ? ~0ull : ((1ull << nvB) - 1ull);
-        SegT sagg;
-        const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
-        if (lane == 0) sm.wseg[(i - 1) & 1][warp] = sagg;
-        DmC = Dm; FmC = Fm; RmC = Rm; VmC = Vm; sexC = sex; saggC = sagg;
-        __syncwarp();
-        if (last_arrival(&sm.cntB[(i - 1) & 1])) publish_seg(a, sm, (i - 1) & 1, (uint32_t)(wtB / CW));
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&sm.mbB[(i - 1) & 1]);
-      CPROF(P_B);
-    }
-    // COUNT mode: stay at most two tiles ahead of the record/column warp
-    if (MODE == MODE_COUNT && i >= 2 && validC) mbar_wait(&sm.mbSP[(i - 2) & 1], ((i - 2) >> 1) & 1);
-    // ---- C(i-2): emission ----
-    if (MODE == MODE_EMIT && i >= 2 && validC) {
-      mbar_wait(&sm.mbSP[(i - 2) & 1], ((i - 2) >> 1) & 1);
-      CPROF(P_WAIT_SP);
-      const Seg wprefix = sm.wpre[(i - 2) & 1][warp];
-      const unsigned long long cstart = wtC * WT + (unsigned long long)lane * CHUNK;
-      const Seg st = seg_op(wprefix, segt_to_seg(sexC, a.base + wtC * WT));
-      emit_tile(a, s_cols, ws, ws->bytes[(i - 2) & 1], st, sexC, saggC, wprefix, DmC, FmC, RmC, VmC,
-                a.base + wtC * WT, a.base + cstart, cnt);
-      CPROF(P_C);
-    }
-    if (prof0 && lane == 0) atomicAdd(a.prof + blockIdx.x * 16 + P_ITERS, 1ull);
-    const bool done = MODE == MODE_EMIT ? (i >= 2 && !validC) : (i >= 1 && !validB);
-    if (done) break;
-    // ---- rotate the pipeline ----
-    validC = validB;
-    wtC = wtB;
-    validB = validA;
-    wtB = wtA;
-    exB = exA;
-    qtB[0] = qtA[0]; qtB[1] = qtA[1]; qtB[2] = qtA[2];
-    nvB = nvA;
-#pragma unroll
-    for (int k = 0; k < 16; k++) vB[k] = vA[k];
-    validA = validN;
-    tA = tN;
-    nvA = nvN;
-#pragma unroll
-    for (int k = 0; k < 16; k++) vA[k] = vN[k];
-  }
-  flush_counters(a, cnt);
-}
+}  // namespace parpa
+#include "parpa_passes.cuh"
+namespace parpa {
 
 // ---- two-phase emit kernel (per warp tile, from the stored prefixes; no look-back) ------------------
 constexpr int EMIT_WARPS = 16;
@@ -1129,7 +778,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 1) k_emit(const KArgs a, cons
   EmitCounters cnt{0ull, 0ull, 0u};
   __syncthreads();
   const uint32_t gw = blockIdx.x * EMIT_WARPS + warp, nw = gridDim.x * EMIT_WARPS;
-  const uint32_t nwt = a.ntiles * CW;
+  const uint32_t nwt = a.ntiles;
   for (uint32_t t = gw; t < nwt; t += nw) {
     const unsigned long long tstart = (unsigned long long)t * WT;
     const unsigned long long cstart = tstart + (unsigned long long)lane * CHUNK;
@@ -1154,8 +803,8 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 1) k_emit(const KArgs a, cons
 // ---- finalize ---------------------------------------------------------------------------------------
 __global__ void k_finalize(const KArgs a, const DfaK dfa, const ColsK colsk) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  Seg tot = a.ntiles ? a.seg_incl[a.ntiles - 1] : a.seed;
-  uint32_t tau = a.ntiles ? (uint32_t)a.tau_desc[a.ntiles - 1] : NIB_IDENT;
+  Seg tot = a.ntiles ? *a.tot_seg : a.seed;
+  uint32_t tau = a.ntiles ? *a.tot_tau : NIB_IDENT;
   uint32_t fin = nib_at(tau, a.seed_dev);
   EmitCounters cnt{0ull, 0ull, 0u};
   unsigned long long R = tot.recs, nf = tot.nflds;

@@ -1,0 +1,260 @@
+// parpa_passes.cuh — the scan half of the hot path as four chain-free / single-pass kernels.
+//
+//   k_pass1     S1+S2+S3a  per warp tile (2 KB, one 64-byte chunk per lane): the chunk's
+//               state-transition vector through the shared-memory LUT, a warp ∘-scan
+//               with shuffles -> lane-exclusive τ (lex) and the warp-tile aggregate.
+//               No inter-CTA dependency: persistent grid, high occupancy.
+//   k_tau_scan  S3b  single-pass scan of the warp-tile aggregates with decoupled look-back
+//               (Merrill & Garland, the paper's P:250 reference): blocks of SCAN_TILE aggregates in
+//               ticket order, block aggregate published before the look-back -> the entry state of
+//               every warp tile, P:361-364 seeded with the range's entry state.
+//   k_pass2     S4+S5a  per warp tile: lane entry = lex applied to the tile entry, re-simulation
+//               -> DATA / DELIM / RECORD masks (the paper's bitmap indexes), record
+//               count by POPCNT and the abs/rel column offset plus the open-field
+//               carries, reduced over the warp -> one SegT per warp tile.
+//   k_seg_scan  S5b  single-pass decoupled look-back scan of the warp-tile SegTs (⊕ of P:408-414,
+//               64-bit positions) -> the global prefix (records, fields, column, open field) of every
+//               warp tile, consumed by k_emit.
+//
+// Every kernel is bounded by its own DRAM stream or ALU work; nothing spins on another CTA except the
+// two small scans, whose look-backs cover SCAN_TILE warp tiles (4 MB of input) per block.
+#pragma once
+
+namespace parpa {
+
+constexpr int PASS_WARPS = 16;                       // k_pass1 / k_pass2: 512 threads per CTA
+constexpr int SCAN_THREADS = 256, SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS; // warp tiles per scan block (4 MB of input)
+
+__device__ __forceinline__ int chunk_valid(const KArgs &a, unsigned long long cstart) {
+  return cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
+}
+
+// ---- K1: pass 1 ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(PASS_WARPS * 32, 2) k_pass1(const KArgs a, const DfaK dfa) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  build_lut(smem, dfa);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t laneoff = (uint32_t)(lane & 15) * 8u;
+  const uint32_t nw = gridDim.x * PASS_WARPS;
+  for (uint32_t t = blockIdx.x * PASS_WARPS + warp; t < a.ntiles; t += nw) {
+    const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
+    const int nv = chunk_valid(a, cstart);
+    uint32_t v[16], t0, t1, qt[3];
+    load_chunk(a.in + cstart, nv, v);
+    if (nv == CHUNK) chunk_tau4<true>(smem, v, nv, laneoff, t0, t1, qt);
+    else chunk_tau4<false>(smem, v, nv, laneoff, t0, t1, qt);
+    uint32_t agg;
+    const uint32_t ex = warp_scan_tau(t0, t1, agg);
+    a.lex[(unsigned long long)t * 32 + lane] = ex;
+    if (lane == 0) a.wtau[t] = agg;
+  }
+}
+
+// ---- K2: τ scan over warp tiles -----------------------------------------------------------------
+__global__ void __launch_bounds__(SCAN_THREADS) k_tau_scan(const KArgs a) {
+  __shared__ uint32_t s_bid, s_prefix;
+  __shared__ uint32_t s_warp[SCAN_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_bid = atomicAdd(&a.ctrl->ticket, 1u);   // ticket order: look-backs only
+  __syncthreads();                                                   // wait on started blocks
+  const uint32_t b = s_bid;
+  const unsigned long long t0 = (unsigned long long)b * SCAN_TILE + (unsigned long long)threadIdx.x * SCAN_ITEMS;
+  uint32_t e[SCAN_ITEMS];
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; k++) e[k] = t0 + k < a.ntiles ? a.wtau[t0 + k] : NIB_IDENT;
+  uint32_t loc = e[0];
+#pragma unroll
+  for (int k = 1; k < SCAN_ITEMS; k++) loc = compose_nib(loc, e[k]);
+  uint32_t inc = loc;                                                // warp inclusive ∘-scan
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc = compose_nib(o, inc);
+  }
+  uint32_t wex = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) wex = NIB_IDENT;
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < SCAN_THREADS / 32 ? s_warp[lane] : NIB_IDENT;
+#pragma unroll
+    for (int d = 1; d < SCAN_THREADS / 32; d <<= 1) {
+      uint32_t o = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w = compose_nib(o, w);
+    }
+    const uint32_t bagg = __shfl_sync(0xffffffffu, w, SCAN_THREADS / 32 - 1);
+    uint32_t bex = __shfl_up_sync(0xffffffffu, w, 1);
+    if (lane < SCAN_THREADS / 32) s_warp[lane] = lane == 0 ? NIB_IDENT : bex;
+    uint32_t prefix = NIB_IDENT;
+    if (b == 0) {
+      if (lane == 0) st_relaxed_u64(a.tau_desc, ((unsigned long long)FLAG_INCL << 32) | bagg);
+    } else {
+      if (lane == 0) st_relaxed_u64(a.tau_desc + b, ((unsigned long long)FLAG_AGG << 32) | bagg);
+      prefix = lookback_tau(a, b);
+      if (lane == 0) st_relaxed_u64(a.tau_desc + b, ((unsigned long long)FLAG_INCL << 32) | compose_nib(prefix, bagg));
+    }
+    if (lane == 0) {
+      s_prefix = prefix;
+      if ((unsigned long long)(b + 1) * SCAN_TILE >= a.ntiles) *a.tot_tau = compose_nib(prefix, bagg);
+    }
+  }
+  __syncthreads();
+  uint32_t cur = compose_nib(compose_nib(s_prefix, s_warp[warp]), wex);
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; k++) {
+    if (t0 + k < a.ntiles) a.wentry[t0 + k] = (uint8_t)nib_at(cur, a.seed_dev);
+    cur = compose_nib(cur, e[k]);
+  }
+}
+
+// ---- K3: pass 2 ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(PASS_WARPS * 32, 2) k_pass2(const KArgs a, const DfaK dfa) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  build_lut(smem, dfa);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t laneoff = (uint32_t)(lane & 15) * 8u;
+  const uint32_t nw = gridDim.x * PASS_WARPS;
+  for (uint32_t t = blockIdx.x * PASS_WARPS + warp; t < a.ntiles; t += nw) {
+    const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
+    const int nv = chunk_valid(a, cstart);
+    uint32_t v[16];
+    load_chunk(a.in + cstart, nv, v);
+    const uint32_t entry = nib_at(a.lex[(unsigned long long)t * 32 + lane], a.wentry[t]);
+    a.chunk_state[(unsigned long long)t * 32 + lane] = (uint8_t)entry;
+    unsigned long long Dm, Fm, Rm;
+    uint32_t fin;
+    if (nv == CHUNK) fin = chunk_masks<true>(smem, v, nv, laneoff, entry, Dm, Fm, Rm);
+    else fin = chunk_masks<false>(smem, v, nv, laneoff, entry, Dm, Fm, Rm);
+    if (fin == INV_DEV && entry != INV_DEV && nv > 0) {
+      int p = first_inv_in_chunk(smem, a.in + cstart, nv, laneoff, entry);
+      if (p >= 0) atomicMax(&a.ctrl->inv_neg, ~(a.base + cstart + (unsigned)p));
+    }
+    const unsigned long long Vm = nv >= 64 ? ~0ull : ((1ull << nv) - 1ull);
+    SegT s = chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {                               // ordered warp reduction
+      SegT o = shfl_down_segt(s, d);
+      if (lane + d < 32) s = segt_op(s, o);
+    }
+    if (lane == 0) a.wseg[t] = make_uint4(s.cnt, s.colf, s.pos, 0u);
+  }
+}
+
+// ---- K4: record / column scan over warp tiles ---------------------------------------------------
+__device__ __forceinline__ Seg shfl_up_seg(const Seg &s, int d) {
+  Seg o;
+  o.recs = __shfl_up_sync(0xffffffffu, s.recs, d);
+  o.nflds = __shfl_up_sync(0xffffffffu, s.nflds, d);
+  o.fd = __shfl_up_sync(0xffffffffu, s.fd, d);
+  o.ld = __shfl_up_sync(0xffffffffu, s.ld, d);
+  o.col = __shfl_up_sync(0xffffffffu, s.col, d);
+  o.flags = __shfl_up_sync(0xffffffffu, s.flags, d);
+  return o;
+}
+__device__ __forceinline__ Seg wseg_at(const KArgs &a, unsigned long long t) {
+  const uint4 w = a.wseg[t];
+  return segt_to_seg(SegT{w.x, w.y, w.z}, a.base + t * WT);
+}
+
+// returns seed ∘ B_0 ∘ ... ∘ B_{b-1} over the block aggregates; one descriptor per lane per round trip
+__device__ Seg lookback_bseg(const KArgs &a, uint32_t b) {
+  const int lane = threadIdx.x & 31;
+  Seg acc = seg_ident();
+  long long base = (long long)b - 1;
+  while (true) {
+    const long long j = base - lane;
+    uint32_t f = j >= 0 ? ld_acquire_u32(a.bflag + j) : FLAG_INCL;
+    unsigned incl, zero;
+    int L;
+    while (true) {
+      incl = __ballot_sync(0xffffffffu, f == FLAG_INCL);
+      zero = __ballot_sync(0xffffffffu, f == 0u);
+      L = incl ? __ffs(incl) - 1 : 31;
+      const unsigned need = L == 31 ? 0xFFFFFFFFu : ((2u << L) - 1u);
+      if (!(zero & need)) break;
+      __nanosleep(32);
+      if (f == 0u) f = ld_acquire_u32(a.bflag + j);
+    }
+    Seg v = seg_ident();
+    if (lane <= L && j >= 0) v = f == FLAG_INCL ? ldcg_seg(a.bincl + j) : ldcg_seg(a.bagg + j);
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {                            // higher lane = earlier block
+      Seg o = shfl_down_seg(v, dd);
+      if (lane + dd < 32) v = seg_op(o, v);
+    }
+    acc = seg_op(shfl_seg(v, 0), acc);
+    if (incl) break;
+    base -= 32;
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_seg_scan(const KArgs a) {
+  __shared__ uint32_t s_bid;
+  __shared__ Seg s_prefix;
+  __shared__ Seg s_warp[SCAN_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_bid = atomicAdd(&a.ctrl->ticket2, 1u);
+  __syncthreads();
+  const uint32_t b = s_bid;
+  const unsigned long long t0 = (unsigned long long)b * SCAN_TILE + (unsigned long long)threadIdx.x * SCAN_ITEMS;
+  Seg loc = seg_ident();
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; k++)
+    if (t0 + k < a.ntiles) loc = seg_op(loc, wseg_at(a, t0 + k));
+  Seg inc = loc;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    Seg o = shfl_up_seg(inc, d);
+    if (lane >= d) inc = seg_op(o, inc);
+  }
+  Seg wex = shfl_up_seg(inc, 1);
+  if (lane == 0) wex = seg_ident();
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    Seg w = lane < SCAN_THREADS / 32 ? s_warp[lane] : seg_ident();
+#pragma unroll
+    for (int d = 1; d < SCAN_THREADS / 32; d <<= 1) {
+      Seg o = shfl_up_seg(w, d);
+      if (lane >= d) w = seg_op(o, w);
+    }
+    const Seg bagg = shfl_seg(w, SCAN_THREADS / 32 - 1);
+    Seg bex = shfl_up_seg(w, 1);
+    if (lane < SCAN_THREADS / 32) s_warp[lane] = lane == 0 ? seg_ident() : bex;
+    Seg prefix = a.seed;
+    if (b == 0) {
+      if (lane == 0) {
+        stcg_seg(a.bincl, seg_op(a.seed, bagg));
+        st_release_u32(a.bflag, FLAG_INCL);
+      }
+    } else {
+      if (lane == 0) {
+        stcg_seg(a.bagg + b, bagg);
+        st_release_u32(a.bflag + b, FLAG_AGG);
+      }
+      prefix = lookback_bseg(a, b);
+      if (lane == 0) {
+        stcg_seg(a.bincl + b, seg_op(prefix, bagg));
+        st_release_u32(a.bflag + b, FLAG_INCL);
+      }
+    }
+    if (lane == 0) {
+      s_prefix = prefix;
+      if ((unsigned long long)(b + 1) * SCAN_TILE >= a.ntiles) *a.tot_seg = seg_op(prefix, bagg);
+    }
+  }
+  __syncthreads();
+  Seg cur = seg_op(seg_op(s_prefix, s_warp[warp]), wex);
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; k++) {
+    if (t0 + k >= a.ntiles) break;
+    a.tinfo[t0 + k].excl = cur;
+    cur = seg_op(cur, wseg_at(a, t0 + k));
+  }
+}
+
+}  // namespace parpa

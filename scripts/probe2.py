@@ -27,7 +27,7 @@ for rep in range(3):
     parpa.set_profiling(False)
 s = parpa.stats_from_tensor(st)
 assert s["status"] == 0 and s["records"] == g.records and r.records == g.records
-fmt = lambda kt: " ".join(f"{k}={v:.3f}ms" for k, v in kt)
-gbs = lambda kt, key: n / (sum(v for k, v in kt if k.startswith(key)) * 1e-3) / 1e9
-print(f"{name} {n/1e9:.2f}GB fused: {fmt(fused)}  -> scan {gbs(fused,'k_scan'):.0f} GB/s")
-print(f"{name} {n/1e9:.2f}GB plan:  {fmt(plan)}  -> scan {gbs(plan,'k_scan'):.0f} GB/s, emit {gbs(plan,'k_emit'):.0f} GB/s")
+fmt = lambda kt: " ".join(f"{k}={v:.3f}" for k, v in kt)
+tot = lambda kt: sum(v for k, v in kt)
+print(f"{name} {n/1e9:.2f}GB into: {tot(fused):.3f} ms -> {n / tot(fused) / 1e6:.0f} GB/s   [{fmt(fused)}]")
+print(f"{name} {n/1e9:.2f}GB plan: {tot(plan):.3f} ms -> {n / tot(plan) / 1e6:.0f} GB/s   [{fmt(plan)}]")
