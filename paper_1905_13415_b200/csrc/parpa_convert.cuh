@@ -111,6 +111,53 @@ __device__ int conv_float64_fast(Src &s, long long &bits) {
   return 1;
 }
 
+// ---- register-window fast path (thread tier, both types in one instruction stream) -----------------
+// x0..x3 = the field's first 16 bytes (byte i of the 128-bit value = field byte i), 1 <= L <= 16.
+// Accepts [+-]?digits with at most one '.' (float64 only) — the common shapes; anything else
+// (exponents, stray bytes, empty digit strings, > 2^53 significands) returns 2 and goes to the
+// byte-at-a-time converters above, which decide validity exactly.  int64 and float64 share the
+// loop so that lanes of different numeric columns do not diverge.
+__device__ __forceinline__ int conv_window(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t L,
+                                           bool isf, long long &out) {
+  const uint32_t c0 = x0 & 0xFFu;
+  const bool neg = c0 == '-';
+  const uint32_t start = (c0 == '-' || c0 == '+') ? 1u : 0u;
+  unsigned long long m = 0;
+  uint32_t nd = 0, frac = 0, dot = 0, bad = 0;
+  const uint32_t xs[4] = {x0, x1, x2, x3};
+#pragma unroll
+  for (int w = 0; w < 4; w++) {
+    if (4u * w >= L) break;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const uint32_t i = 4u * w + j;
+      const uint32_t c = (xs[w] >> (8 * j)) & 0xFFu;
+      const uint32_t d = c - '0';
+      const bool in = i < L && i >= start;
+      const bool isd = in && d < 10u;
+      const bool isdot = in && c == '.';
+      if (isd) { m = m * 10ull + d; nd++; frac += dot; }
+      bad |= (in && !isd && !(isdot && !dot)) ? 1u : 0u;
+      dot |= isdot ? 1u : 0u;
+    }
+  }
+  if (bad || nd == 0 || (dot && !isf)) return 2;
+  if (!isf) {
+    out = neg ? (long long)(0ull - m) : (long long)m;        // < 10^16: no overflow
+    return 1;
+  }
+  if (m == 0) {
+    out = neg ? (long long)0x8000000000000000ull : 0;
+    return 1;
+  }
+  if (m > (1ull << 53)) return 2;
+  double v = (double)m;
+  if (frac) v = __ddiv_rn(v, c_pow10[frac]);                   // Clinger: one correctly rounded op
+  if (neg) v = -v;
+  out = __double_as_longlong(v);
+  return 1;
+}
+
 // ---- exact slow path ------------------------------------------------------------------------
 constexpr int DEC_MAX = 800;
 struct Decimal {

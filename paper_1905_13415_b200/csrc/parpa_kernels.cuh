@@ -598,22 +598,16 @@ __device__ __forceinline__ void flush_counters(const KArgs &a, EmitCounters &cnt
 constexpr int FCAP = 512;                   // fields per warp tile handled by E1/E2
 constexpr int RCAP = 128;                   // records per warp tile handled by E1/E2
 struct WarpScratch {
-  uint32_t bytes[2][WT / 4];                // two tiles (stages B and C), 16-byte units swizzled
+  uint32_t bytes[WT / 4 + 8];               // the tile (plain layout) + a tail pad for 16-byte windows
   uint2 fields[FCAP];                       // {offset relative to the tile (int32), length | IC << 31}
   uint32_t rows[RCAP];                      // end field index (low 16) | record delimiter position (high 16)
 };
 constexpr uint32_t FIELD_WRITTEN = 0xFFFFFFFFu;   // length marker: E1 already wrote this field
 
-__device__ __forceinline__ uint32_t swz(uint32_t p) {         // tile byte p -> scratch byte offset
-  uint32_t l = p >> 6, u = (p >> 4) & 3u;
-  return (l << 6) | (((u + (l >> 1)) & 3u) << 4) | (p & 15u);
-}
 __device__ __forceinline__ void stash_chunk(uint32_t *buf, int lane, const uint32_t (&v)[16]) {
-  uint8_t *b = reinterpret_cast<uint8_t *>(buf);
+  uint4 *b = reinterpret_cast<uint4 *>(buf) + lane * 4;
 #pragma unroll
-  for (int u = 0; u < 4; u++)
-    *reinterpret_cast<uint4 *>(b + swz((uint32_t)lane * 64u + 16u * u)) =
-        make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+  for (int u = 0; u < 4; u++) b[u] = make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
 }
 
 struct TileSrc {                       // raw field bytes: shared-memory tile copy, global before it
@@ -625,7 +619,7 @@ struct TileSrc {                       // raw field bytes: shared-memory tile co
   __device__ __forceinline__ bool next(uint8_t &c) {
     if (pos > end) return false;
     unsigned long long p = pos++;
-    c = p >= tbase ? tb[swz((uint32_t)(p - tbase))] : fetch_byte(*a, p, ok);
+    c = p >= tbase ? tb[p - tbase] : fetch_byte(*a, p, ok);
     return true;
   }
 };
@@ -641,9 +635,20 @@ __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, u
     push_defer(a, fd, ld, row, c, 1u);
     return;
   } else {
-    TileSrc src{&a, tb, tbase, fd, ld, true};
-    int res = cd->type == T_INT64 ? conv_int64(src, v) : conv_float64_fast(src, v);
-    if (!src.ok) res = 2;
+    int res = 2;
+    const unsigned long long L = ld + 1 - fd;
+    if (fd >= tbase && L <= 16) {                       // field inside the tile copy: register window
+      const uint32_t o = (uint32_t)(fd - tbase), i0 = o >> 2, sh = (o & 3u) * 8u;
+      const uint32_t *w = reinterpret_cast<const uint32_t *>(tb) + i0;
+      const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
+      res = conv_window(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                        __funnelshift_r(w3, w4, sh), (uint32_t)L, cd->type == T_FLOAT64, v);
+    }
+    if (res == 2) {
+      TileSrc src{&a, tb, tbase, fd, ld, true};
+      res = cd->type == T_INT64 ? conv_int64(src, v) : conv_float64_fast(src, v);
+      if (!src.ok) res = 2;
+    }
     if (res == 2) { push_defer(a, fd, ld, row, c, 0u); return; }
     ok = res;
     if (!ok) v = 0;
@@ -652,9 +657,26 @@ __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, u
   __stcs(cd->valid + row, (uint8_t)ok);
 }
 
+// (column c, tile row jr) -> the field index k in the warp's field list, or "missing" / "skip"
+enum { ITEM_SKIP = 0, ITEM_FIELD = 1, ITEM_MISSING = 2 };
+__device__ __forceinline__ int tile_item(const KArgs &a, const WarpScratch *ws, uint32_t c, uint32_t jr, uint32_t nrec,
+                                         uint32_t nf, uint32_t c0, unsigned long long r0, uint32_t &k, uint32_t &end,
+                                         unsigned long long &row) {
+  const uint32_t start = jr == 0 ? 0u : (ws->rows[jr - 1] & 0xFFFFu);
+  end = jr < nrec ? (ws->rows[jr] & 0xFFFFu) : nf;
+  const uint32_t cs = jr == 0 ? c0 : 0u;
+  if (c < cs) return ITEM_SKIP;                             // written by an earlier tile
+  k = start + (c - cs);
+  row = r0 + jr - a.row_base;
+  if (row >= a.cap) return ITEM_SKIP;
+  if (k < end) return ITEM_FIELD;
+  return jr < nrec ? ITEM_MISSING : ITEM_SKIP;
+}
+
 // Per-warp emission of one tile.  st = the lane's chunk-start state (global), sex = the lane's exclusive
 // tile-local summary, agg = the tile summary, prefix = everything before the tile.
-__device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, const uint32_t *tbytes, const Seg &st, SegT sex,
+__device__ void emit_tile(const KArgs &a, const ColDesc *cols, const uint8_t *num_cols, uint32_t nnum, WarpScratch *ws,
+                          const uint32_t *tbytes, const Seg &st, SegT sex,
                           SegT agg, const Seg &prefix, unsigned long long Dm, unsigned long long Fm,
                           unsigned long long Rm, unsigned long long Vm, unsigned long long tbase_g,
                           unsigned long long cbase, EmitCounters &cnt) {
@@ -718,34 +740,36 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   const uint32_t nrows = nrec + (nf > last_end ? 1u : 0u);
   const uint32_t c0 = prefix.col;
   const unsigned long long r0 = prefix.recs;
-  // (column, row) items flattened over the lanes, column-major: consecutive lanes hold consecutive
-  // rows of one column (coalesced stores); a warp touches at most two columns per step.
-  const uint32_t total = a.C * nrows;
-  const float rcp = nrows ? 1.0f / (float)nrows : 0.f;
-  for (uint32_t it = lane; it < total; it += 32) {
-    uint32_t c = __float2uint_rz(((float)it + 0.5f) * rcp);
-    uint32_t jr = it - c * nrows;
-    const ColDesc *cd = cols + c;
-    {
-      uint32_t start = jr == 0 ? 0u : (ws->rows[jr - 1] & 0xFFFFu);
-      uint32_t end = jr < nrec ? (ws->rows[jr] & 0xFFFFu) : nf;
-      uint32_t cs = jr == 0 ? c0 : 0u;
-      if (c < cs) continue;                                   // written by an earlier tile
-      uint32_t k = start + (c - cs);
-      unsigned long long row = r0 + jr - a.row_base;
-      if (row >= a.cap) continue;
+  // Column-major writes: lanes = (tile row, column group).  R = rows per group (power of two >= the
+  // tile's rows, <= 32), G = 32 / R groups; group g handles columns g, g + G, ...  With >= 17 rows a
+  // tile has one group, so every lane of a step works on the same column: the stores of a step are
+  // consecutive rows of one column (coalesced) and all lanes run the same converter.
+  const uint32_t lg = nrows > 16 ? 5u : nrows > 8 ? 4u : nrows > 4 ? 3u : nrows > 2 ? 2u : nrows > 1 ? 1u : 0u;
+  const uint32_t G = 32u >> lg;
+  const uint32_t g = (uint32_t)lane >> lg;
+  for (uint32_t rb = 0; rb < nrows; rb += 1u << lg) {
+    const uint32_t jr = rb + ((uint32_t)lane & ((1u << lg) - 1u));
+    if (jr >= nrows) continue;
+    const uint32_t start = jr == 0 ? 0u : (ws->rows[jr - 1] & 0xFFFFu);
+    const uint32_t end = jr < nrec ? (ws->rows[jr] & 0xFFFFu) : nf;
+    const uint32_t cs = jr == 0 ? c0 : 0u;
+    const unsigned long long row = r0 + jr - a.row_base;
+    if (row >= a.cap) continue;
+    const unsigned long long dpos = jr < nrec ? tbase_g + (ws->rows[jr] >> 16) : 0ull;
+    if (jr < nrec && end - start + cs < a.C && g == 0) cnt.missing++;
+    for (uint32_t c = g + (cs > g ? (cs - g + G - 1) / G * G : 0u); c < a.C; c += G) {
+      const uint32_t k = start + (c - cs);
+      const ColDesc *cd = cols + c;
       if (k < end) {
-        uint2 e = ws->fields[k];
+        const uint2 e = ws->fields[k];
         if (e.y == FIELD_WRITTEN) continue;
-        uint32_t len = e.y & 0x7FFFFFFFu;
-        unsigned long long off = tbase_g + (unsigned long long)(long long)(int32_t)e.x;
+        const uint32_t len = e.y & 0x7FFFFFFFu;
+        const unsigned long long off = tbase_g + (unsigned long long)(long long)(int32_t)e.x;
         __stcs(cd->off + row, off);
         __stcs(cd->len + row, len);
         if (cd->type != T_SPAN)
           write_value(a, cd, c, row, off, off + len - 1, (e.y >> 31) != 0, len == 0, tb, tbase_g);
-      } else if (jr < nrec) {                                 // record closed with fewer fields
-        if (k == end) cnt.missing++;
-        unsigned long long dpos = tbase_g + (ws->rows[jr] >> 16);
+      } else if (jr < nrec) {                               // record closed with fewer fields
         __stcs(cd->off + row, dpos);
         __stcs(cd->len + row, 0xFFFFFFFFu);
         if (cd->type != T_SPAN) {
@@ -770,8 +794,16 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 1) k_emit(const KArgs a, cons
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t *lut = smem;
   __shared__ ColDesc s_cols[MAX_COLS];
+  __shared__ uint8_t s_num[MAX_COLS];
+  __shared__ uint32_t s_nnum;
   build_lut(lut, dfa);
   for (int c = threadIdx.x; c < (int)a.C; c += blockDim.x) s_cols[c] = colsk.c[c];
+  if (threadIdx.x == 0) {                                   // numeric columns, in order
+    uint32_t n = 0;
+    for (uint32_t c = 0; c < a.C; c++)
+      if (colsk.c[c].type != T_SPAN) s_num[n++] = (uint8_t)c;
+    s_nnum = n;
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpScratch *ws = reinterpret_cast<WarpScratch *>(smem + LUT_BYTES) + warp;
   const uint32_t laneoff = (uint32_t)(lane & 15) * 8u;
@@ -785,7 +817,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 1) k_emit(const KArgs a, cons
     const int nvalid = cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
     uint32_t v[16];
     load_chunk(a.in + cstart, nvalid, v);
-    stash_chunk(ws->bytes[0], lane, v);
+    stash_chunk(ws->bytes, lane, v);
     const uint32_t entry = a.chunk_state[(unsigned long long)t * 32 + lane];
     unsigned long long Dm, Fm, Rm;
     if (nvalid == CHUNK) chunk_masks<true>(lut, v, nvalid, laneoff, entry, Dm, Fm, Rm);
@@ -795,7 +827,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 1) k_emit(const KArgs a, cons
     const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
     const Seg prefix = a.tinfo[t].excl;
     const Seg st = seg_op(prefix, segt_to_seg(sex, a.base + tstart));
-    emit_tile(a, s_cols, ws, ws->bytes[0], st, sex, sagg, prefix, Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
+    emit_tile(a, s_cols, s_num, s_nnum, ws, ws->bytes, st, sex, sagg, prefix, Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
   }
   flush_counters(a, cnt);
 }
