@@ -601,6 +601,9 @@ struct WarpScratch {
   uint32_t bytes[WT / 4 + 8];               // the tile (plain layout) + a tail pad for 16-byte windows
   uint2 fields[FCAP];                       // {offset relative to the tile (int32), length | IC << 31}
   uint32_t rows[RCAP];                      // end field index (low 16) | record delimiter position (high 16)
+  uint16_t dlist[FCAP];                     // delimiter positions (tile-local) | record bit << 15
+  uint32_t dmask[WT / 32], kmask[WT / 32];  // DATA / CTRL bits of the tile, 32 per word
+  uint16_t kpre[WT / 32];                   // CTRL bits before each word
 };
 constexpr uint32_t FIELD_WRITTEN = 0xFFFFFFFFu;   // length marker: E1 already wrote this field
 
@@ -673,69 +676,139 @@ __device__ __forceinline__ int tile_item(const KArgs &a, const WarpScratch *ws, 
   return jr < nrec ? ITEM_MISSING : ITEM_SKIP;
 }
 
-// Per-warp emission of one tile.  st = the lane's chunk-start state (global), sex = the lane's exclusive
-// tile-local summary, agg = the tile summary, prefix = everything before the tile.
-__device__ void emit_tile(const KArgs &a, const ColDesc *cols, const uint8_t *num_cols, uint32_t nnum, WarpScratch *ws,
-                          const uint32_t *tbytes, const Seg &st, SegT sex,
-                          SegT agg, const Seg &prefix, unsigned long long Dm, unsigned long long Fm,
-                          unsigned long long Rm, unsigned long long Vm, unsigned long long tbase_g,
-                          unsigned long long cbase, EmitCounters &cnt) {
+// Per-warp emission of one tile (S6+S7).  prefix = everything before the tile (seed included).
+// E1a: each lane appends its delimiters (tile position | record bit) to the warp's delimiter list at
+//      its exclusive delimiter count, and publishes its DATA / CTRL words and CTRL prefix counts.
+// E1b: one lane per field: the first / last DATA byte between the two delimiters from the DATA words
+//      (ffs / clz, usually one word), inner control bytes from the CTRL prefix counts, record and
+//      column from ballots over the record bits.  Only field 0 can have begun in an earlier tile; it
+//      is combined with the prefix's open-field carry (P:408-414 extended with the carries).
+// E2:  column-major writes (below).
+__device__ __forceinline__ uint32_t kcount(const WarpScratch *ws, uint32_t x) {   // CTRL bytes before x
+  return ws->kpre[x >> 5] + __popc(ws->kmask[x >> 5] & ((1u << (x & 31u)) - 1u));
+}
+__device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, const Seg &prefix,
+                          unsigned long long Dm, unsigned long long Fm, unsigned long long Rm,
+                          unsigned long long Vm, unsigned long long tbase_g, unsigned long long cbase,
+                          EmitCounters &cnt) {
   const int lane = threadIdx.x & 31;
-  const uint32_t nf = agg.cnt >> 16, nrec = agg.cnt & 0xFFFFu;
+  const unsigned long long Km = Vm & ~Dm & ~Fm;
+  // per-lane (delimiters << 16 | records) and CTRL counts -> exclusive offsets, tile totals
+  const uint32_t mine = (uint32_t)__popcll(Rm) | ((uint32_t)__popcll(Fm) << 16);
+  const uint32_t kmine = (uint32_t)__popcll(Km);
+  uint32_t inc = mine, kinc = kmine;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d), ko = __shfl_up_sync(0xffffffffu, kinc, d);
+    if (lane >= d) { inc += o; kinc += ko; }
+  }
+  const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+  const uint32_t nf = tot >> 16, nrec = tot & 0xFFFFu;
   if (nf > (uint32_t)FCAP || nrec >= (uint32_t)RCAP) {       // warp-uniform: dense tile, direct path
-    emit_chunk(a, cols, st, Dm, Fm, Rm, Vm, cbase, cnt);
+    SegT sagg;
+    const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
+    emit_chunk(a, cols, seg_op(prefix, segt_to_seg(sex, tbase_g)), Dm, Fm, Rm, Vm, cbase, cnt);
     return;
   }
-  // ---- E1 ----
+  // ---- E1a ----
   {
-    unsigned long long Km = Vm & ~Dm & ~Fm;
-    unsigned long long r = st.recs;
-    uint32_t c = st.col;
-    unsigned long long cfd = st.fd, cld = st.ld;
-    uint32_t cfl = st.flags & (F_IC | F_PC | F_PRE);
-    uint32_t k = sex.cnt >> 16, j = sex.cnt & 0xFFFFu;
-    int prev = -1;
+    uint32_t k = (inc - mine) >> 16;
+    const uint32_t base = (uint32_t)lane * CHUNK;
     unsigned long long fm = Fm;
     while (fm) {
-      int p = lsb64(fm);
+      const int p = lsb64(fm);
       fm &= fm - 1ull;
-      unsigned long long rng = below(p) & above(prev);
-      int fd, ld;
-      uint32_t fl = open_summary(Dm & rng, Km & rng, fd, ld);
-      unsigned long long sfd = fd < 0 ? NONE : cbase + (unsigned)fd;
-      unsigned long long sld = fd < 0 ? NONE : cbase + (unsigned)ld;
-      if (prev >= 0) { cfd = sfd; cld = sld; cfl = fl; }
-      else open_combine(cfd, cld, cfl, sfd, sld, fl);
-      const unsigned long long dpos = cbase + (unsigned)p;
-      uint2 e;
-      if (cfd == NONE) {
-        e = make_uint2((uint32_t)(dpos - tbase_g), 0u);
-      } else {
-        unsigned long long L = cld + 1 - cfd;
-        long long rel = (long long)cfd - (long long)tbase_g;
-        if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {     // huge / far-away field: write it here
-          emit_field(a, cols, r, c, cfd, cld, cfl, dpos, cnt);
-          e = make_uint2(0u, FIELD_WRITTEN);
-          if (c >= a.C) cnt.extra--;                          // counted again below
-        } else {
-          e = make_uint2((uint32_t)(int32_t)rel, (uint32_t)L | ((cfl & F_IC) ? 0x80000000u : 0u));
+      ws->dlist[k++] = (uint16_t)((base + (uint32_t)p) | ((uint32_t)((Rm >> p) & 1ull) << 15));
+    }
+    ws->dmask[2 * lane] = (uint32_t)Dm;
+    ws->dmask[2 * lane + 1] = (uint32_t)(Dm >> 32);
+    ws->kmask[2 * lane] = (uint32_t)Km;
+    ws->kmask[2 * lane + 1] = (uint32_t)(Km >> 32);
+    const uint32_t kex = kinc - kmine;
+    ws->kpre[2 * lane] = (uint16_t)kex;
+    ws->kpre[2 * lane + 1] = (uint16_t)(kex + __popc((uint32_t)Km));
+  }
+  __syncwarp();
+  // ---- E1b ----
+  {
+    const uint32_t c0 = prefix.col;
+    uint32_t jcarry = 0;
+    int lastrec = -1;
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint32_t kb = 0; kb < nf; kb += 32) {
+      const uint32_t k = kb + (uint32_t)lane;
+      const bool act = k < nf;
+      const uint32_t dl = act ? ws->dlist[k] : 0u;
+      const uint32_t p = dl & 0x7FFu;
+      const bool isrec = act && (dl >> 15);
+      const unsigned recm = __ballot_sync(0xffffffffu, isrec);
+      const uint32_t jr = jcarry + __popc(recm & lt);
+      const unsigned before = recm & lt;
+      const int lr = before ? (int)(kb + 31u - __clz(before)) : lastrec;
+      const uint32_t c = lr >= 0 ? k - (uint32_t)lr - 1u : c0 + k;
+      if (act) {
+        const uint32_t x = k ? (ws->dlist[k - 1] & 0x7FFu) + 1u : 0u;   // field bytes [x, p)
+        int fd = -1, ld = -1;
+        if (x < p) {
+          uint32_t w = x >> 5;
+          uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu << (x & 31u));
+          const uint32_t wp = p >> 5;
+          while (!bits && w < wp) bits = ws->dmask[++w];
+          if (bits) {
+            const uint32_t f = (w << 5) + (uint32_t)__ffs(bits) - 1u;
+            if (f < p) fd = (int)f;
+          }
         }
+        if (fd >= 0) {
+          const uint32_t y = p - 1u;
+          uint32_t w = y >> 5;
+          uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu >> (31u - (y & 31u)));
+          while (!bits) bits = ws->dmask[--w];
+          ld = (int)((w << 5) + 31u - (uint32_t)__clz(bits));
+        }
+        uint32_t fl = 0;
+        if (ld > fd && kcount(ws, (uint32_t)ld) > kcount(ws, (uint32_t)fd + 1u)) fl |= F_IC;
+        unsigned long long cfd = fd >= 0 ? tbase_g + (unsigned)fd : NONE;
+        unsigned long long cld = fd >= 0 ? tbase_g + (unsigned)ld : NONE;
+        uint32_t cfl = fl;
+        const unsigned long long dpos = tbase_g + p;
+        if (k == 0) {                                         // may continue a field of an earlier tile
+          if (fd >= 0) {
+            if (kcount(ws, (uint32_t)fd) > 0u) fl |= F_PRE;
+            if (kcount(ws, p) > kcount(ws, (uint32_t)ld + 1u)) fl |= F_PC;
+          } else if (kcount(ws, p) > 0u) {
+            fl |= F_PRE;
+          }
+          unsigned long long sfd = cfd, sld = cld;
+          cfd = prefix.fd; cld = prefix.ld;
+          cfl = prefix.flags & (F_IC | F_PC | F_PRE);
+          open_combine(cfd, cld, cfl, sfd, sld, fl);
+        }
+        uint2 e;
+        if (cfd == NONE) {
+          e = make_uint2(p, 0u);
+        } else {
+          const unsigned long long L = cld + 1 - cfd;
+          const long long rel = (long long)cfd - (long long)tbase_g;
+          if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away field: write it here
+            emit_field(a, cols, prefix.recs + jr, c, cfd, cld, cfl, dpos, cnt);
+            e = make_uint2(0u, FIELD_WRITTEN);
+            if (c >= a.C) cnt.extra--;                        // counted again below
+          } else {
+            e = make_uint2((uint32_t)(int32_t)rel, (uint32_t)L | ((cfl & F_IC) ? 0x80000000u : 0u));
+          }
+        }
+        ws->fields[k] = e;
+        if (c >= a.C) cnt.extra++;
+        if (isrec) ws->rows[jr] = (k + 1u) | (p << 16);
       }
-      ws->fields[k++] = e;
-      if (c >= a.C) cnt.extra++;
-      if ((Rm >> p) & 1ull) {
-        ws->rows[j++] = k | ((uint32_t)(dpos - tbase_g) << 16);
-        r++;
-        c = 0;
-      } else {
-        c++;
-      }
-      prev = p;
+      jcarry += (uint32_t)__popc(recm);
+      if (recm) lastrec = (int)(kb + 31u - __clz(recm));
     }
   }
   __syncwarp();
   // ---- E2 ----
-  const uint8_t *tb = reinterpret_cast<const uint8_t *>(tbytes);
+  const uint8_t *tb = reinterpret_cast<const uint8_t *>(ws->bytes);
   const uint32_t last_end = nrec ? (ws->rows[nrec - 1] & 0xFFFFu) : 0u;
   const uint32_t nrows = nrec + (nf > last_end ? 1u : 0u);
   const uint32_t c0 = prefix.col;
@@ -794,16 +867,8 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 1) k_emit(const KArgs a, cons
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t *lut = smem;
   __shared__ ColDesc s_cols[MAX_COLS];
-  __shared__ uint8_t s_num[MAX_COLS];
-  __shared__ uint32_t s_nnum;
   build_lut(lut, dfa);
   for (int c = threadIdx.x; c < (int)a.C; c += blockDim.x) s_cols[c] = colsk.c[c];
-  if (threadIdx.x == 0) {                                   // numeric columns, in order
-    uint32_t n = 0;
-    for (uint32_t c = 0; c < a.C; c++)
-      if (colsk.c[c].type != T_SPAN) s_num[n++] = (uint8_t)c;
-    s_nnum = n;
-  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpScratch *ws = reinterpret_cast<WarpScratch *>(smem + LUT_BYTES) + warp;
   const uint32_t laneoff = (uint32_t)(lane & 15) * 8u;
@@ -823,11 +888,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 1) k_emit(const KArgs a, cons
     if (nvalid == CHUNK) chunk_masks<true>(lut, v, nvalid, laneoff, entry, Dm, Fm, Rm);
     else chunk_masks<false>(lut, v, nvalid, laneoff, entry, Dm, Fm, Rm);
     const unsigned long long Vm = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull);
-    SegT sagg;
-    const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
-    const Seg prefix = a.tinfo[t].excl;
-    const Seg st = seg_op(prefix, segt_to_seg(sex, a.base + tstart));
-    emit_tile(a, s_cols, s_num, s_nnum, ws, ws->bytes, st, sex, sagg, prefix, Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
+    emit_tile(a, s_cols, ws, a.tinfo[t].excl, Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
   }
   flush_counters(a, cnt);
 }
