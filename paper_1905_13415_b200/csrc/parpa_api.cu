@@ -143,6 +143,7 @@ struct Work {
   Seg *bagg = nullptr, *bincl = nullptr, *tot_seg = nullptr;
   TileInfo *tinfo = nullptr;
   uint8_t *chunk_state = nullptr;
+  unsigned long long *masks = nullptr;
   DeferItem *dq = nullptr;
   Stats *stats = nullptr;
   uint8_t *aligned_in = nullptr;
@@ -172,6 +173,7 @@ int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cu
   size_t o_tot = o; o = align_up(o + sizeof(Seg) + 16);
   size_t o_tinfo = o; o = align_up(o + nt * sizeof(TileInfo));
   size_t o_cs = o; o = align_up(o + nt * 32);
+  size_t o_mk = o; o = align_up(o + nt * 96 * 8);
   size_t o_dq = o; o = align_up(o + (size_t)w.dq_cap * sizeof(DeferItem));
   size_t o_st = o; o = align_up(o + sizeof(Stats));
   size_t o_in = o; if (need_aligned_copy) o = align_up(o + len);
@@ -190,6 +192,7 @@ int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cu
   w.tot_tau = (uint32_t *)(b + o_tot + sizeof(Seg));
   w.tinfo = (TileInfo *)(b + o_tinfo);
   w.chunk_state = b + o_cs;
+  w.masks = (unsigned long long *)(b + o_mk);
   w.dq = (DeferItem *)(b + o_dq);
   w.stats = (Stats *)(b + o_st);
   w.aligned_in = need_aligned_copy ? b + o_in : nullptr;
@@ -231,6 +234,7 @@ void make_args(KArgs &a, const Work &w, const uint8_t *in, uint64_t len) {
   a.tot_seg = w.tot_seg;
   a.tinfo = w.tinfo;
   a.chunk_state = w.chunk_state;
+  a.masks = w.masks;
   a.ctrl = w.ctrl;
   a.dq = w.dq;
   a.dq_cap = w.dq_cap;
@@ -314,7 +318,7 @@ int launch_emit(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, 
   if (rc) return rc;
   {
     Launch L(s, "k_emit");
-    k_emit<<<grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s>>>(a, k, ck);
+    k_emit<<<grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s>>>(a, ck);
   }
   CK(cudaGetLastError());
   if (launches) (*launches)++;

@@ -100,6 +100,7 @@ struct KArgs {
   Seg *tot_seg;                      // seed ∘ Seg of the whole range
   TileInfo *tinfo;                   // [ntiles]
   uint8_t *chunk_state;              // [ntiles * 32] device entry state of each chunk
+  unsigned long long *masks;         // [ntiles][3][32] DATA / DELIM / RECORD masks of each chunk
   Ctrl *ctrl;
   DeferItem *dq;
   uint32_t dq_cap, strict;
@@ -597,15 +598,17 @@ __device__ __forceinline__ void flush_counters(const KArgs &a, EmitCounters &cnt
 //     "partition by column, then convert per column" at warp-tile granularity.
 constexpr int FCAP = 512;                   // fields per warp tile handled by E1/E2
 constexpr int RCAP = 128;                   // records per warp tile handled by E1/E2
-struct WarpScratch {
+struct alignas(16) WarpScratch {
   uint32_t bytes[WT / 4 + 8];               // the tile (plain layout) + a tail pad for 16-byte windows
-  uint2 fields[FCAP];                       // {offset relative to the tile (int32), length | IC << 31}
+  uint32_t fields[FCAP];                    // tile offset (11 bits) | length << 11 (12 bits) | IC << 31
+  uint2 f0;                                 // field 0 when it starts before the tile: {rel, len | IC << 31}
   uint32_t rows[RCAP];                      // end field index (low 16) | record delimiter position (high 16)
   uint16_t dlist[FCAP];                     // delimiter positions (tile-local) | record bit << 15
   uint32_t dmask[WT / 32], kmask[WT / 32];  // DATA / CTRL bits of the tile, 32 per word
   uint16_t kpre[WT / 32];                   // CTRL bits before each word
 };
-constexpr uint32_t FIELD_WRITTEN = 0xFFFFFFFFu;   // length marker: E1 already wrote this field
+constexpr uint32_t FIELD_WRITTEN = 0xFFFFFFFFu;   // E1 already wrote this field
+constexpr uint32_t FIELD_FAR = 0xFFFFFFFEu;       // field 0 began before the tile: see WarpScratch::f0
 
 __device__ __forceinline__ void stash_chunk(uint32_t *buf, int lane, const uint32_t (&v)[16]) {
   uint4 *b = reinterpret_cast<uint4 *>(buf) + lane * 4;
@@ -784,18 +787,22 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
           cfl = prefix.flags & (F_IC | F_PC | F_PRE);
           open_combine(cfd, cld, cfl, sfd, sld, fl);
         }
-        uint2 e;
+        uint32_t e;
         if (cfd == NONE) {
-          e = make_uint2(p, 0u);
+          e = p;                                              // empty: offset = delimiter, length 0
         } else {
           const unsigned long long L = cld + 1 - cfd;
           const long long rel = (long long)cfd - (long long)tbase_g;
-          if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away field: write it here
+          const uint32_t ic = (cfl & F_IC) ? 0x80000000u : 0u;
+          if (rel >= 0 && L <= (unsigned long long)WT) {
+            e = (uint32_t)rel | ((uint32_t)L << 11) | ic;
+          } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
             emit_field(a, cols, prefix.recs + jr, c, cfd, cld, cfl, dpos, cnt);
-            e = make_uint2(0u, FIELD_WRITTEN);
+            e = FIELD_WRITTEN;
             if (c >= a.C) cnt.extra--;                        // counted again below
-          } else {
-            e = make_uint2((uint32_t)(int32_t)rel, (uint32_t)L | ((cfl & F_IC) ? 0x80000000u : 0u));
+          } else {                                            // k == 0 only
+            ws->f0 = make_uint2((uint32_t)(int32_t)rel, (uint32_t)L | ic);
+            e = FIELD_FAR;
           }
         }
         ws->fields[k] = e;
@@ -834,14 +841,24 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
       const uint32_t k = start + (c - cs);
       const ColDesc *cd = cols + c;
       if (k < end) {
-        const uint2 e = ws->fields[k];
-        if (e.y == FIELD_WRITTEN) continue;
-        const uint32_t len = e.y & 0x7FFFFFFFu;
-        const unsigned long long off = tbase_g + (unsigned long long)(long long)(int32_t)e.x;
+        const uint32_t e = ws->fields[k];
+        if (e == FIELD_WRITTEN) continue;
+        uint32_t len;
+        unsigned long long off;
+        bool ic;
+        if (e == FIELD_FAR) {
+          const uint2 f = ws->f0;
+          off = tbase_g + (unsigned long long)(long long)(int32_t)f.x;
+          len = f.y & 0x7FFFFFFFu;
+          ic = (f.y >> 31) != 0;
+        } else {
+          off = tbase_g + (e & 0x7FFu);
+          len = (e >> 11) & 0xFFFu;
+          ic = (e >> 31) != 0;
+        }
         __stcs(cd->off + row, off);
         __stcs(cd->len + row, len);
-        if (cd->type != T_SPAN)
-          write_value(a, cd, c, row, off, off + len - 1, (e.y >> 31) != 0, len == 0, tb, tbase_g);
+        if (cd->type != T_SPAN) write_value(a, cd, c, row, off, off + len - 1, ic, len == 0, tb, tbase_g);
       } else if (jr < nrec) {                               // record closed with fewer fields
         __stcs(cd->off + row, dpos);
         __stcs(cd->len + row, 0xFFFFFFFFu);
@@ -861,32 +878,30 @@ namespace parpa {
 
 // ---- two-phase emit kernel (per warp tile, from the stored prefixes; no look-back) ------------------
 constexpr int EMIT_WARPS = 16;
-constexpr size_t EMIT_SMEM = LUT_BYTES + EMIT_WARPS * sizeof(WarpScratch);
+constexpr size_t EMIT_SMEM = EMIT_WARPS * sizeof(WarpScratch);
 
-__global__ void __launch_bounds__(EMIT_WARPS * 32, 1) k_emit(const KArgs a, const DfaK dfa, const ColsK colsk) {
+// S6+S7 per warp tile from what the scan half stored: the DATA / DELIM / RECORD masks of every chunk
+// (k_pass2) and the tile prefix (k_seg_scan).  No LUT, no re-simulation: 2 CTAs per SM.
+__global__ void __launch_bounds__(EMIT_WARPS * 32, 2) k_emit(const KArgs a, const ColsK colsk) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint8_t *lut = smem;
   __shared__ ColDesc s_cols[MAX_COLS];
-  build_lut(lut, dfa);
   for (int c = threadIdx.x; c < (int)a.C; c += blockDim.x) s_cols[c] = colsk.c[c];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpScratch *ws = reinterpret_cast<WarpScratch *>(smem + LUT_BYTES) + warp;
-  const uint32_t laneoff = (uint32_t)(lane & 15) * 8u;
+  WarpScratch *ws = reinterpret_cast<WarpScratch *>(smem) + warp;
   EmitCounters cnt{0ull, 0ull, 0u};
   __syncthreads();
   const uint32_t gw = blockIdx.x * EMIT_WARPS + warp, nw = gridDim.x * EMIT_WARPS;
-  const uint32_t nwt = a.ntiles;
-  for (uint32_t t = gw; t < nwt; t += nw) {
+  for (uint32_t t = gw; t < a.ntiles; t += nw) {
     const unsigned long long tstart = (unsigned long long)t * WT;
     const unsigned long long cstart = tstart + (unsigned long long)lane * CHUNK;
     const int nvalid = cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
-    uint32_t v[16];
-    load_chunk(a.in + cstart, nvalid, v);
-    stash_chunk(ws->bytes, lane, v);
-    const uint32_t entry = a.chunk_state[(unsigned long long)t * 32 + lane];
-    unsigned long long Dm, Fm, Rm;
-    if (nvalid == CHUNK) chunk_masks<true>(lut, v, nvalid, laneoff, entry, Dm, Fm, Rm);
-    else chunk_masks<false>(lut, v, nvalid, laneoff, entry, Dm, Fm, Rm);
+    {
+      uint32_t v[16];
+      load_chunk(a.in + cstart, nvalid, v);
+      stash_chunk(ws->bytes, lane, v);
+    }
+    const unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;
+    const unsigned long long Dm = mk[0], Fm = mk[32], Rm = mk[64];
     const unsigned long long Vm = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull);
     emit_tile(a, s_cols, ws, a.tinfo[t].excl, Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
   }

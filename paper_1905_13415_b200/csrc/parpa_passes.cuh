@@ -132,6 +132,10 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 2) k_pass2(const KArgs a, con
       int p = first_inv_in_chunk(smem, a.in + cstart, nv, laneoff, entry);
       if (p >= 0) atomicMax(&a.ctrl->inv_neg, ~(a.base + cstart + (unsigned)p));
     }
+    unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;   // for k_emit
+    mk[0] = Dm;
+    mk[32] = Fm;
+    mk[64] = Rm;
     const unsigned long long Vm = nv >= 64 ? ~0ull : ((1ull << nv) - 1ull);
     SegT s = chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK);
 #pragma unroll
