@@ -116,34 +116,53 @@ __device__ int conv_float64_fast(Src &s, long long &bits) {
 // Accepts [+-]?digits with at most one '.' (float64 only) — the common shapes; anything else
 // (exponents, stray bytes, empty digit strings, > 2^53 significands) returns 2 and goes to the
 // byte-at-a-time converters above, which decide validity exactly.  int64 and float64 share the
-// loop so that lanes of different numeric columns do not diverge.
+// instruction stream so that lanes of different numeric columns do not diverge.
+// Four characters per step (SWAR): classify digits / '.' with carry-free byte arithmetic, turn the
+// sign into a leading zero digit and drop the '.' (shift the bytes before it up by one, so that it
+// becomes a leading zero of the step, which then contributes one digit less), right-align the step's
+// characters and fold them as four decimal digits.
+__device__ __forceinline__ uint32_t digits4(uint32_t d) {          // byte 0 = most significant digit
+  const uint32_t t = d * 10u + (d >> 8);                           // bytes 0, 2: two-digit pairs
+  return (t & 0xFFu) * 100u + ((t >> 16) & 0xFFu);
+}
 __device__ __forceinline__ int conv_window(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t L,
                                            bool isf, long long &out) {
   const uint32_t c0 = x0 & 0xFFu;
   const bool neg = c0 == '-';
-  const uint32_t start = (c0 == '-' || c0 == '+') ? 1u : 0u;
-  unsigned long long m = 0;
-  uint32_t nd = 0, frac = 0, dot = 0, bad = 0;
+  const uint32_t sgn = (c0 == '-' || c0 == '+') ? 1u : 0u;
+  if (sgn) x0 = (x0 & 0xFFFFFF00u) | 0x30u;                        // sign -> leading '0'
   const uint32_t xs[4] = {x0, x1, x2, x3};
+  unsigned long long m = 0;
+  uint32_t bad = 0, ndots = 0, dotpos = 0;
 #pragma unroll
   for (int w = 0; w < 4; w++) {
     if (4u * w >= L) break;
-#pragma unroll
-    for (int j = 0; j < 4; j++) {
-      const uint32_t i = 4u * w + j;
-      const uint32_t c = (xs[w] >> (8 * j)) & 0xFFu;
-      const uint32_t d = c - '0';
-      const bool in = i < L && i >= start;
-      const bool isd = in && d < 10u;
-      const bool isdot = in && c == '.';
-      if (isd) { m = m * 10ull + d; nd++; frac += dot; }
-      bad |= (in && !isd && !(isdot && !dot)) ? 1u : 0u;
-      dot |= isdot ? 1u : 0u;
+    const uint32_t k = min(4u, L - 4u * w);                        // characters of the field in this step
+    const uint32_t x = xs[w];
+    uint32_t d = x ^ 0x30303030u;                                  // digits -> 0..9
+    const uint32_t t = x ^ 0x2E2E2E2Eu;                            // '.' -> 0
+    const uint32_t vm = k == 4u ? 0x80808080u : (0x80808080u & ((1u << (8u * k)) - 1u));
+    const uint32_t dotm = ~(((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & vm;
+    const uint32_t ndm = (((d & 0x7F7F7F7Fu) + 0x76767676u) | d) & vm;
+    bad |= ndm & ~dotm;
+    uint32_t kd = k;                                               // digits this step contributes
+    if (dotm) {
+      const uint32_t q = ((uint32_t)__ffs(dotm) - 1u) >> 3;       // byte of the '.'
+      ndots += (uint32_t)__popc(dotm);
+      dotpos = 4u * w + q;
+      const uint32_t lo = (1u << (8u * q)) - 1u;                   // bytes before the '.'
+      const uint32_t hi = q == 3u ? 0u : (0xFFFFFFFFu << (8u * (q + 1u)));
+      d = ((d & lo) << 8) | (d & hi);                              // drop it: a leading zero of the step
+      kd--;
     }
+    if (k < 4u) d <<= 8u * (4u - k);                               // right-align (zeros lead)
+    const uint32_t p10 = kd == 4u ? 10000u : kd == 3u ? 1000u : kd == 2u ? 100u : kd == 1u ? 10u : 1u;
+    m = m * p10 + digits4(d);
   }
-  if (bad || nd == 0 || (dot && !isf)) return 2;
+  const uint32_t nd = L - sgn - ndots;
+  if (bad || ndots > 1u || nd == 0u || (ndots && !isf)) return 2;
   if (!isf) {
-    out = neg ? (long long)(0ull - m) : (long long)m;        // < 10^16: no overflow
+    out = neg ? (long long)(0ull - m) : (long long)m;              // < 10^16: no overflow
     return 1;
   }
   if (m == 0) {
@@ -151,8 +170,9 @@ __device__ __forceinline__ int conv_window(uint32_t x0, uint32_t x1, uint32_t x2
     return 1;
   }
   if (m > (1ull << 53)) return 2;
+  const uint32_t frac = ndots ? L - 1u - dotpos : 0u;
   double v = (double)m;
-  if (frac) v = __ddiv_rn(v, c_pow10[frac]);                   // Clinger: one correctly rounded op
+  if (frac) v = __ddiv_rn(v, c_pow10[frac]);                       // Clinger: one correctly rounded op
   if (neg) v = -v;
   out = __double_as_longlong(v);
   return 1;

@@ -818,54 +818,57 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   const uint8_t *tb = reinterpret_cast<const uint8_t *>(ws->bytes);
   const uint32_t last_end = nrec ? (ws->rows[nrec - 1] & 0xFFFFu) : 0u;
   const uint32_t nrows = nrec + (nf > last_end ? 1u : 0u);
+  if (nrows == 0) {                                         // no delimiter: the open field continues
+    __syncwarp();
+    return;
+  }
   const uint32_t c0 = prefix.col;
   const unsigned long long r0 = prefix.recs;
-  // Column-major writes: lanes = (tile row, column group).  R = rows per group (power of two >= the
-  // tile's rows, <= 32), G = 32 / R groups; group g handles columns g, g + G, ...  With >= 17 rows a
-  // tile has one group, so every lane of a step works on the same column: the stores of a step are
-  // consecutive rows of one column (coalesced) and all lanes run the same converter.
-  const uint32_t lg = nrows > 16 ? 5u : nrows > 8 ? 4u : nrows > 4 ? 3u : nrows > 2 ? 2u : nrows > 1 ? 1u : 0u;
-  const uint32_t G = 32u >> lg;
-  const uint32_t g = (uint32_t)lane >> lg;
-  for (uint32_t rb = 0; rb < nrows; rb += 1u << lg) {
-    const uint32_t jr = rb + ((uint32_t)lane & ((1u << lg) - 1u));
-    if (jr >= nrows) continue;
-    const uint32_t start = jr == 0 ? 0u : (ws->rows[jr - 1] & 0xFFFFu);
-    const uint32_t end = jr < nrec ? (ws->rows[jr] & 0xFFFFu) : nf;
-    const uint32_t cs = jr == 0 ? c0 : 0u;
-    const unsigned long long row = r0 + jr - a.row_base;
+  // Column-major writes: (column, tile row) items flattened over the lanes, rows fastest, so a warp
+  // step stores consecutive rows of one or two columns (coalesced) with every lane busy; numeric
+  // columns share one converter, so mixed int / float steps do not diverge.
+  const uint32_t total = a.C * nrows;
+  uint32_t c = (uint32_t)lane / nrows, jr = (uint32_t)lane - c * nrows;   // nrows >= 1 here
+  const uint32_t dc = 32u / nrows, djr = 32u - dc * nrows;
+  for (uint32_t it = lane; it < total; it += 32) {
+    const uint32_t ci = c, ji = jr;
+    jr += djr;
+    c += dc;
+    if (jr >= nrows) { jr -= nrows; c++; }
+    const uint32_t start = ji == 0 ? 0u : (ws->rows[ji - 1] & 0xFFFFu);
+    const uint32_t end = ji < nrec ? (ws->rows[ji] & 0xFFFFu) : nf;
+    const uint32_t cs = ji == 0 ? c0 : 0u;
+    if (ci < cs) continue;                                  // written by an earlier tile
+    const unsigned long long row = r0 + ji - a.row_base;
     if (row >= a.cap) continue;
-    const unsigned long long dpos = jr < nrec ? tbase_g + (ws->rows[jr] >> 16) : 0ull;
-    if (jr < nrec && end - start + cs < a.C && g == 0) cnt.missing++;
-    for (uint32_t c = g + (cs > g ? (cs - g + G - 1) / G * G : 0u); c < a.C; c += G) {
-      const uint32_t k = start + (c - cs);
-      const ColDesc *cd = cols + c;
-      if (k < end) {
-        const uint32_t e = ws->fields[k];
-        if (e == FIELD_WRITTEN) continue;
-        uint32_t len;
-        unsigned long long off;
-        bool ic;
-        if (e == FIELD_FAR) {
-          const uint2 f = ws->f0;
-          off = tbase_g + (unsigned long long)(long long)(int32_t)f.x;
-          len = f.y & 0x7FFFFFFFu;
-          ic = (f.y >> 31) != 0;
-        } else {
-          off = tbase_g + (e & 0x7FFu);
-          len = (e >> 11) & 0xFFFu;
-          ic = (e >> 31) != 0;
-        }
-        __stcs(cd->off + row, off);
-        __stcs(cd->len + row, len);
-        if (cd->type != T_SPAN) write_value(a, cd, c, row, off, off + len - 1, ic, len == 0, tb, tbase_g);
-      } else if (jr < nrec) {                               // record closed with fewer fields
-        __stcs(cd->off + row, dpos);
-        __stcs(cd->len + row, 0xFFFFFFFFu);
-        if (cd->type != T_SPAN) {
-          __stcs(reinterpret_cast<long long *>(cd->val) + row, cd->has_def ? cd->def_bits : 0ll);
-          __stcs(cd->valid + row, (uint8_t)(cd->has_def ? 1 : 0));
-        }
+    const uint32_t k = start + (ci - cs);
+    const ColDesc *cd = cols + ci;
+    if (k < end) {
+      const uint32_t e = ws->fields[k];
+      if (e == FIELD_WRITTEN) continue;
+      uint32_t len;
+      unsigned long long off;
+      bool ic;
+      if (e == FIELD_FAR) {
+        const uint2 f = ws->f0;
+        off = tbase_g + (unsigned long long)(long long)(int32_t)f.x;
+        len = f.y & 0x7FFFFFFFu;
+        ic = (f.y >> 31) != 0;
+      } else {
+        off = tbase_g + (e & 0x7FFu);
+        len = (e >> 11) & 0xFFFu;
+        ic = (e >> 31) != 0;
+      }
+      __stcs(cd->off + row, off);
+      __stcs(cd->len + row, len);
+      if (cd->type != T_SPAN) write_value(a, cd, ci, row, off, off + len - 1, ic, len == 0, tb, tbase_g);
+    } else if (ji < nrec) {                                 // record closed with fewer fields
+      if (k == end) cnt.missing++;
+      __stcs(cd->off + row, tbase_g + (ws->rows[ji] >> 16));
+      __stcs(cd->len + row, 0xFFFFFFFFu);
+      if (cd->type != T_SPAN) {
+        __stcs(reinterpret_cast<long long *>(cd->val) + row, cd->has_def ? cd->def_bits : 0ll);
+        __stcs(cd->valid + row, (uint8_t)(cd->has_def ? 1 : 0));
       }
     }
   }

@@ -71,7 +71,8 @@ def main():
     rb = num(r["dram__bytes_read.sum"][0]) * scale.get(r["dram__bytes_read.sum"][1], 1)
     wb = num(r["dram__bytes_write.sum"][0]) * scale.get(r["dram__bytes_write.sum"][1], 1)
     tu = r["gpu__time_duration.sum"][1]
-    t = num(r["gpu__time_duration.sum"][0]) * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}.get(tu, 1e-9)
+    t = num(r["gpu__time_duration.sum"][0]) * {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6,
+                                                "msecond": 1e-3, "ms": 1e-3, "s": 1.0}.get(tu, 1e-9)
     print(f"  dram_read_bytes  {rb:.4e}\n  dram_write_bytes {wb:.4e}\n  dram_total_bytes {rb + wb:.4e}")
     print(f"  dram_gbs         {(rb + wb) / t / 1e9:.1f}")
     if len(sys.argv) > 2:

@@ -1,0 +1,75 @@
+// Host build of the device converter in paper_1905_13415_b200/csrc/parpa_convert.cuh (shims below),
+// checked against libc strtod / strtoll on random short numeric strings.  Exercised by
+// tests/test_convert_host.py; no GPU needed.
+#include <algorithm>
+#include <cerrno>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <string>
+#define __device__
+#define __host__
+#define __forceinline__ inline
+#define __constant__
+static inline int __ffs(uint32_t x) { return __builtin_ffs(x); }
+static inline int __popc(uint32_t x) { return __builtin_popcount(x); }
+static inline double __ddiv_rn(double a, double b) { return a / b; }
+static inline double __dmul_rn(double a, double b) { return a * b; }
+static inline long long __double_as_longlong(double d) { long long r; memcpy(&r, &d, 8); return r; }
+static inline double __longlong_as_double(long long x) { double r; memcpy(&r, &x, 8); return r; }
+static inline unsigned long long __umul64hi(unsigned long long a, unsigned long long b) {
+  return (unsigned long long)(((unsigned __int128)a * b) >> 64);
+}
+using std::min;
+using std::max;
+#include "../../paper_1905_13415_b200/csrc/parpa_convert.cuh"
+
+int main(int argc, char **argv) {
+  const long iters = argc > 1 ? atol(argv[1]) : 2000000;
+  std::mt19937_64 r(12345);
+  long bad = 0, n = 0;
+  const char *fixed[] = {"12.5", "1234.567", "123.4567", ".5", "5.", "-0.0", "+7", "-73.987654", "0.001", "100",
+                         "9007199254740993", "1.2.3", "-", ".", "1e5", "1234567.12345678", "99999999999999.9",
+                         "-.5", "+.", "0", "-0", "007", "1234", "12345", "123456789012345"};
+  const int nfixed = sizeof(fixed) / sizeof(fixed[0]);
+  for (long it = 0; it < iters + nfixed; it++) {
+    std::string f;
+    if (it < nfixed) {
+      f = fixed[it];
+    } else {
+      const int L = 1 + (int)(r() % 16);
+      const char al[] = "0123456789.-+eE";
+      for (int i = 0; i < L; i++) f += (r() % 10 < 8) ? char('0' + r() % 10) : al[r() % 15];
+    }
+    char buf[32] = {0};
+    memcpy(buf, f.data(), f.size());
+    uint32_t x[4];
+    memcpy(x, buf, 16);
+    for (int isf = 0; isf < 2; isf++) {
+      long long out = 0;
+      const int res = parpa::conv_window(x[0], x[1], x[2], x[3], (uint32_t)f.size(), isf != 0, out);
+      if (res == 2) continue;                      // deferred to the exact converters
+      char *e;
+      bool ok;
+      long long ref;
+      errno = 0;
+      if (isf) {
+        const double v = strtod(buf, &e);
+        ok = *e == 0 && f.find_first_of("eExXnNiI") == std::string::npos;
+        memcpy(&ref, &v, 8);
+      } else {
+        ref = strtoll(buf, &e, 10);
+        ok = *e == 0 && errno == 0;
+      }
+      if (res != 1 || !ok || ref != out) {
+        if (bad < 10) printf("BAD '%s' isf=%d res=%d ok=%d out=%lld ref=%lld\n", buf, isf, res, ok, out, ref);
+        bad++;
+      }
+      n++;
+    }
+  }
+  printf("checked %ld fast-path conversions, %ld mismatches\n", n, bad);
+  return bad != 0;
+}
