@@ -60,11 +60,11 @@ int dev_cfg(DevCfg **out) {
   DevCfg &c = g_dev[dev];
   if (!c.init) {
     CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
-    CK(cudaFuncSetAttribute(k_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, LUT_BYTES));
-    CK(cudaFuncSetAttribute(k_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, LUT_BYTES));
+    CK(cudaFuncSetAttribute(k_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PASS_SMEM));
+    CK(cudaFuncSetAttribute(k_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PASS_SMEM));
     CK(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass1, k_pass1, PASS_WARPS * 32, LUT_BYTES));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass2, k_pass2, PASS_WARPS * 32, LUT_BYTES));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass1, k_pass1, PASS_WARPS * 32, PASS_SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass2, k_pass2, PASS_WARPS * 32, PASS_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit, EMIT_WARPS * 32, EMIT_SMEM));
     if (getenv("PARPA_DEBUG")) {
       auto show = [](const char *n, const void *f) {
@@ -285,7 +285,7 @@ int launch_passes(int mode, const KArgs &a, const DfaK &k, cudaStream_t s, uint3
   const uint32_t nblk = (a.ntiles + SCAN_TILE - 1) / SCAN_TILE;
   {
     Launch L(s, "k_pass1");
-    k_pass1<<<grid_for(dc->occ_pass1, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, LUT_BYTES, s>>>(a, k);
+    k_pass1<<<grid_for(dc->occ_pass1, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, PASS_SMEM, s>>>(a, k);
   }
   CK(cudaGetLastError());
   {
@@ -297,7 +297,7 @@ int launch_passes(int mode, const KArgs &a, const DfaK &k, cudaStream_t s, uint3
   if (mode != MODE_TAU) {
     {
       Launch L(s, "k_pass2");
-      k_pass2<<<grid_for(dc->occ_pass2, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, LUT_BYTES, s>>>(a, k);
+      k_pass2<<<grid_for(dc->occ_pass2, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, PASS_SMEM, s>>>(a, k);
     }
     CK(cudaGetLastError());
     {

@@ -22,7 +22,8 @@
 
 namespace parpa {
 
-constexpr int PASS_WARPS = 16;                       // k_pass1 / k_pass2: 512 threads per CTA
+constexpr int PASS_WARPS = 32;                       // k_pass1 / k_pass2: one 1024-thread CTA per SM
+constexpr size_t PASS_SMEM = LUT_BYTES + PASS_WARPS * 2 * WT;   // LUT + two tile buffers per warp
 constexpr int SCAN_THREADS = 256, SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS; // warp tiles per scan block (4 MB of input)
 
@@ -30,19 +31,54 @@ __device__ __forceinline__ int chunk_valid(const KArgs &a, unsigned long long cs
   return cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
 }
 
+// ---- per-warp double-buffered tile staging (cp.async, no registers held across the wait) ----------
+// Each lane copies its own 64-byte chunk as four 16-byte units and reads back only those, so a lane's
+// own cp.async.wait_group orders everything it reads (no warp barrier needed).  Units are XOR-swizzled
+// so that the 128-bit reads of eight consecutive lanes hit distinct banks.
+__device__ __forceinline__ uint32_t pswz(int lane, int u) { return (uint32_t)lane * 4u + (uint32_t)(u ^ ((lane >> 1) & 3)); }
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void stage_chunk(const KArgs &a, uint4 *buf, uint32_t t, int lane) {
+  const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
+  const int nv = chunk_valid(a, cstart);
+#pragma unroll
+  for (int u = 0; u < 4; u++) {
+    const int nb = max(0, min(16, nv - 16 * u));                     // tail: zero-filled
+    cp_async16(buf + pswz(lane, u), nb ? (const void *)(a.in + cstart + 16 * u) : (const void *)a.in, (uint32_t)nb);
+  }
+}
+__device__ __forceinline__ void read_chunk(const uint4 *buf, int lane, uint32_t (&v)[16]) {
+#pragma unroll
+  for (int u = 0; u < 4; u++) {
+    const uint4 x = buf[pswz(lane, u)];
+    v[4 * u] = x.x; v[4 * u + 1] = x.y; v[4 * u + 2] = x.z; v[4 * u + 3] = x.w;
+  }
+}
+
 // ---- K1: pass 1 ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(PASS_WARPS * 32, 2) k_pass1(const KArgs a, const DfaK dfa) {
+__global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass1(const KArgs a, const DfaK dfa) {
   extern __shared__ __align__(16) uint8_t smem[];
   build_lut(smem, dfa);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint4 *bufs = reinterpret_cast<uint4 *>(smem + LUT_BYTES) + (size_t)warp * 2 * (WT / 16);
   const uint32_t laneoff = (uint32_t)(lane & 15) * 8u;
   const uint32_t nw = gridDim.x * PASS_WARPS;
-  for (uint32_t t = blockIdx.x * PASS_WARPS + warp; t < a.ntiles; t += nw) {
+  uint32_t t = blockIdx.x * PASS_WARPS + warp;
+  if (t < a.ntiles) stage_chunk(a, bufs, t, lane);
+  cp_async_commit();
+  for (uint32_t i = 0; t < a.ntiles; t += nw, i ^= 1u) {
+    if (t + nw < a.ntiles) stage_chunk(a, bufs + (i ^ 1u) * (WT / 16), t + nw, lane);
+    cp_async_commit();
+    cp_async_wait1();
     const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
     const int nv = chunk_valid(a, cstart);
     uint32_t v[16], t0, t1, qt[3];
-    load_chunk(a.in + cstart, nv, v);
+    read_chunk(bufs + i * (WT / 16), lane, v);
     if (nv == CHUNK) chunk_tau4<true>(smem, v, nv, laneoff, t0, t1, qt);
     else chunk_tau4<false>(smem, v, nv, laneoff, t0, t1, qt);
     uint32_t agg;
@@ -110,18 +146,25 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_tau_scan(const KArgs a) {
 }
 
 // ---- K3: pass 2 ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(PASS_WARPS * 32, 2) k_pass2(const KArgs a, const DfaK dfa) {
+__global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, const DfaK dfa) {
   extern __shared__ __align__(16) uint8_t smem[];
   build_lut(smem, dfa);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint4 *bufs = reinterpret_cast<uint4 *>(smem + LUT_BYTES) + (size_t)warp * 2 * (WT / 16);
   const uint32_t laneoff = (uint32_t)(lane & 15) * 8u;
   const uint32_t nw = gridDim.x * PASS_WARPS;
-  for (uint32_t t = blockIdx.x * PASS_WARPS + warp; t < a.ntiles; t += nw) {
+  uint32_t t = blockIdx.x * PASS_WARPS + warp;
+  if (t < a.ntiles) stage_chunk(a, bufs, t, lane);
+  cp_async_commit();
+  for (uint32_t i = 0; t < a.ntiles; t += nw, i ^= 1u) {
+    if (t + nw < a.ntiles) stage_chunk(a, bufs + (i ^ 1u) * (WT / 16), t + nw, lane);
+    cp_async_commit();
+    cp_async_wait1();
     const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
     const int nv = chunk_valid(a, cstart);
     uint32_t v[16];
-    load_chunk(a.in + cstart, nv, v);
+    read_chunk(bufs + i * (WT / 16), lane, v);
     const uint32_t entry = nib_at(a.lex[(unsigned long long)t * 32 + lane], a.wentry[t]);
     a.chunk_state[(unsigned long long)t * 32 + lane] = (uint8_t)entry;
     unsigned long long Dm, Fm, Rm;
