@@ -145,6 +145,60 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_tau_scan(const KArgs a) {
   }
 }
 
+// ---- the warp tile's SegT directly from the lanes' masks (ballots + warp reductions) ----------------
+// Same value as the ordered ∘-reduction of the 32 chunk summaries (segt_op over chunk_segt): record and
+// delimiter counts, the column after the last record delimiter, and the open field after
+// the last delimiter (first / last DATA byte, control bytes before / inside / after).
+__device__ __forceinline__ SegT warp_tile_segt(unsigned long long Dm, unsigned long long Fm, unsigned long long Rm,
+                                               unsigned long long Vm) {
+  const int lane = threadIdx.x & 31;
+  const unsigned FULL = 0xffffffffu;
+  const uint32_t nrec = __reduce_add_sync(FULL, (uint32_t)__popcll(Rm));
+  const uint32_t nd = __reduce_add_sync(FULL, (uint32_t)__popcll(Fm));
+  uint32_t fl = 0, col;
+  const unsigned rb = __ballot_sync(FULL, Rm != 0ull);
+  if (rb) {
+    const int L = 31 - __clz(rb);
+    const uint32_t mine = lane > L ? (uint32_t)__popcll(Fm)
+                          : lane == L ? (uint32_t)__popcll(Fm & above(msb64(Rm))) : 0u;
+    col = __reduce_add_sync(FULL, mine);
+    fl |= F_ABS;
+  } else {
+    col = nd;
+  }
+  unsigned long long open = Vm;
+  const unsigned fb = __ballot_sync(FULL, Fm != 0ull);
+  if (fb) {
+    fl |= F_HD;
+    const int Lf = 31 - __clz(fb);
+    open = lane > Lf ? Vm : lane == Lf ? (Vm & above(msb64(Fm))) : 0ull;
+  }
+  const unsigned long long Km = Vm & ~Dm & ~Fm;
+  const unsigned long long Do = Dm & open, Ko = Km & open;
+  const unsigned db = __ballot_sync(FULL, Do != 0ull);
+  uint32_t pos;
+  if (db) {
+    const int fl_lane = __ffs(db) - 1, ll_lane = 31 - __clz(db);
+    const int fdl = Do ? lsb64(Do) : 0, ldl = Do ? msb64(Do) : 0;
+    const int fdloc = __shfl_sync(FULL, fdl, fl_lane), ldloc = __shfl_sync(FULL, ldl, ll_lane);
+    const bool pre = (lane < fl_lane && Ko) || (lane == fl_lane && (Ko & below(fdloc)));
+    const bool pc = (lane > ll_lane && Ko) || (lane == ll_lane && (Ko & above(ldloc)));
+    unsigned long long in = 0ull;
+    if (lane > fl_lane && lane < ll_lane) in = Ko;
+    else if (lane == fl_lane && lane == ll_lane) in = Ko & above(fdloc) & below(ldloc);
+    else if (lane == fl_lane) in = Ko & above(fdloc);
+    else if (lane == ll_lane) in = Ko & below(ldloc);
+    if (__any_sync(FULL, pre)) fl |= F_PRE;
+    if (__any_sync(FULL, pc)) fl |= F_PC;
+    if (__any_sync(FULL, in != 0ull)) fl |= F_IC;
+    pos = (uint32_t)(fl_lane * CHUNK + fdloc) | ((uint32_t)(ll_lane * CHUNK + ldloc) << 16);
+  } else {
+    pos = 0xFFFFFFFFu;
+    if (__any_sync(FULL, Ko != 0ull)) fl |= F_PRE;
+  }
+  return SegT{nrec | (nd << 16), col | (fl << 16), pos};
+}
+
 // ---- K3: pass 2 ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, const DfaK dfa) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -180,12 +234,7 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, con
     mk[32] = Fm;
     mk[64] = Rm;
     const unsigned long long Vm = nv >= 64 ? ~0ull : ((1ull << nv) - 1ull);
-    SegT s = chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK);
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {                               // ordered warp reduction
-      SegT o = shfl_down_segt(s, d);
-      if (lane + d < 32) s = segt_op(s, o);
-    }
+    const SegT s = warp_tile_segt(Dm, Fm, Rm, Vm);
     if (lane == 0) a.wseg[t] = make_uint4(s.cnt, s.colf, s.pos, 0u);
   }
 }

@@ -4,7 +4,7 @@ from collections import Counter
 sass_csv, disasm, kern = sys.argv[1], sys.argv[2], sys.argv[3]
 lo, hi = float(sys.argv[4]), float(sys.argv[5])
 rows = list(csv.reader(open(sass_csv))); hdr = rows[1]
-data = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
+data = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr) and r[0] != 'Address']
 num = lambda x: float(x.replace(',', '')) if x.strip() else 0.0
 lines = {}; cur = None; infn = False
 for ln in open(disasm):

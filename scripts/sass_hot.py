@@ -5,7 +5,7 @@ from collections import Counter, defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = rows[1]
-data = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr)]
+data = [dict(zip(hdr, r)) for r in rows[2:] if len(r) == len(hdr) and r[0] != 'Address']
 
 
 def num(x):
