@@ -153,11 +153,11 @@ int parpa_plan_emit(parpa_plan *plan, const parpa_schema *schema, const parpa_co
                     parpa_stats *d_stats, void *stream);
 void parpa_plan_destroy(parpa_plan *plan);
 
-/* ---- single-pass parse into caller-owned columns (capacity path) ----------------------- *
- * parpa_parse_into — one fused kernel reads the input once: S1-S3 with a decoupled look-back
- * over tile transition vectors, S4-S5 with a second look-back over record/column offsets, then
- * S6-S7 straight into the caller's columns (capacity rows each), then finalize and deferred
- * conversion.  Rows >= capacity are not written; d_stats->status is then PARPA_ENEEDMORE and
+/* ---- parse into caller-owned columns without a host round trip (capacity path) ---------- *
+ * parpa_parse_into — enqueues the whole parse: pass 1 (S1-S2, warp ∘-scan), the single-pass
+ * decoupled look-back scan of warp-tile transition vectors (S3), pass 2 (S4, warp-tile record /
+ * column summaries), the look-back scan of those (S5), emission (S6-S7) straight into the
+ * caller's columns (capacity rows each), then finalize and deferred conversion (7 launches).  Rows >= capacity are not written; d_stats->status is then PARPA_ENEEDMORE and
  * d_stats->records the number required.  Asynchronous; d_stats is a device pointer (required).
  * gpu_launches (host, may be NULL) receives the number of kernels enqueued. */
 int parpa_parse_into(const parpa_dfa *dfa, const parpa_schema *schema, const uint8_t *d_bytes,
@@ -215,7 +215,7 @@ int parpa_parse_range(const parpa_dfa *dfa, const parpa_schema *schema, const ui
 int parpa_debug_trace(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len,
                       uint8_t *d_chunk_states, uint8_t *d_kinds, uint8_t *d_states, void *stream);
 uint32_t parpa_chunk_bytes(void);
-uint32_t parpa_tile_bytes(void);
+uint32_t parpa_tile_bytes(void);   /* bytes per warp tile (the unit of the scans and of emission) */
 
 /* ---- profiling hooks ----------------------------------------------------------------------- *
  * parpa_set_profiling(1) clears the history and starts recording a CUDA event pair around every

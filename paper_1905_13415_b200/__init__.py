@@ -221,7 +221,7 @@ def parse(dfa: Dfa, schema: Schema, data, stream=None) -> ParseResult:
 
 
 def parse_into(dfa: Dfa, schema: Schema, data, columns, capacity: int, stats_tensor, stream=None) -> int:
-    """Single-pass fused parse into caller columns (parpa_parse_into).  Asynchronous; returns the
+    """Parse into caller columns without a host round trip (parpa_parse_into).  Asynchronous; returns the
     number of kernels launched."""
     L = _lib.load()
     _check_input(data)

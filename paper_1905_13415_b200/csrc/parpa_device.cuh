@@ -28,8 +28,6 @@ namespace parpa {
 
 constexpr int CHUNK = 64;                  // bytes per thread ("chunk")
 constexpr int WT = CHUNK * 32;             // one warp tile = 2 KB (a lane per 64-byte chunk)
-constexpr int CW = 14;                     // compute warps per CTA (+2 look-back warps = 512 threads)
-constexpr int PTILE = CW * WT;             // bytes per look-back tile (28 KB)
 constexpr int LUT_BYTES = 256 * 256;       // 64 KB shared-memory LUT
 constexpr uint32_t NIB_IDENT = 0x76543210u;
 constexpr uint32_t INV_DEV = 0xFu;
@@ -223,11 +221,6 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -240,37 +233,7 @@ __device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
 }  // namespace parpa
 
 namespace parpa {
-// ---- mbarrier helpers (shared::cta) --------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {            // shared-window address
   return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
-      "r"(parity), "r"(1000000u)                            /* suspend up to 1 ms: sleep, don't poll */
-      : "memory");
-  // lanes can leave the suspend loop separately; without this the warp stays split into halves
-  // that execute the following stage twice (measured: 2x instructions at 16 threads/issue)
-  __syncwarp();
-}
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-// shift the tile-local positions of a summary by `off` bytes
-__device__ __forceinline__ SegT segt_shift(SegT s, uint32_t off) {
-  uint32_t fd = s.pos & 0xFFFFu, ld = s.pos >> 16;
-  if (fd != NONE16) fd += off;
-  if (ld != NONE16) ld += off;
-  s.pos = fd | (ld << 16);
-  return s;
 }
 }  // namespace parpa

@@ -1,24 +1,18 @@
-// parpa_kernels.cuh — the hot-path kernels of libparpa (sm_100a).
+// parpa_kernels.cuh — the hot-path kernels of libparpa (sm_100a) and their device building blocks.
 //
-//   k_scan<MODE>   persistent CTAs take 16 KB tiles in ticket order.  Per tile:
-//                  S1+S2  each thread classifies its 64-byte chunk through the shared-memory LUT and
-//                         builds its state-transition vector right-to-left with PRMT;
-//                  S3     warp-shuffle scan of the vectors with ∘ + decoupled look-back
-//                         over tile aggregates (single-pass scan after Merrill);
-//                  S4     re-simulation from the now known entry state -> DATA / DELIM / RECORD
-//                         masks (the paper's three bitmap indexes);
-//                  S5     record counts by POPCNT and the abs/rel column offset plus the
-//                         open-field carries, reduced (MODE_COUNT) or scanned (MODE_EMIT) over the
-//                         CTA and chained across tiles by a second decoupled look-back;
-//                  S6+S7  (MODE_EMIT) each thread walks its delimiters and writes every field's span
-//                         column-major, converting int64 / float64 fields in place.
-//   k_emit         S4-S7 for the two-phase path, from the per-chunk entry states and per-tile
-//                  prefixes that k_scan<MODE_COUNT> stored (input read a second time).
-//   k_finalize     end-of-input action, implicit last record, missing columns, status.
-//   k_deferred     device-tier conversion of typed fields the thread tier deferred: fields with
-//                  control bytes inside their span (re-simulated from the chunk entry state to
-//                  drop them) and floats outside the exact fast path (exact decimal algorithm).
-//   k_debug_trace  per-byte states / emission kinds from the per-chunk entry states (tests only).
+//   building blocks  LUT build, chunk load, S1+S2 τ of a chunk (chunk_tau4: four 16-byte chains),
+//                    S4 re-simulation masks (chunk_masks), warp ∘-scan of τ, look-back over τ
+//                    descriptors (lookback_tau), field emission helpers, conversion glue.
+//   k_pass1 .. k_seg_scan   the scan half (parpa_passes.cuh): S1-S5, chain-free passes + two
+//                    single-pass decoupled look-back scans over warp-tile aggregates.
+//   k_emit           S6+S7 per 2 KB warp tile from the stored chunk masks and tile prefixes: one lane
+//                    per field (E1), column-major coalesced writes with int64 / float64 conversion (E2)
+//                    (P:432-469).
+//   k_finalize       end-of-input action, implicit last record, missing columns, status.
+//   k_deferred       device-tier conversion of typed fields the thread tier deferred: fields with
+//                    control bytes inside their span (re-simulated from the chunk entry state to
+//                    drop them) and floats outside the exact fast path (exact decimal algorithm).
+//   k_debug_trace    per-byte states / emission kinds from the per-chunk entry states (tests only).
 #pragma once
 #include "parpa_convert.cuh"
 #include "parpa_device.cuh"
@@ -107,10 +101,6 @@ struct KArgs {
   Stats *stats;
   unsigned long long *prof;          // optional [gridDim][16] cycle counters (PARPA_DEBUG)
 };
-enum { P_TICKET, P_A, P_WAIT_TP, P_B, P_WAIT_SP, P_C, P_LBT_WAIT, P_LBT_WORK, P_LBS_WAIT, P_LBS_WORK, P_ITERS, P_NPROF };
-#define PROF_T0(x) unsigned long long x = a.prof ? clock64() : 0ull
-#define PROF_ADD(slot, t0) do { if (a.prof && (threadIdx.x & 31) == 0) { unsigned long long _n = clock64(); \
-  atomicAdd(a.prof + blockIdx.x * 16 + (slot), _n - (t0)); (t0) = _n; } } while (0)
 
 constexpr uint32_t FLAG_AGG = 1, FLAG_INCL = 2;
 
@@ -145,23 +135,6 @@ __device__ __forceinline__ void load_chunk(const uint8_t *p, int nvalid, uint32_
 }
 
 // ---- S1+S2: state-transition vector of a chunk (right to left: τ <- row(b_i) ∘ τ) -------------
-template <bool FULL>
-__device__ __forceinline__ void chunk_tau(const uint8_t *lut, const uint32_t (&v)[16], int nvalid,
-                                          uint32_t laneoff, uint32_t &t0, uint32_t &t1) {
-  t0 = 0x83828180u;
-  t1 = 0x87868584u;
-#pragma unroll
-  for (int i = CHUNK - 1; i >= 0; --i) {
-    if (!FULL && i >= nvalid) continue;
-    uint32_t addr = prmt(v[i >> 2], laneoff, 0x5504u | ((uint32_t)(i & 3) << 4));
-    uint2 e = *reinterpret_cast<const uint2 *>(lut + addr);
-    uint32_t n0 = prmt(t0, t1, e.x);
-    uint32_t n1 = prmt(t0, t1, e.y);
-    t0 = n0;
-    t1 = n1;
-  }
-}
-
 // ---- S4: re-simulation from the entry state -> DATA / DELIM / RECORD masks --------------------
 // multipliers that gather bit (4+k) of each byte into bits 32..35 of the 64-bit product
 __device__ __forceinline__ uint32_t gather4(uint32_t x, uint32_t bitmask, uint32_t mul) {
@@ -203,10 +176,8 @@ __device__ __forceinline__ uint32_t chunk_masks(const uint8_t *lut, const uint32
   return x & 0xFu;
 }
 
-// ---- 4-way ILP variants: the chunk is cut into four 16-byte quarters with independent chains ----
-// Pass 1 computes one τ per quarter (four independent PRMT chains) and composes them; pass 2 starts
-// each quarter from its own entry state, derived from the entry state and the quarter τ's, so its
-// four state chains are independent too.  qt[q] = nibble τ of quarter q (q = 0..2 needed later).
+// ---- 4-way ILP τ: the chunk is cut into four 16-byte quarters with independent PRMT chains, composed
+// at the end.  qt[q] = nibble τ of quarter q (q = 0..2).
 template <bool FULL>
 __device__ __forceinline__ void chunk_tau4(const uint8_t *lut, const uint32_t (&v)[16], int nvalid,
                                            uint32_t laneoff, uint32_t &t0, uint32_t &t1, uint32_t (&qt)[3]) {
@@ -237,52 +208,6 @@ __device__ __forceinline__ void chunk_tau4(const uint8_t *lut, const uint32_t (&
   uint32_t y = pack_nib(y0, y1);
   t0 = prmt(x0, x1, y);                                                               // (n0∘n1)∘(n2∘n3)
   t1 = prmt(x0, x1, y >> 16);
-}
-
-template <bool FULL>
-__device__ __forceinline__ uint32_t chunk_masks4(const uint8_t *lut, const uint32_t (&v)[16], int nvalid,
-                                                 uint32_t laneoff, uint32_t entry, const uint32_t (&qt)[3],
-                                                 unsigned long long &Dm, unsigned long long &Fm,
-                                                 unsigned long long &Rm) {
-  uint32_t x[4];
-  x[0] = 0x80u | entry;
-  x[1] = 0x80u | nib_at(qt[0], x[0] & 0xFu);
-  x[2] = 0x80u | nib_at(qt[1], x[1] & 0xFu);
-  x[3] = 0x80u | nib_at(qt[2], x[2] & 0xFu);
-  uint32_t d[2] = {0, 0}, f[2] = {0, 0}, r[2] = {0, 0};
-#pragma unroll
-  for (int ww = 0; ww < 4; ww++) {
-    uint32_t xs[4][4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const int w = 4 * q + ww, b = 4 * w + k;
-        if (FULL || b < nvalid) {
-          uint32_t addr = prmt(v[w], laneoff, 0x5504u | ((uint32_t)k << 4));
-          uint2 st = *reinterpret_cast<const uint2 *>(lut + addr + 128);
-          x[q] = prmt(st.x, st.y, x[q]);
-          xs[q][k] = x[q];
-        } else {
-          xs[q][k] = 0xFFu;
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const int w = 4 * q + ww;
-      uint32_t pk = prmt(prmt(xs[q][0], xs[q][1], 0x0040u), prmt(xs[q][2], xs[q][3], 0x0040u), 0x5410u);
-      uint32_t npk = ~pk;
-      const int h = w >> 3, sh = 4 * (w & 7);
-      d[h] |= gather4(npk, 0x10101010u, 0x10204080u) << sh;
-      f[h] |= gather4(npk, 0x20202020u, 0x08102040u) << sh;
-      r[h] |= gather4(npk, 0x40404040u, 0x04081020u) << sh;
-    }
-  }
-  Dm = (unsigned long long)d[0] | ((unsigned long long)d[1] << 32);
-  Fm = (unsigned long long)f[0] | ((unsigned long long)f[1] << 32);
-  Rm = (unsigned long long)r[0] | ((unsigned long long)r[1] << 32);
-  return x[3] & 0xFu;
 }
 
 // scalar re-walk (rare): position of the first byte whose transition enters INV
@@ -434,17 +359,6 @@ __device__ __forceinline__ void stcg_seg(Seg *p, const Seg &s) {
   __stcg(&p->ld, s.ld);
   __stcg(&p->col, s.col);
   __stcg(&p->flags, s.flags);
-}
-
-__device__ __forceinline__ uint4 ld_relaxed_v4(const uint4 *p) {
-  uint4 v;
-  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed_v4(uint4 *p, uint4 v) {
-  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w) : "memory");
 }
 
 // ---- S6+S7: field emission ---------------------------------------------------------------------

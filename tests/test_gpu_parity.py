@@ -48,8 +48,8 @@ def run_all_paths(dialect, data, types, defaults=None, strict=False, label=""):
     cap = max(ora.R, 1) + 3
     cols = parpa.alloc_columns(schema, cap)
     st = parpa.new_stats_tensor()
-    parpa.parse_into(dfa(dialect), schema, d, cols, cap, st)   # fused single pass
-    compare(parpa.ParseResult(cols, parpa.stats_from_tensor(st)), ora, types, label + "/fused")
+    parpa.parse_into(dfa(dialect), schema, d, cols, cap, st)   # parse_into: no host round trip
+    compare(parpa.ParseResult(cols, parpa.stats_from_tensor(st)), ora, types, label + "/into")
     res3 = parpa.parse_c_owned(dfa(dialect), schema, d)        # library-owned result
     compare(res3, ora, types, label + "/owned")
     return ora
