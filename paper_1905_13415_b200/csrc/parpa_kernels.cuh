@@ -648,8 +648,9 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   __syncwarp();
   // ---- E1b ----
   {
+    const uint32_t ktot = __shfl_sync(0xffffffffu, kinc, 31);  // CTRL bytes in the tile (warp-uniform)
     const uint32_t c0 = prefix.col;
-    uint32_t jcarry = 0;
+    uint32_t jcarry = 0, extra = 0;
     int lastrec = -1;
     const unsigned lt = (1u << lane) - 1u;
     for (uint32_t kb = 0; kb < nf; kb += 32) {
@@ -663,69 +664,73 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
       const unsigned before = recm & lt;
       const int lr = before ? (int)(kb + 31u - __clz(before)) : lastrec;
       const uint32_t c = lr >= 0 ? k - (uint32_t)lr - 1u : c0 + k;
+      extra += (uint32_t)__popc(__ballot_sync(0xffffffffu, act && c >= a.C));
       if (act) {
         const uint32_t x = k ? (ws->dlist[k - 1] & 0x7FFu) + 1u : 0u;   // field bytes [x, p)
         int fd = -1, ld = -1;
-        if (x < p) {
-          uint32_t w = x >> 5;
-          uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu << (x & 31u));
-          const uint32_t wp = p >> 5;
-          while (!bits && w < wp) bits = ws->dmask[++w];
-          if (bits) {
-            const uint32_t f = (w << 5) + (uint32_t)__ffs(bits) - 1u;
-            if (f < p) fd = (int)f;
-          }
-        }
-        if (fd >= 0) {
-          const uint32_t y = p - 1u;
-          uint32_t w = y >> 5;
-          uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu >> (31u - (y & 31u)));
-          while (!bits) bits = ws->dmask[--w];
-          ld = (int)((w << 5) + 31u - (uint32_t)__clz(bits));
-        }
-        uint32_t fl = 0;
-        if (ld > fd && kcount(ws, (uint32_t)ld) > kcount(ws, (uint32_t)fd + 1u)) fl |= F_IC;
-        unsigned long long cfd = fd >= 0 ? tbase_g + (unsigned)fd : NONE;
-        unsigned long long cld = fd >= 0 ? tbase_g + (unsigned)ld : NONE;
-        uint32_t cfl = fl;
-        const unsigned long long dpos = tbase_g + p;
-        if (k == 0) {                                         // may continue a field of an earlier tile
-          if (fd >= 0) {
-            if (kcount(ws, (uint32_t)fd) > 0u) fl |= F_PRE;
-            if (kcount(ws, p) > kcount(ws, (uint32_t)ld + 1u)) fl |= F_PC;
-          } else if (kcount(ws, p) > 0u) {
-            fl |= F_PRE;
-          }
-          unsigned long long sfd = cfd, sld = cld;
-          cfd = prefix.fd; cld = prefix.ld;
-          cfl = prefix.flags & (F_IC | F_PC | F_PRE);
-          open_combine(cfd, cld, cfl, sfd, sld, fl);
-        }
-        uint32_t e;
-        if (cfd == NONE) {
-          e = p;                                              // empty: offset = delimiter, length 0
+        uint32_t ic = 0;
+        if (ktot == 0u) {                                     // no CTRL byte: [x, p) is all DATA
+          if (x < p) { fd = (int)x; ld = (int)p - 1; }
         } else {
-          const unsigned long long L = cld + 1 - cfd;
-          const long long rel = (long long)cfd - (long long)tbase_g;
-          const uint32_t ic = (cfl & F_IC) ? 0x80000000u : 0u;
-          if (rel >= 0 && L <= (unsigned long long)WT) {
-            e = (uint32_t)rel | ((uint32_t)L << 11) | ic;
-          } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
-            emit_field(a, cols, prefix.recs + jr, c, cfd, cld, cfl, dpos, cnt);
-            e = FIELD_WRITTEN;
-            if (c >= a.C) cnt.extra--;                        // counted again below
-          } else {                                            // k == 0 only
-            ws->f0 = make_uint2((uint32_t)(int32_t)rel, (uint32_t)L | ic);
-            e = FIELD_FAR;
+          if (x < p) {
+            uint32_t w = x >> 5;
+            uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu << (x & 31u));
+            const uint32_t wp = p >> 5;
+            while (!bits && w < wp) bits = ws->dmask[++w];
+            if (bits) {
+              const uint32_t f = (w << 5) + (uint32_t)__ffs(bits) - 1u;
+              if (f < p) fd = (int)f;
+            }
+          }
+          if (fd >= 0) {
+            const uint32_t y = p - 1u;
+            uint32_t w = y >> 5;
+            uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu >> (31u - (y & 31u)));
+            while (!bits) bits = ws->dmask[--w];
+            ld = (int)((w << 5) + 31u - (uint32_t)__clz(bits));
+            if (ld > fd && kcount(ws, (uint32_t)ld) > kcount(ws, (uint32_t)fd + 1u)) ic = 0x80000000u;
+          }
+        }
+        uint32_t e = fd < 0 ? p : ((uint32_t)fd | ((uint32_t)(ld + 1 - fd) << 11) | ic);  // empty: (delim, 0)
+        if (k == 0) {                                         // may continue a field of an earlier tile
+          uint32_t fl = ic ? F_IC : 0u;
+          if (ktot) {
+            if (fd >= 0) {
+              if (kcount(ws, (uint32_t)fd) > 0u) fl |= F_PRE;
+              if (kcount(ws, p) > kcount(ws, (uint32_t)ld + 1u)) fl |= F_PC;
+            } else if (kcount(ws, p) > 0u) {
+              fl |= F_PRE;
+            }
+          }
+          unsigned long long cfd = prefix.fd, cld = prefix.ld;
+          uint32_t cfl = prefix.flags & (F_IC | F_PC | F_PRE);
+          open_combine(cfd, cld, cfl, fd >= 0 ? tbase_g + (unsigned)fd : NONE, fd >= 0 ? tbase_g + (unsigned)ld : NONE,
+                       fl);
+          if (cfd == NONE) {
+            e = p;
+          } else {
+            const unsigned long long L = cld + 1 - cfd;
+            const long long rel = (long long)cfd - (long long)tbase_g;
+            const uint32_t icf = (cfl & F_IC) ? 0x80000000u : 0u;
+            if (rel >= 0 && L <= (unsigned long long)WT) {
+              e = (uint32_t)rel | ((uint32_t)L << 11) | icf;
+            } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
+              emit_field(a, cols, prefix.recs + jr, c, cfd, cld, cfl, tbase_g + p, cnt);
+              e = FIELD_WRITTEN;
+              if (c >= a.C) cnt.extra--;                      // emit_field counted it already
+            } else {
+              ws->f0 = make_uint2((uint32_t)(int32_t)rel, (uint32_t)L | icf);
+              e = FIELD_FAR;
+            }
           }
         }
         ws->fields[k] = e;
-        if (c >= a.C) cnt.extra++;
         if (isrec) ws->rows[jr] = (k + 1u) | (p << 16);
       }
       jcarry += (uint32_t)__popc(recm);
       if (recm) lastrec = (int)(kb + 31u - __clz(recm));
     }
+    if (lane == 0) cnt.extra += extra;
   }
   __syncwarp();
   // ---- E2 ----
