@@ -16,6 +16,21 @@ namespace parpa {
 
 __constant__ double c_pow10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
                                    1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
+// RN(10^-k): the compiler rounds each decimal literal correctly
+__constant__ double c_rpow10[23] = {1e-0,  1e-1,  1e-2,  1e-3,  1e-4,  1e-5,  1e-6,  1e-7,  1e-8,  1e-9,  1e-10, 1e-11,
+                                    1e-12, 1e-13, 1e-14, 1e-15, 1e-16, 1e-17, 1e-18, 1e-19, 1e-20, 1e-21, 1e-22};
+
+// Correctly rounded m / 10^k for an exact double m (0 < m <= 2^53) and 1 <= k <= 22 with three FP64
+// operations instead of a full division: y = RN(1/b) (table), q = RN(m·y) is within an ulp of m/b, the
+// residual r = m - q·b is exact in one FMA, and RN(q + r·y) is then the correctly rounded quotient
+// (Markstein's theorem; no over/underflow is possible in this range).  Verified against libc strtod
+// by tests/test_convert_host.py.
+__device__ __forceinline__ double div_pow10(double m, uint32_t k) {
+  const double b = c_pow10[k], y = c_rpow10[k];
+  const double q = __dmul_rn(m, y);
+  const double r = __fma_rn(-q, b, m);
+  return __fma_rn(r, y, q);
+}
 
 // returns 1 valid, 0 invalid
 template <class Src>
@@ -172,7 +187,7 @@ __device__ __forceinline__ int conv_window(uint32_t x0, uint32_t x1, uint32_t x2
   if (m > (1ull << 53)) return 2;
   const uint32_t frac = ndots ? L - 1u - dotpos : 0u;
   double v = (double)m;
-  if (frac) v = __ddiv_rn(v, c_pow10[frac]);                       // Clinger: one correctly rounded op
+  if (frac) v = div_pow10(v, frac);                                // Clinger: one correctly rounded op
   if (neg) v = -v;
   out = __double_as_longlong(v);
   return 1;

@@ -17,6 +17,7 @@ static inline int __ffs(uint32_t x) { return __builtin_ffs(x); }
 static inline int __popc(uint32_t x) { return __builtin_popcount(x); }
 static inline double __ddiv_rn(double a, double b) { return a / b; }
 static inline double __dmul_rn(double a, double b) { return a * b; }
+static inline double __fma_rn(double a, double b, double c) { return __builtin_fma(a, b, c); }
 static inline long long __double_as_longlong(double d) { long long r; memcpy(&r, &d, 8); return r; }
 static inline double __longlong_as_double(long long x) { double r; memcpy(&r, &x, 8); return r; }
 static inline unsigned long long __umul64hi(unsigned long long a, unsigned long long b) {
@@ -69,6 +70,19 @@ int main(int argc, char **argv) {
       }
       n++;
     }
+  }
+  // div_pow10 against the correctly rounded quotient (strtod of "m e-k") over random m <= 2^53, k <= 22
+  for (long it = 0; it < iters; it++) {
+    const unsigned long long m = 1 + (r() % 4 == 0 ? r() % 100000 : r() % (1ull << 53));
+    const uint32_t k = 1 + (uint32_t)(r() % 22);
+    char buf[64];
+    snprintf(buf, sizeof buf, "%llue-%u", m, k);
+    const double ref = strtod(buf, nullptr), got = parpa::div_pow10((double)m, k);
+    if (memcmp(&ref, &got, 8) != 0) {
+      if (bad < 20) printf("BAD div_pow10 %s got %.17g ref %.17g\n", buf, got, ref);
+      bad++;
+    }
+    n++;
   }
   printf("checked %ld fast-path conversions, %ld mismatches\n", n, bad);
   return bad != 0;

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 def test_conv_window_matches_libc():
     with tempfile.TemporaryDirectory() as d:
         exe = os.path.join(d, "conv")
-        subprocess.run(["g++", "-O2", "-std=c++17", "-o", exe, os.path.join(HERE, "host", "conv_window_host.cpp")],
+        subprocess.run(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-o", exe, os.path.join(HERE, "host", "conv_window_host.cpp")],
                        check=True, capture_output=True)
         r = subprocess.run([exe, "1000000"], capture_output=True, text=True)
         assert r.returncode == 0, r.stdout + r.stderr
