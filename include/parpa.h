@@ -202,6 +202,27 @@ int parpa_count(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint
                 uint32_t entry_state, void *stream, parpa_counts *out, parpa_tau *tau_out);
 int parpa_compose_tau(const parpa_dfa *dfa, const parpa_tau *a, const parpa_tau *b, parpa_tau *out);
 int parpa_compose_counts(const parpa_counts *a, const parpa_counts *b, parpa_counts *out);
+/* ---- staged range plan: the same exchange with every pass run once per rank ------------- *
+ * parpa_range_begin  runs S1-S3 on the device range [d_bytes, d_bytes+len) at global offset
+ *                    `base` and returns the range's transition vector (host *tau_out) — the
+ *                    summary the first allgather exchanges.  The plan keeps the device state.
+ * parpa_range_count  runs S4-S5 from `entry_state` (the composition of the other ranks' vectors,
+ *                    P:361-364) and returns the range's counts (host *out; unseeded, base-relative
+ *                    positions are global) — the summary the second allgather exchanges.
+ * parpa_range_emit   writes the range's columns given ctx (entry_state as passed to
+ *                    parpa_range_count, prefix = ⊕ of the earlier ranks' counts), with the same
+ *                    left-context / is_last / capacity semantics as parpa_parse_range.
+ *                    Asynchronous; d_stats is a device pointer.
+ * Release with parpa_plan_destroy.  Errors: PARPA_EINVAL on a null argument, an entry state out of
+ * range or an emit whose entry state differs from the count's. */
+int parpa_range_begin(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint64_t base,
+                      void *stream, parpa_plan **plan, parpa_tau *tau_out);
+int parpa_range_count(parpa_plan *plan, uint32_t entry_state, parpa_counts *out);
+int parpa_range_emit(parpa_plan *plan, const parpa_schema *schema, const parpa_context *ctx,
+                     const uint8_t *left_context, uint64_t left_len, int is_last,
+                     const parpa_column *columns, uint64_t capacity, parpa_stats *d_stats,
+                     void *stream);
+
 int parpa_parse_range(const parpa_dfa *dfa, const parpa_schema *schema, const uint8_t *d_bytes,
                       uint64_t len, const parpa_context *ctx, const uint8_t *left_context,
                       uint64_t left_len, int is_last, const parpa_column *columns,

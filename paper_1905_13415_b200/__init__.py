@@ -382,6 +382,52 @@ def parse_range(dfa: Dfa, schema: Schema, data, entry_state: int, base: int, pre
                                ctypes.c_void_p(stats_tensor.data_ptr()), _stream_handle(stream)), "parpa_parse_range")
 
 
+class RangePlan:
+    """Staged parse of one byte range (the multi-GPU exchange with every pass run once):
+    ``begin`` -> the range's transition vector, ``count(entry_state)`` -> its counts,
+    ``emit(...)`` -> its columns (parpa_range_begin / _count / _emit)."""
+
+    def __init__(self, dfa: Dfa, data, base: int, stream=None):
+        L = _lib.load()
+        _check_input(data)
+        self._dfa, self._data, self._stream = dfa, data, stream
+        self.handle = ctypes.c_void_p()
+        t = _lib.Tau_t()
+        _check(L.parpa_range_begin(dfa.handle, ctypes.c_void_p(data.data_ptr()), data.numel(), int(base),
+                                   _stream_handle(stream), ctypes.byref(self.handle), ctypes.byref(t)),
+               "parpa_range_begin")
+        self.tau = list(t.tau[:dfa.num_states])
+        self.base = int(base)
+
+    def count(self, entry_state: int):
+        c = _lib.Counts_t()
+        _check(_lib.load().parpa_range_count(self.handle, int(entry_state), ctypes.byref(c)), "parpa_range_count")
+        self.entry_state = int(entry_state)
+        return c
+
+    def emit(self, schema: Schema, prefix, columns, capacity: int, stats_tensor, left=None, is_last=True):
+        L = _lib.load()
+        ctx = _lib.Context_t(self.entry_state, 0, self.base, prefix)
+        sch = schema.struct()
+        arr = _col_array(columns)
+        lptr = ctypes.c_void_p(left.data_ptr()) if left is not None and left.numel() else None
+        llen = left.numel() if left is not None else 0
+        _check(L.parpa_range_emit(self.handle, ctypes.byref(sch), ctypes.byref(ctx), lptr, llen, int(bool(is_last)),
+                                  arr, int(capacity), ctypes.c_void_p(stats_tensor.data_ptr()),
+                                  _stream_handle(self._stream)), "parpa_range_emit")
+
+    def close(self):
+        if getattr(self, "handle", None) and self.handle.value:
+            try:
+                _lib.load().parpa_plan_destroy(self.handle)
+            except Exception:
+                pass
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+
 def set_profiling(enable: bool):
     _lib.load().parpa_set_profiling(int(enable))
 

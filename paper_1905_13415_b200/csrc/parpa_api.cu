@@ -138,7 +138,7 @@ struct Work {
   uint32_t *bflag = nullptr;
   Ctrl *ctrl = nullptr;
   uint32_t *lex = nullptr, *wtau = nullptr, *tot_tau = nullptr;
-  uint8_t *wentry = nullptr;
+  uint32_t *wpre = nullptr;
   uint4 *wseg = nullptr;
   Seg *bagg = nullptr, *bincl = nullptr, *tot_seg = nullptr;
   TileInfo *tinfo = nullptr;
@@ -166,7 +166,7 @@ int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cu
   size_t zero = o;
   size_t o_lex = o; o = align_up(o + nt * 32 * 4);
   size_t o_wtau = o; o = align_up(o + nt * 4);
-  size_t o_went = o; o = align_up(o + nt);
+  size_t o_went = o; o = align_up(o + nt * 4);
   size_t o_wseg = o; o = align_up(o + nt * 16);
   size_t o_bagg = o; o = align_up(o + nb * sizeof(Seg));
   size_t o_binc = o; o = align_up(o + nb * sizeof(Seg));
@@ -184,7 +184,7 @@ int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cu
   w.ctrl = (Ctrl *)(b + o_ctrl);
   w.lex = (uint32_t *)(b + o_lex);
   w.wtau = (uint32_t *)(b + o_wtau);
-  w.wentry = b + o_went;
+  w.wpre = (uint32_t *)(b + o_went);
   w.wseg = (uint4 *)(b + o_wseg);
   w.bagg = (Seg *)(b + o_bagg);
   w.bincl = (Seg *)(b + o_binc);
@@ -224,7 +224,7 @@ void make_args(KArgs &a, const Work &w, const uint8_t *in, uint64_t len) {
   a.seed = seg_identity();
   a.lex = w.lex;
   a.wtau = w.wtau;
-  a.wentry = w.wentry;
+  a.wpre = w.wpre;
   a.wseg = w.wseg;
   a.tau_desc = w.tau_desc;
   a.bflag = w.bflag;
@@ -276,7 +276,9 @@ int grid_for(int occ, int sms, uint32_t ntiles, int warps_per_cta) {
   return (int)std::max<long long>(1, std::min<long long>(g, need));
 }
 
-// S1-S5: pass 1, τ scan (MODE_TAU stops here), pass 2, record/column scan.
+// S1-S3: pass 1 and the τ scan (unseeded); S4-S5: pass 2 (seeded by a.seed_dev) and the
+// record/column scan (unseeded; a.seed is applied by k_emit / k_finalize).
+int launch_half2(const KArgs &a, const DfaK &k, cudaStream_t s, uint32_t *launches);
 int launch_passes(int mode, const KArgs &a, const DfaK &k, cudaStream_t s, uint32_t *launches) {
   if (a.ntiles == 0) return PARPA_OK;
   DevCfg *dc;
@@ -293,21 +295,27 @@ int launch_passes(int mode, const KArgs &a, const DfaK &k, cudaStream_t s, uint3
     k_tau_scan<<<nblk, SCAN_THREADS, 0, s>>>(a);
   }
   CK(cudaGetLastError());
-  uint32_t n = 2;
-  if (mode != MODE_TAU) {
-    {
-      Launch L(s, "k_pass2");
-      k_pass2<<<grid_for(dc->occ_pass2, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, PASS_SMEM, s>>>(a, k);
-    }
-    CK(cudaGetLastError());
-    {
-      Launch L(s, "k_seg_scan");
-      k_seg_scan<<<nblk, SCAN_THREADS, 0, s>>>(a);
-    }
-    CK(cudaGetLastError());
-    n += 2;
+  if (launches) *launches += 2;
+  return mode == MODE_TAU ? PARPA_OK : launch_half2(a, k, s, launches);
+}
+
+int launch_half2(const KArgs &a, const DfaK &k, cudaStream_t s, uint32_t *launches) {
+  if (a.ntiles == 0) return PARPA_OK;
+  DevCfg *dc;
+  int rc = dev_cfg(&dc);
+  if (rc) return rc;
+  const uint32_t nblk = (a.ntiles + SCAN_TILE - 1) / SCAN_TILE;
+  {
+    Launch L(s, "k_pass2");
+    k_pass2<<<grid_for(dc->occ_pass2, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, PASS_SMEM, s>>>(a, k);
   }
-  if (launches) *launches += n;
+  CK(cudaGetLastError());
+  {
+    Launch L(s, "k_seg_scan");
+    k_seg_scan<<<nblk, SCAN_THREADS, 0, s>>>(a);
+  }
+  CK(cudaGetLastError());
+  if (launches) *launches += 2;
   return PARPA_OK;
 }
 
@@ -503,6 +511,7 @@ static int plan_totals(parpa_plan *p, Seg &tot, uint32_t &tau, uint64_t &first_i
     CK(cudaMemcpyAsync(&tau, p->w.tot_tau, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&ctrl, p->w.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    tot = seg_op(p->a.seed, tot);                      // the device total is unseeded
     first_inv = ctrl.inv_neg ? ~ctrl.inv_neg : NONE;
   } else {
     first_inv = NONE;
@@ -798,6 +807,73 @@ int parpa_compose_counts(const parpa_counts *a, const parpa_counts *b, parpa_cou
   Seg c = seg_op(counts_to_seg(*a), counts_to_seg(*b));
   *out = seg_to_counts(c, std::min(a->first_invalid, b->first_invalid));
   return PARPA_OK;
+}
+
+// ---- staged range plan (multi-GPU exchange with every pass run once) ------------------------------
+int parpa_range_begin(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint64_t base, void *stream,
+                      parpa_plan **out, parpa_tau *tau_out) {
+  if (!dfa || !out || !tau_out || (len && !d_bytes)) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  parpa_plan *p = new (std::nothrow) parpa_plan;
+  if (!p) return PARPA_ENOMEM;
+  p->dfa = dfa;
+  p->len = len;
+  p->s = s;
+  p->records = 0;
+  int rc = work_alloc(p->w, len, 1, len && misaligned(d_bytes), s);
+  if (rc) { delete p; return rc; }
+  const uint8_t *in = d_bytes;
+  if (!rc) rc = prepare_input(p->w, in, len, s);
+  p->in = in;
+  make_args(p->a, p->w, in, len);
+  p->a.base = base;
+  p->a.seed_dev = INV_DEV + 1;                            // not known yet: set by parpa_range_count
+  if (!rc) rc = launch_passes(MODE_TAU, p->a, dfa->k, s, nullptr);
+  uint32_t tau = NIB_IDENT;
+  if (!rc && p->w.ntiles && cudaMemcpyAsync(&tau, p->w.tot_tau, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    rc = PARPA_ECUDA;
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
+  if (rc) { work_free(p->w, s); delete p; return rc; }
+  host_tau_dfa(dfa, tau, tau_out);
+  *out = p;
+  return PARPA_OK;
+}
+
+int parpa_range_count(parpa_plan *p, uint32_t entry_state, parpa_counts *out) {
+  if (!p || !out || entry_state >= p->dfa->S) return PARPA_EINVAL;
+  p->a.seed_dev = p->dfa->dmap[entry_state];
+  int rc = launch_half2(p->a, p->dfa->k, p->s, nullptr);
+  if (rc) return rc;
+  Seg tot;
+  uint32_t tau;
+  uint64_t fi;
+  if ((rc = plan_totals(p, tot, tau, fi))) return rc;        // a.seed is the identity here
+  *out = seg_to_counts(tot, fi);
+  return PARPA_OK;
+}
+
+int parpa_range_emit(parpa_plan *p, const parpa_schema *sch, const parpa_context *ctx, const uint8_t *left,
+                     uint64_t left_len, int is_last, const parpa_column *cols, uint64_t cap, parpa_stats *d_stats,
+                     void *stream) {
+  if (!p || !sch || !ctx || !d_stats || (sch->num_columns && !cols)) return PARPA_EINVAL;
+  if (ctx->entry_state >= p->dfa->S || p->dfa->dmap[ctx->entry_state] != p->a.seed_dev) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  ColsK ck;
+  int rc = set_columns(sch, cols, sch->num_columns, ck);
+  if (rc) return rc;
+  KArgs a = p->a;
+  a.C = sch->num_columns;
+  a.strict = sch->strict;
+  a.cap = cap;
+  a.stats = (Stats *)d_stats;
+  a.seed = counts_to_seg(ctx->prefix);
+  a.row_base = a.seed.recs;
+  a.left = left;
+  a.left_len = left_len;
+  a.is_last = is_last;
+  rc = launch_emit(a, p->dfa->k, ck, s, nullptr);
+  if (!rc) rc = launch_tail(a, p->dfa->k, ck, s, nullptr);
+  return rc;
 }
 
 // ---- debug ----------------------------------------------------------------------------------------

@@ -85,13 +85,13 @@ struct KArgs {
   // ntiles = warp tiles (WT bytes each); nblk = scan blocks (SCAN_TILE warp tiles each)
   uint32_t *lex;                     // [ntiles * 32] lane-exclusive τ within its warp tile (nibble form)
   uint32_t *wtau;                    // [ntiles] warp-tile τ aggregate
-  uint8_t *wentry;                   // [ntiles] entry state of each warp tile (device numbering)
+  uint32_t *wpre;                    // [ntiles] τ of everything before the warp tile in this range (unseeded)
   uint4 *wseg;                       // [ntiles] warp-tile SegT aggregate {cnt, colf, pos, 0}
   unsigned long long *tau_desc;      // [nblk] decoupled look-back descriptors (flag << 32) | nibble τ
   uint32_t *bflag;                   // [nblk] Seg look-back flags
   Seg *bagg, *bincl;                 // [nblk] block aggregate / inclusive prefix (valid once flagged)
   uint32_t *tot_tau;                 // τ of the whole range (nibble form, seed not applied)
-  Seg *tot_seg;                      // seed ∘ Seg of the whole range
+  Seg *tot_seg;                      // Seg of the whole range (unseeded; the seed is applied on use)
   TileInfo *tinfo;                   // [ntiles]
   uint8_t *chunk_state;              // [ntiles * 32] device entry state of each chunk
   unsigned long long *masks;         // [ntiles][3][32] DATA / DELIM / RECORD masks of each chunk
@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 2) k_emit(const KArgs a, cons
     const unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;
     const unsigned long long Dm = mk[0], Fm = mk[32], Rm = mk[64];
     const unsigned long long Vm = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull);
-    emit_tile(a, s_cols, ws, a.tinfo[t].excl, Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
+    emit_tile(a, s_cols, ws, seg_op(a.seed, a.tinfo[t].excl), Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
   }
   flush_counters(a, cnt);
 }
@@ -833,7 +833,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 2) k_emit(const KArgs a, cons
 // ---- finalize ---------------------------------------------------------------------------------------
 __global__ void k_finalize(const KArgs a, const DfaK dfa, const ColsK colsk) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  Seg tot = a.ntiles ? *a.tot_seg : a.seed;
+  Seg tot = a.ntiles ? seg_op(a.seed, *a.tot_seg) : a.seed;
   uint32_t tau = a.ntiles ? *a.tot_tau : NIB_IDENT;
   uint32_t fin = nib_at(tau, a.seed_dev);
   EmitCounters cnt{0ull, 0ull, 0u};

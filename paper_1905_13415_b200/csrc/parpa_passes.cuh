@@ -6,15 +6,15 @@
 //               No inter-CTA dependency: persistent grid, high occupancy.
 //   k_tau_scan  S3b  single-pass scan of the warp-tile aggregates with decoupled look-back
 //               (Merrill & Garland, the paper's P:250 reference): blocks of SCAN_TILE aggregates in
-//               ticket order, block aggregate published before the look-back -> the entry state of
-//               every warp tile, P:361-364 seeded with the range's entry state.
+//               ticket order, block aggregate published before the look-back -> the τ of everything
+//               before every warp tile; k_pass2 applies the range's entry state to it.
 //   k_pass2     S4+S5a  per warp tile: lane entry = lex applied to the tile entry, re-simulation
 //               -> DATA / DELIM / RECORD masks (the paper's bitmap indexes), record
 //               count by POPCNT and the abs/rel column offset plus the open-field
 //               carries, reduced over the warp -> one SegT per warp tile.
 //   k_seg_scan  S5b  single-pass decoupled look-back scan of the warp-tile SegTs (⊕ of P:408-414,
-//               64-bit positions) -> the global prefix (records, fields, column, open field) of every
-//               warp tile, consumed by k_emit.
+//               64-bit positions) -> the prefix (records, fields, column, open field) of every warp
+//               tile within the range; k_emit / k_finalize compose it after the range's seed.
 //
 // Every kernel is bounded by its own DRAM stream or ALU work; nothing spins on another CTA except the
 // two small scans, whose look-backs cover SCAN_TILE warp tiles (4 MB of input) per block.
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_tau_scan(const KArgs a) {
   uint32_t cur = compose_nib(compose_nib(s_prefix, s_warp[warp]), wex);
 #pragma unroll
   for (int k = 0; k < SCAN_ITEMS; k++) {
-    if (t0 + k < a.ntiles) a.wentry[t0 + k] = (uint8_t)nib_at(cur, a.seed_dev);
+    if (t0 + k < a.ntiles) a.wpre[t0 + k] = cur;
     cur = compose_nib(cur, e[k]);
   }
 }
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, con
     const int nv = chunk_valid(a, cstart);
     uint32_t v[16];
     read_chunk(bufs + i * (WT / 16), lane, v);
-    const uint32_t entry = nib_at(a.lex[(unsigned long long)t * 32 + lane], a.wentry[t]);
+    const uint32_t entry = nib_at(a.lex[(unsigned long long)t * 32 + lane], nib_at(a.wpre[t], a.seed_dev));
     a.chunk_state[(unsigned long long)t * 32 + lane] = (uint8_t)entry;
     unsigned long long Dm, Fm, Rm;
     uint32_t fin;
@@ -255,7 +255,7 @@ __device__ __forceinline__ Seg wseg_at(const KArgs &a, unsigned long long t) {
   return segt_to_seg(SegT{w.x, w.y, w.z}, a.base + t * WT);
 }
 
-// returns seed ∘ B_0 ∘ ... ∘ B_{b-1} over the block aggregates; one descriptor per lane per round trip
+// returns B_0 ∘ ... ∘ B_{b-1} over the block aggregates; one descriptor per lane per round trip
 __device__ Seg lookback_bseg(const KArgs &a, uint32_t b) {
   const int lane = threadIdx.x & 31;
   Seg acc = seg_ident();
@@ -321,10 +321,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_seg_scan(const KArgs a) {
     const Seg bagg = shfl_seg(w, SCAN_THREADS / 32 - 1);
     Seg bex = shfl_up_seg(w, 1);
     if (lane < SCAN_THREADS / 32) s_warp[lane] = lane == 0 ? seg_ident() : bex;
-    Seg prefix = a.seed;
+    Seg prefix = seg_ident();                       // unseeded: k_emit / k_finalize apply a.seed
     if (b == 0) {
       if (lane == 0) {
-        stcg_seg(a.bincl, seg_op(a.seed, bagg));
+        stcg_seg(a.bincl, bagg);
         st_release_u32(a.bflag, FLAG_INCL);
       }
     } else {

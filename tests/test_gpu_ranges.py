@@ -26,20 +26,25 @@ def dev(a):
     return t[:len(a)]
 
 
-def sharded_parse(dialect, data, types, cuts, left_bytes=4096):
+def sharded_parse(dialect, data, types, cuts, left_bytes=4096, staged=False):
     """Parse every range as its own "rank" and assemble the global columns.  Columns stay sharded
     (SURVEY §8e): the record straddling cut g has its columns < col(g) on rank g-1 (local row
-    R_local) and the rest on rank g (local row 0)."""
+    R_local) and the rest on rank g (local row 0).  staged=True uses the range plan
+    (parpa_range_begin / _count / _emit: every pass once), else summarize / count / parse_range."""
     dfa = parpa.Dfa.dialect(dialect)
     schema = parpa.Schema(list(types))
     G = len(cuts) - 1
     taus, counts = [], []
+    plans = [parpa.RangePlan(dfa, dev(data[cuts[g]:cuts[g + 1]]), cuts[g]) for g in range(G)] if staged else None
     for g in range(G):
-        taus.append(parpa.summarize(dfa, dev(data[cuts[g]:cuts[g + 1]])))
+        taus.append(plans[g].tau if staged else parpa.summarize(dfa, dev(data[cuts[g]:cuts[g + 1]])))
     for g in range(G):
         e = pdist.entry_state(dfa, taus, g)
-        c, tau2 = parpa.count(dfa, dev(data[cuts[g]:cuts[g + 1]]), cuts[g], e)
-        assert tau2 == taus[g]
+        if staged:
+            c = plans[g].count(e)
+        else:
+            c, tau2 = parpa.count(dfa, dev(data[cuts[g]:cuts[g + 1]]), cuts[g], e)
+            assert tau2 == taus[g]
         counts.append(c)
     C = len(types)
     out = [[[] for _ in range(4)] for _ in range(C)]
@@ -53,7 +58,10 @@ def sharded_parse(dialect, data, types, cuts, left_bytes=4096):
         st = parpa.new_stats_tensor()
         left = dev(data[max(0, lo - left_bytes):lo]) if lo else None
         last = g == G - 1
-        parpa.parse_range(dfa, schema, dev(data[lo:hi]), e, lo, prefix, cols, cap, st, left=left, is_last=last)
+        if staged:
+            plans[g].emit(schema, prefix, cols, cap, st, left=left, is_last=last)
+        else:
+            parpa.parse_range(dfa, schema, dev(data[lo:hi]), e, lo, prefix, cols, cap, st, left=left, is_last=last)
         s = parpa.stats_from_tensor(st)
         assert s["status"] in (0, parpa.ECOLUMNS), s
         n = s["records"]
@@ -80,9 +88,10 @@ def sharded_parse(dialect, data, types, cuts, left_bytes=4096):
     return [tuple(np.concatenate(x[i]) if x[i] else None for i in range(4)) for x in out]
 
 
+@pytest.mark.parametrize("staged", [False, True])
 @pytest.mark.parametrize("name,G,seed", [("cfg1", 2, 0), ("cfg1", 5, 1), ("yelp", 3, 2), ("clf", 4, 3),
                                          ("taxi", 3, 4)])
-def test_virtual_ranks_equal_single_shot(name, G, seed):
+def test_virtual_ranks_equal_single_shot(name, G, seed, staged):
     w = datagen.WORKLOADS[name]
     data, _ = datagen.generate(name, 1_500_000)
     data = bytes(data)
@@ -91,7 +100,7 @@ def test_virtual_ranks_equal_single_shot(name, G, seed):
     inner = sorted(rng.sample(range(1, len(data) - 1), G - 1))
     # nudge one cut onto a delimiter and one just after, and keep 16-byte alignment of nothing in particular
     cuts = [0] + inner + [len(data)]
-    cols = sharded_parse(w.dialect, data, w.types, cuts)
+    cols = sharded_parse(w.dialect, data, w.types, cuts, staged=staged)
     for c, t in enumerate(w.types):
         off, ln, val, ok = cols[c]
         assert np.array_equal(off, ora.offset[c]), (name, c)
@@ -110,7 +119,7 @@ def test_cuts_at_delimiters_and_inside_quotes():
     for trial in range(6):
         picks = sorted(set(rng.sample(special, 3) + [rng.choice(special) + 1]))
         cuts = [0] + picks + [len(data)]
-        cols = sharded_parse("csv", data, types, cuts)
+        cols = sharded_parse("csv", data, types, cuts, staged=bool(trial & 1))
         for c in range(3):
             assert np.array_equal(cols[c][0], ora.offset[c])
             assert np.array_equal(cols[c][1], ora.length[c])
