@@ -250,7 +250,7 @@ def main():
         if world == 1:
             return parpa.parse_into(dfa, schema, d, cols, cap, st)
         pdist.parse_sharded(dfa, schema, d, base, cols, cap, st, left=left, is_last=is_last)
-        return 5
+        return 7                                  # range_begin 2 + range_count 2 + range_emit 3
 
     for _ in range(args.warmup):
         step()
