@@ -164,9 +164,15 @@ int parpa_parse_into(const parpa_dfa *dfa, const parpa_schema *schema, const uin
                      uint64_t len, const parpa_column *columns, uint64_t capacity,
                      parpa_stats *d_stats, void *stream, uint32_t *gpu_launches);
 
-/* ---- end-to-end from host memory ------------------------------------------------------- *
- * parpa_parse_host — h_bytes (host) -> device copy -> parse_into -> columns copied back into
- * the caller's host columns (capacity rows each) -> *stats (host).  Synchronous. */
+/* ---- end-to-end from host memory (streaming: the paper's §4.4) ---------------- *
+ * parpa_parse_host — h_bytes (host) -> device -> parse -> columns copied back into the caller's
+ * host columns (capacity rows each) -> *stats (host).  Synchronous.  Inputs longer than one
+ * partition (512 MB, or the byte count in the environment variable PARPA_STREAM_PARTITION) are
+ * streamed: partition i+1 is copied in while partition i is parsed and partition i-1's columns are
+ * copied out (three streams, double-buffered input), with the context carried between partitions
+ * by the staged range plan; results are identical to a single-shot parse.  Pinned host buffers
+ * give full PCIe overlap.  Errors as parpa_parse_into; PARPA_ENEEDMORE if capacity is short
+ * (stats->records = the number required, the first `capacity` rows are written). */
 int parpa_parse_host(const parpa_dfa *dfa, const parpa_schema *schema, const uint8_t *h_bytes,
                      uint64_t len, const parpa_column *h_columns, uint64_t capacity,
                      parpa_stats *stats, void *stream);

@@ -267,7 +267,10 @@ def parse_host(dfa: Dfa, schema: Schema, host_bytes, capacity: int, stream=None)
     """End to end from host memory (parpa_parse_host): returns (stats, numpy columns)."""
     import numpy as np
     L = _lib.load()
-    buf = np.ascontiguousarray(host_bytes, dtype=np.uint8).reshape(-1)
+    if isinstance(host_bytes, (bytes, bytearray, memoryview)):
+        buf = np.frombuffer(bytes(host_bytes), np.uint8)
+    else:
+        buf = np.ascontiguousarray(host_bytes, dtype=np.uint8).reshape(-1)
     cap = max(int(capacity), 1)
     cols_np = []
     arr = (_lib.Column_t * max(schema.C, 1))()

@@ -695,10 +695,172 @@ int parpa_parse_range(const parpa_dfa *dfa, const parpa_schema *sch, const uint8
 }
 
 // ---- end-to-end from host memory ---------------------------------------------------------------------
+// Streaming (the paper's §4.4): the input is cut into partitions of P bytes;
+// partition i+1 is copied host->device on one stream while partition i is parsed on the caller's
+// stream and partition i-1's columns are copied back on a third.  The context carry between
+// partitions is the staged range plan (τ -> entry state, counts -> ⊕-prefix); a record straddling a
+// cut has its first columns in partition i-1's last local row and the rest in partition i's row 0,
+// and each partition copies back only its own columns of those rows.  Each partition sees a 1 MB
+// left context (the "halo") for typed fields that straddle the cut.
+static uint64_t stream_partition_bytes() {
+  const char *e = getenv("PARPA_STREAM_PARTITION");
+  if (e) {
+    unsigned long long v = strtoull(e, nullptr, 10);
+    if (v >= 4096) return v;
+  }
+  return 512ull << 20;
+}
+
+static int parse_host_stream(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *h_bytes, uint64_t len,
+                             const parpa_column *h_cols, uint64_t cap, parpa_stats *stats, cudaStream_t s,
+                             uint64_t P) {
+  const uint32_t C = sch->num_columns;
+  const uint64_t HALO = 1ull << 20;
+  const uint64_t np = (len + P - 1) / P;
+  cudaStream_t sc = nullptr, sd = nullptr;
+  cudaEvent_t evH[2] = {nullptr, nullptr}, evC[2] = {nullptr, nullptr}, evA = nullptr;
+  uint8_t *inbuf[2] = {nullptr, nullptr};
+  Stats *d_pst = nullptr;
+  std::vector<Stats> pst(np);
+  int rc = PARPA_OK;
+  auto ck = [&](cudaError_t e) { if (e != cudaSuccess && rc == PARPA_OK) rc = cuda_status(e); return rc == PARPA_OK; };
+  ck(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
+  ck(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; b++) {
+    ck(cudaEventCreateWithFlags(&evH[b], cudaEventDisableTiming));
+    ck(cudaEventCreateWithFlags(&evC[b], cudaEventDisableTiming));
+    ck(cudaMallocAsync(&inbuf[b], HALO + P + 64, s));
+  }
+  ck(cudaEventCreateWithFlags(&evA, cudaEventDisableTiming));
+  ck(cudaMallocAsync(&d_pst, np * sizeof(Stats), s));
+  ck(cudaEventRecord(evA, s));                           // allocations visible to the copy streams
+  ck(cudaStreamWaitEvent(sc, evA, 0));
+  ck(cudaStreamWaitEvent(sd, evA, 0));
+  auto h2d = [&](uint64_t i) {
+    const uint64_t base = i * P, n = std::min(P, len - base), halo = std::min(HALO, base);
+    const int b = (int)(i & 1);
+    ck(cudaStreamWaitEvent(sc, evC[b], 0));             // partition i-2 is done with this buffer
+    ck(cudaMemcpyAsync(inbuf[b] + HALO - halo, h_bytes + base - halo, halo + n, cudaMemcpyHostToDevice, sc));
+    ck(cudaEventRecord(evH[b], sc));
+  };
+  Seg prefix = seg_identity();
+  uint32_t state = dfa->start;
+  uint64_t total_rows = 0;
+  if (rc == PARPA_OK) h2d(0);
+  for (uint64_t i = 0; i < np && rc == PARPA_OK; i++) {
+    const uint64_t base = i * P, n = std::min(P, len - base), halo = std::min(HALO, base);
+    const int b = (int)(i & 1);
+    const bool last = i + 1 == np;
+    if (!last) h2d(i + 1);                               // overlaps this partition's parse
+    if (!ck(cudaStreamWaitEvent(s, evH[b], 0))) break;
+    parpa_plan *p = nullptr;
+    parpa_tau tau;
+    if ((rc = parpa_range_begin(dfa, inbuf[b] + HALO, n, base, s, &p, &tau))) break;
+    parpa_counts cnt;
+    if ((rc = parpa_range_count(p, state, &cnt))) { parpa_plan_destroy(p); break; }
+    const uint32_t next_state = tau.tau[state];
+    const uint64_t nloc = cnt.records + ((last && dfa->eoi[next_state] == PARPA_EOI_RECORD) ? 1 : 0);
+    const Seg after = seg_op(prefix, counts_to_seg(cnt));
+    const uint64_t rows_alloc = nloc + 2;
+    std::vector<parpa_column> dcols(C);
+    void *blk = nullptr;
+    size_t tot = 0;
+    for (uint32_t c = 0; c < C; c++) {
+      const uint8_t type = sch->types ? sch->types[c] : PARPA_SPAN;
+      tot += align_up(rows_alloc * 8) + align_up(rows_alloc * 4) + (type != PARPA_SPAN ? align_up(rows_alloc * 8) + align_up(rows_alloc) : 0);
+    }
+    if (!ck(cudaMallocAsync(&blk, std::max<size_t>(tot, 256), s))) { parpa_plan_destroy(p); break; }
+    uint8_t *q = (uint8_t *)blk;
+    for (uint32_t c = 0; c < C; c++) {
+      const uint8_t type = sch->types ? sch->types[c] : PARPA_SPAN;
+      dcols[c].offset = (uint64_t *)q; q += align_up(rows_alloc * 8);
+      dcols[c].length = (uint32_t *)q; q += align_up(rows_alloc * 4);
+      if (type != PARPA_SPAN) {
+        dcols[c].value = q; q += align_up(rows_alloc * 8);
+        dcols[c].valid = q; q += align_up(rows_alloc);
+      } else {
+        dcols[c].value = nullptr;
+        dcols[c].valid = nullptr;
+      }
+    }
+    parpa_context ctx;
+    memset(&ctx, 0, sizeof(ctx));
+    ctx.entry_state = state;
+    ctx.base = base;
+    ctx.prefix = seg_to_counts(prefix, NONE);
+    rc = parpa_range_emit(p, sch, &ctx, halo ? inbuf[b] + HALO - halo : nullptr, halo, last ? 1 : 0, dcols.data(),
+                          rows_alloc, (parpa_stats *)(d_pst + i), s);
+    parpa_plan_destroy(p);
+    if (rc) { cudaFreeAsync(blk, s); break; }
+    ck(cudaEventRecord(evC[b], s));
+    ck(cudaStreamWaitEvent(sd, evC[b], 0));
+    // this partition's rows: local row 0 = global row prefix.recs; columns before the partition's
+    // start column belong to the previous partition, those after its end column to the next
+    const uint64_t row0 = prefix.recs;
+    for (uint32_t c = 0; c < C && rc == PARPA_OK; c++) {
+      const uint64_t lo = c < prefix.col ? 1 : 0;
+      const uint64_t hi = nloc + ((!last && c < after.col) ? 1 : 0);
+      const uint64_t glo = row0 + lo, ghi = std::min<uint64_t>(row0 + hi, cap);
+      if (glo >= ghi) continue;
+      const uint64_t m = ghi - glo;
+      if (h_cols[c].offset) ck(cudaMemcpyAsync(h_cols[c].offset + glo, dcols[c].offset + lo, m * 8, cudaMemcpyDeviceToHost, sd));
+      if (h_cols[c].length) ck(cudaMemcpyAsync(h_cols[c].length + glo, dcols[c].length + lo, m * 4, cudaMemcpyDeviceToHost, sd));
+      if (dcols[c].value && h_cols[c].value)
+        ck(cudaMemcpyAsync((uint8_t *)h_cols[c].value + glo * 8, (uint8_t *)dcols[c].value + lo * 8, m * 8, cudaMemcpyDeviceToHost, sd));
+      if (dcols[c].valid && h_cols[c].valid) ck(cudaMemcpyAsync(h_cols[c].valid + glo, dcols[c].valid + lo, m, cudaMemcpyDeviceToHost, sd));
+    }
+    ck(cudaMemcpyAsync(&pst[i], d_pst + i, sizeof(Stats), cudaMemcpyDeviceToHost, sd));
+    ck(cudaFreeAsync(blk, sd));
+    total_rows += nloc;
+    state = next_state;
+    prefix = after;
+  }
+  if (sd) cudaStreamSynchronize(sd);
+  if (sc) cudaStreamSynchronize(sc);
+  cudaStreamSynchronize(s);
+  if (rc == PARPA_OK) {                                   // combine the partitions' statistics
+    Stats t;
+    memset(&t, 0, sizeof(t));
+    t.first_invalid = NONE;
+    int st = ST_OK;
+    for (uint64_t i = 0; i < np; i++) {
+      t.fields += pst[i].fields;
+      t.missing_records += pst[i].missing_records;
+      t.extra_fields += pst[i].extra_fields;
+      t.deferred_fields += pst[i].deferred_fields;
+      t.first_invalid = std::min(t.first_invalid, pst[i].first_invalid);
+      const int ps = pst[i].status;
+      if (ps == ST_EFORMAT) st = ST_EFORMAT;
+      else if (ps == ST_EUNSUPPORTED && st != ST_EFORMAT) st = ST_EUNSUPPORTED;
+      else if (ps == ST_ECOLUMNS && st == ST_OK) st = ST_ECOLUMNS;
+    }
+    t.records = total_rows;
+    if (st == ST_OK || st == ST_ECOLUMNS) {
+      if (total_rows > cap) st = ST_ENEEDMORE;
+    }
+    t.status = st;
+    t.final_state = pst[np - 1].final_state;
+    memcpy(stats, &t, sizeof(t));
+  }
+  for (int b = 0; b < 2; b++) {
+    if (inbuf[b]) cudaFreeAsync(inbuf[b], s);
+    if (evH[b]) cudaEventDestroy(evH[b]);
+    if (evC[b]) cudaEventDestroy(evC[b]);
+  }
+  if (d_pst) cudaFreeAsync(d_pst, s);
+  if (evA) cudaEventDestroy(evA);
+  cudaStreamSynchronize(s);
+  if (sc) cudaStreamDestroy(sc);
+  if (sd) cudaStreamDestroy(sd);
+  return rc;
+}
+
 int parpa_parse_host(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *h_bytes, uint64_t len,
                      const parpa_column *h_cols, uint64_t cap, parpa_stats *stats, void *stream) {
   if (!dfa || !sch || !stats || (len && !h_bytes)) return PARPA_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t P = stream_partition_bytes();
+  if (len > P) return parse_host_stream(dfa, sch, h_bytes, len, h_cols, cap, stats, s, P);
   uint32_t C = sch->num_columns;
   std::vector<parpa_column> dcols(C);
   std::vector<size_t> per(C);

@@ -229,3 +229,43 @@ def test_parse_host_end_to_end():
         if t != oracle.SPAN:
             assert np.array_equal(cols[c][3], ora.valid[c])
             assert np.array_equal(cols[c][2].view(np.int64), ora.value[c])
+
+
+@pytest.mark.parametrize("name,part", [("cfg1", 65536), ("yelp", 300_000), ("clf", 131072), ("taxi", 200_000),
+                                       ("cfg1", 4096 + 17)])
+def test_parse_host_streaming_partitions(name, part, monkeypatch):
+    """parpa_parse_host in streaming mode: small partitions force many cuts inside
+    records, quoted fields and typed values; the assembled host columns must equal the oracle."""
+    monkeypatch.setenv("PARPA_STREAM_PARTITION", str(part))
+    w = datagen.WORKLOADS[name]
+    data, g = datagen.generate(name, 2_500_000)
+    ora = oracle.parse(w.dialect, data, w.C, list(w.types))
+    stats, cols = parpa.parse_host(dfa(w.dialect), parpa.Schema(list(w.types)), data, ora.R + 1)
+    assert stats["status"] == 0 and stats["records"] == ora.R == g.records, stats
+    assert stats["fields"] == ora.nfields and stats["missing_records"] == ora.n_missing
+    for c, t in enumerate(w.types):
+        assert np.array_equal(cols[c][0], ora.offset[c]), (name, c)
+        assert np.array_equal(cols[c][1], ora.length[c]), (name, c)
+        if t != oracle.SPAN:
+            assert np.array_equal(cols[c][3], ora.valid[c]), (name, c)
+            assert np.array_equal(cols[c][2].view(np.int64), ora.value[c]), (name, c)
+
+
+def test_parse_host_streaming_needmore_and_format_error(monkeypatch):
+    monkeypatch.setenv("PARPA_STREAM_PARTITION", "8192")
+    w = datagen.WORKLOADS["cfg1"]
+    data, g = datagen.generate("cfg1", 100_000)
+    stats, cols = parpa.parse_host(dfa("csv"), parpa.Schema(list(w.types)), data, g.records // 2)
+    assert stats["status"] == parpa.ENEEDMORE and stats["records"] == g.records
+    ora = oracle.parse("csv", data, w.C, list(w.types))
+    for c in range(w.C):
+        assert np.array_equal(cols[c][0], ora.offset[c][:g.records // 2])
+    wt = datagen.WORKLOADS["taxi"]
+    tdata, tg = datagen.generate("taxi", 100_000)
+    bad = bytearray(tdata)
+    pos = next(i for i in range(60_000, 70_000) if chr(bad[i - 1]).isdigit() and chr(bad[i]).isdigit())
+    bad[pos] = ord('"')                                        # quote inside an unquoted field -> INV
+    orab = oracle.parse("csv", bytes(bad), wt.C, list(wt.types))
+    stats, _ = parpa.parse_host(dfa("csv"), parpa.Schema(list(wt.types)), bytes(bad), tg.records + 1)
+    assert orab.status == oracle.EFORMAT
+    assert stats["status"] == parpa.EFORMAT and stats["first_invalid"] == orab.first_invalid
