@@ -35,7 +35,7 @@ DIALECTS = {"csv": CSV, "csv_comment": CSV_COMMENT, "clf": CLF}
 # emission kinds, EOI actions, column types, status codes (mirrors the paper's readings)
 DATA, CTRL, FIELD, RECORD = 0, 1, 2, 3
 EOI_NONE, EOI_RECORD, EOI_ERROR = 0, 1, 2
-SPAN, INT64, FLOAT64 = 0, 1, 2
+SPAN, INT64, FLOAT64, TIMESTAMP = 0, 1, 2, 3
 OK, EFORMAT, ECOLUMNS, EUNSUPPORTED = 0, -4, -5, -6
 NONE64 = 0xFFFFFFFFFFFFFFFF
 MISSING_LEN = 0xFFFFFFFF
@@ -70,6 +70,7 @@ def _load():
             lib.oracle_free.argtypes = [P]
             lib.oracle_conv_int64.argtypes = [u8p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int64)]
             lib.oracle_conv_float64.argtypes = [u8p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int64)]
+            lib.oracle_conv_timestamp.argtypes = [u8p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int64)]
             _lib = lib
     return _lib
 
@@ -201,6 +202,15 @@ def conv_int64(s: bytes):
     a = np.frombuffer(s + b"\0", np.uint8)
     v = ctypes.c_int64(0)
     ok = lib.oracle_conv_int64(_u8(a), len(s), ctypes.byref(v))
+    return bool(ok), v.value if ok else 0
+
+
+def conv_timestamp(s: bytes):
+    """R29: (ok, seconds since 1970-01-01T00:00:00Z) for ISO or CLF datetimes."""
+    lib = _load()
+    a = np.frombuffer(s + b"\0", np.uint8)
+    v = ctypes.c_int64(0)
+    ok = lib.oracle_conv_timestamp(_u8(a), len(s), ctypes.byref(v))
     return bool(ok), v.value if ok else 0
 
 

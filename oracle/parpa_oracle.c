@@ -41,7 +41,7 @@
 
 enum { K_DATA = 0, K_CTRL = 1, K_FIELD = 2, K_RECORD = 3 };
 enum { EOI_NONE = 0, EOI_RECORD = 1, EOI_ERROR = 2 };
-enum { T_SPAN = 0, T_INT64 = 1, T_FLOAT64 = 2 };
+enum { T_SPAN = 0, T_INT64 = 1, T_FLOAT64 = 2, T_TIMESTAMP = 3 };
 enum { ST_OK = 0, ST_EFORMAT = -4, ST_ECOLUMNS = -5, ST_EUNSUPPORTED = -6 };
 enum { D_CSV = 0, D_CSV_COMMENT = 1, D_CLF = 2, D_TABLES = 3 };
 #define NONE64 0xFFFFFFFFFFFFFFFFull
@@ -278,6 +278,72 @@ static int conv_float64(const uint8_t *s, uint64_t n, int64_t *bits) {
   return 1;
 }
 
+/* N2 / reading R29: timestamp = int64 seconds since 1970-01-01T00:00:00Z, proleptic Gregorian
+ * calendar, no leap seconds.  Accepted shapes, exact lengths only:
+ *   ISO  "YYYY-MM-DD HH:MM:SS" (19 bytes; 'T' also accepted between date and time), read as UTC
+ *        (the taxi and yelp datetime columns);
+ *   CLF  "DD/Mon/YYYY:HH:MM:SS +HHMM" (26 bytes; Mon = Jan..Dec), local time minus the offset
+ *        (the Common Log Format %t field).
+ * Month 1-12, day 1..days in that month, hour 0-23, minute 0-59, second 0-59, offset hours 0-23 and
+ * minutes 0-59; anything else is invalid (null).  Days from the civil date by the textbook
+ * era / year-of-era / day-of-year decomposition (400-year cycles of 146097 days). */
+static int64_t days_from_civil(int64_t y, int64_t m, int64_t d) {
+  y -= m <= 2;
+  const int64_t era = (y >= 0 ? y : y - 399) / 400;
+  const int64_t yoe = y - era * 400;
+  const int64_t doy = (153 * (m > 2 ? m - 3 : m + 9) + 2) / 5 + d - 1;
+  const int64_t doe = yoe * 365 + yoe / 4 - yoe / 100 + doy;
+  return era * 146097 + doe - 719468;
+}
+static int is_leap(int64_t y) { return (y % 4 == 0 && y % 100 != 0) || y % 400 == 0; }
+static int digits_at(const uint8_t *s, int n, int64_t *v) {
+  int64_t a = 0;
+  for (int i = 0; i < n; i++) {
+    if (s[i] < '0' || s[i] > '9') return 0;
+    a = a * 10 + (s[i] - '0');
+  }
+  *v = a;
+  return 1;
+}
+static int civil_seconds(int64_t Y, int64_t M, int64_t D, int64_t h, int64_t mi, int64_t sec, int64_t *out) {
+  static const int mdays[12] = {31, 28, 31, 30, 31, 30, 31, 31, 30, 31, 30, 31};
+  if (M < 1 || M > 12 || D < 1) return 0;
+  if (D > mdays[M - 1] + (M == 2 && is_leap(Y))) return 0;
+  if (h > 23 || mi > 59 || sec > 59) return 0;
+  *out = days_from_civil(Y, M, D) * 86400 + h * 3600 + mi * 60 + sec;
+  return 1;
+}
+static int conv_timestamp(const uint8_t *s, uint64_t n, int64_t *out) {
+  int64_t Y, M, D, h, mi, sec;
+  if (n == 19) {
+    if (s[4] != '-' || s[7] != '-' || (s[10] != ' ' && s[10] != 'T') || s[13] != ':' || s[16] != ':') return 0;
+    if (!digits_at(s, 4, &Y) || !digits_at(s + 5, 2, &M) || !digits_at(s + 8, 2, &D) || !digits_at(s + 11, 2, &h) ||
+        !digits_at(s + 14, 2, &mi) || !digits_at(s + 17, 2, &sec))
+      return 0;
+    return civil_seconds(Y, M, D, h, mi, sec, out);
+  }
+  if (n == 26) {
+    static const char *mon = "JanFebMarAprMayJunJulAugSepOctNovDec";
+    int64_t zh, zm;
+    if (s[2] != '/' || s[6] != '/' || s[11] != ':' || s[14] != ':' || s[17] != ':' || s[20] != ' ') return 0;
+    if (s[21] != '+' && s[21] != '-') return 0;
+    M = 0;
+    for (int k = 0; k < 12; k++)
+      if (memcmp(s + 3, mon + 3 * k, 3) == 0) M = k + 1;
+    if (!M) return 0;
+    if (!digits_at(s, 2, &D) || !digits_at(s + 7, 4, &Y) || !digits_at(s + 12, 2, &h) || !digits_at(s + 15, 2, &mi) ||
+        !digits_at(s + 18, 2, &sec) || !digits_at(s + 22, 2, &zh) || !digits_at(s + 24, 2, &zm))
+      return 0;
+    if (zh > 23 || zm > 59) return 0;
+    int64_t t;
+    if (!civil_seconds(Y, M, D, h, mi, sec, &t)) return 0;
+    const int64_t off = zh * 3600 + zm * 60;
+    *out = s[21] == '+' ? t - off : t + off;
+    return 1;
+  }
+  return 0;
+}
+
 static void close_field(or_result *r, uint32_t c, uint64_t pos, uint64_t first, uint64_t last) {
   r->nfields++;
   if (c >= r->C) { r->n_extra++; r->flen = 0; return; }
@@ -297,6 +363,8 @@ static void close_field(or_result *r, uint32_t c, uint64_t pos, uint64_t first, 
     ok = conv_int64(r->fbuf, r->flen, &v);
   } else if (r->types[c] == T_FLOAT64) {
     ok = conv_float64(r->fbuf, r->flen, &v);
+  } else if (r->types[c] == T_TIMESTAMP) {
+    ok = conv_timestamp(r->fbuf, r->flen, &v);
   }
   if (!ok) v = 0;
   r->val[c][row] = v;
@@ -450,3 +518,4 @@ void oracle_free(or_result *r) {
 /* Conversion routines exposed for the number pins (R14/R15). */
 int oracle_conv_int64(const uint8_t *s, uint64_t n, int64_t *out) { return conv_int64(s, n, out); }
 int oracle_conv_float64(const uint8_t *s, uint64_t n, int64_t *bits) { return conv_float64(s, n, bits); }
+int oracle_conv_timestamp(const uint8_t *s, uint64_t n, int64_t *out) { return conv_timestamp(s, n, out); }
