@@ -131,6 +131,24 @@ def gen_range(config, rank, world, pin=True, records=0):
     return data_host, left, block_len, c0, g0
 
 
+TS_COLS = {"taxi": (1, 2), "yelp": (8,), "clf": (3,), "cfg1": (), "taxi64": (1, 2)}
+TIMESTAMP = 3
+
+
+def workload(config, timestamps=False):
+    """The workload of a config; with --timestamps its datetime columns are typed TIMESTAMP
+    (int64 epoch seconds) instead of spans."""
+    import dataclasses
+    import datagen
+    w = datagen.WORKLOADS[config]
+    if not timestamps:
+        return w
+    t = list(w.types)
+    for c in TS_COLS[config]:
+        t[c] = TIMESTAMP
+    return dataclasses.replace(w, types=tuple(t))
+
+
 def run_reference(args):
     """--impl reference: the oracle (the sequential CPU parser) on bounded samples of the workload."""
     rank = int(os.environ.get("RANK", "0"))
@@ -139,7 +157,7 @@ def run_reference(args):
     import numpy as np
     import datagen
     import oracle
-    w = datagen.WORKLOADS[args.config]
+    w = workload(args.config, args.timestamps)
     sample = args.ref_sample_bytes
     data, g = datagen.generate(args.config, sample)
     times = []
@@ -155,7 +173,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.config, "description": CONFIG_LABEL[args.config],
+            "config": {"workload": args.config, "description": CONFIG_LABEL[args.config], "timestamps": bool(args.timestamps),
                        "sample_bytes": len(data), "records": g.records},
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "sample": f"first {len(data)} bytes ({g.records} records) of the {args.config} workload, "
@@ -164,12 +182,12 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(config, data_host, budget_s=10.0):
+def cpu_baseline(config, data_host, budget_s=10.0, timestamps=False):
     """The oracle as it stands, 1 host core, on a bounded prefix of this workload."""
     import numpy as np
     import datagen
     import oracle
-    w = datagen.WORKLOADS[config]
+    w = workload(config, timestamps)
     arr = data_host.numpy()
     probe = min(arr.size, 20_000_000)
     t0 = time.perf_counter()
@@ -196,6 +214,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--ref-sample-bytes", type=int, default=150_000_000)
     ap.add_argument("--records", type=int, default=0, help="override records per rank (profiling runs)")
+    ap.add_argument("--timestamps", action="store_true", help="type the datetime columns as TIMESTAMP (SURVEY N2)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -214,7 +233,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w = datagen.WORKLOADS[args.config]
+    w = workload(args.config, args.timestamps)
     dfa = parpa.Dfa.dialect(w.dialect)
     schema = parpa.Schema(list(w.types))
 
@@ -316,7 +335,7 @@ def main():
 
     cpu = None
     if rank == 0 and not args.no_cpu:
-        cpu = cpu_baseline(args.config, data_host)
+        cpu = cpu_baseline(args.config, data_host, timestamps=args.timestamps)
 
     e2e = None
     if rank == 0 and world == 1 and not args.no_e2e:
@@ -326,7 +345,7 @@ def main():
         line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-                "config": {"workload": args.config, "description": CONFIG_LABEL[args.config],
+                "config": {"workload": args.config, "description": CONFIG_LABEL[args.config], "timestamps": bool(args.timestamps),
                            "bytes_per_gpu": n, "records_per_gpu": R, "columns": w.C, "typed_columns": T,
                            "dialect": w.dialect, "path": "parse_into (k_pass1, k_tau_scan, k_pass2, k_seg_scan, k_emit, k_finalize, k_deferred)" if world == 1 else
                            "summarize + allgather + count + allgather + parse_range",

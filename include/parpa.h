@@ -51,7 +51,7 @@ enum { PARPA_DATA = 0, PARPA_CTRL = 1, PARPA_FIELD = 2, PARPA_RECORD = 3 };
 /* End-of-input action per final state (reading R6, "non-accepting end state"). */
 enum { PARPA_EOI_NONE = 0, PARPA_EOI_RECORD = 1, PARPA_EOI_ERROR = 2 };
 /* Column types: SPAN = raw field span only (strings, datetimes); INT64 / FLOAT64 converted. */
-enum { PARPA_SPAN = 0, PARPA_INT64 = 1, PARPA_FLOAT64 = 2 };
+enum { PARPA_SPAN = 0, PARPA_INT64 = 1, PARPA_FLOAT64 = 2, PARPA_TIMESTAMP = 3 };
 
 #define PARPA_MISSING_LENGTH 0xFFFFFFFFu   /* length of a missing field (record had fewer fields) */
 #define PARPA_NONE 0xFFFFFFFFFFFFFFFFull   /* "no position" */
@@ -81,7 +81,9 @@ int parpa_create_dfa(uint32_t num_states, uint32_t start_state, uint32_t invalid
 void parpa_destroy_dfa(parpa_dfa *dfa);
 
 /* ---- schema ------------------------------------------------------------------------------ *
- * C columns; types[c] in {PARPA_SPAN, PARPA_INT64, PARPA_FLOAT64}; has_default[c] / default_bits[c]
+ * C columns; types[c] in {PARPA_SPAN, PARPA_INT64, PARPA_FLOAT64, PARPA_TIMESTAMP}
+ * (PARPA_TIMESTAMP: int64 seconds since 1970-01-01T00:00:00Z of an ISO "YYYY-MM-DD HH:MM:SS" or
+ * Common-Log-Format "DD/Mon/YYYY:HH:MM:SS +HHMM" field; DESIGN reading R29); has_default[c] / default_bits[c]
  * give the column default for empty AND missing typed fields (reading R16: without a
  * default such fields are null, valid = 0).  default_bits holds the int64 value or the IEEE-754
  * bits of the double.  strict != 0 turns records with != C fields into PARPA_ECOLUMNS.

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 from . import _lib
 from . import dialects
 
-SPAN, INT64, FLOAT64 = 0, 1, 2
+SPAN, INT64, FLOAT64, TIMESTAMP = 0, 1, 2, 3
 DATA, CTRL, FIELD, RECORD = 0, 1, 2, 3
 OK, EINVAL, ENOMEM, ECUDA, EFORMAT, ECOLUMNS, EUNSUPPORTED, ENEEDMORE = 0, -1, -2, -3, -4, -5, -6, -7
 MISSING_LENGTH = 0xFFFFFFFF

@@ -62,10 +62,11 @@ int dev_cfg(DevCfg **out) {
     CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
     CK(cudaFuncSetAttribute(k_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PASS_SMEM));
     CK(cudaFuncSetAttribute(k_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PASS_SMEM));
-    CK(cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
+    CK(cudaFuncSetAttribute(k_emit<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
+    CK(cudaFuncSetAttribute(k_emit<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass1, k_pass1, PASS_WARPS * 32, PASS_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass2, k_pass2, PASS_WARPS * 32, PASS_SMEM));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit, EMIT_WARPS * 32, EMIT_SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit<false>, EMIT_WARPS * 32, EMIT_SMEM));
     if (getenv("PARPA_DEBUG")) {
       auto show = [](const char *n, const void *f) {
         cudaFuncAttributes fa;
@@ -77,7 +78,8 @@ int dev_cfg(DevCfg **out) {
       show("k_tau_scan", (const void *)k_tau_scan);
       show("k_pass2", (const void *)k_pass2);
       show("k_seg_scan", (const void *)k_seg_scan);
-      show("k_emit", (const void *)k_emit);
+      show("k_emit", (const void *)k_emit<false>);
+      show("k_emit<ts>", (const void *)k_emit<true>);
       fprintf(stderr, "[parpa] occ pass1=%d pass2=%d emit=%d sms=%d\n", c.occ_pass1, c.occ_pass2, c.occ_emit, c.sms);
     }
     cudaMemPool_t pool;
@@ -263,7 +265,7 @@ int set_columns(const parpa_schema *sch, const parpa_column *cols, uint32_t C, C
     d.type = sch->types ? sch->types[c] : PARPA_SPAN;
     d.has_def = sch->has_default ? sch->has_default[c] : 0;
     d.def_bits = sch->default_bits ? sch->default_bits[c] : 0;
-    if (d.type > PARPA_FLOAT64) return PARPA_EINVAL;
+    if (d.type > PARPA_TIMESTAMP) return PARPA_EINVAL;
     if (!d.off || !d.len) return PARPA_EINVAL;
     if (d.type != PARPA_SPAN && (!d.val || !d.valid)) return PARPA_EINVAL;
   }
@@ -319,6 +321,12 @@ int launch_half2(const KArgs &a, const DfaK &k, cudaStream_t s, uint32_t *launch
   return PARPA_OK;
 }
 
+bool has_timestamps(const KArgs &a, const ColsK &ck) {
+  for (uint32_t c = 0; c < a.C && c < (uint32_t)MAX_COLS; c++)
+    if (ck.c[c].type == T_TIMESTAMP) return true;
+  return false;
+}
+
 int launch_emit(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, uint32_t *launches) {
   if (a.ntiles == 0) return PARPA_OK;
   DevCfg *dc;
@@ -326,7 +334,10 @@ int launch_emit(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, 
   if (rc) return rc;
   {
     Launch L(s, "k_emit");
-    k_emit<<<grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s>>>(a, ck);
+    if (has_timestamps(a, ck))
+      k_emit<true><<<grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s>>>(a, ck);
+    else
+      k_emit<false><<<grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s>>>(a, ck);
   }
   CK(cudaGetLastError());
   if (launches) (*launches)++;
@@ -344,7 +355,8 @@ int launch_tail(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, 
   CK(cudaGetLastError());
   {
     Launch L(s, "k_deferred");
-    k_deferred<<<dc->sms * 2, 128, 0, s>>>(a, k, ck);
+    if (has_timestamps(a, ck)) k_deferred<true><<<dc->sms * 2, 128, 0, s>>>(a, k, ck);
+    else k_deferred<false><<<dc->sms * 2, 128, 0, s>>>(a, k, ck);
   }
   CK(cudaGetLastError());
   if (launches) *launches += 2;

@@ -193,6 +193,91 @@ __device__ __forceinline__ int conv_window(uint32_t x0, uint32_t x1, uint32_t x2
   return 1;
 }
 
+// ---- timestamps (reading R29) ----------------------------------------------------------
+// Seconds since 1970-01-01T00:00:00Z of an ISO "YYYY-MM-DD HH:MM:SS" ('T' also accepted) or CLF
+// "DD/Mon/YYYY:HH:MM:SS +HHMM" datetime (the zone offset is subtracted); proleptic Gregorian, no
+// leap seconds, exact lengths 19 / 26, fields range-checked, anything else invalid.  Day count:
+// 365 days per year plus the leap years before it (y/4 - y/100 + y/400, years shifted by one
+// 400-year cycle so that every quantity is positive), plus the days before the month from the
+// closed form (367 M - 362) / 12 minus 2 (1 in a leap year) after February, plus the day.
+__device__ __forceinline__ bool ts_leap(int y) { return (y % 4 == 0 && y % 100 != 0) || y % 400 == 0; }
+__host__ __device__ constexpr long long ts_days_shifted(int Y, int M, int D, bool leap) {
+  return 365LL * (Y + 400) + (Y + 399) / 4 - (Y + 399) / 100 + (Y + 399) / 400 + (367 * M - 362) / 12 -
+         (M <= 2 ? 0 : (leap ? 1 : 2)) + D - 1;
+}
+constexpr long long TS_EPOCH_DAYS = ts_days_shifted(1970, 1, 1, false);
+__device__ __forceinline__ int ts_dig(uint8_t c, int &bad) {
+  const int d = (int)c - '0';
+  bad |= (unsigned)d > 9u;
+  return d;
+}
+// x = the field's bytes packed little-endian (byte i = bits 8(i%4).. of x[i/4]); n = length.  Every
+// byte index below is a compile-time constant, so x stays in registers.
+#define TSB(i) ((uint8_t)(x[(i) >> 2] >> (8 * ((i) & 3))))
+__device__ __forceinline__ int conv_timestamp_words(const uint32_t (&x)[7], int n, long long &out) {
+  int bad = 0, Y, M, D, h, mi, sec, zoff = 0;
+  if (n == 19) {
+    bad |= TSB(4) != '-' || TSB(7) != '-' || (TSB(10) != ' ' && TSB(10) != 'T') || TSB(13) != ':' || TSB(16) != ':';
+    Y = ts_dig(TSB(0), bad) * 1000 + ts_dig(TSB(1), bad) * 100 + ts_dig(TSB(2), bad) * 10 + ts_dig(TSB(3), bad);
+    M = ts_dig(TSB(5), bad) * 10 + ts_dig(TSB(6), bad);
+    D = ts_dig(TSB(8), bad) * 10 + ts_dig(TSB(9), bad);
+    h = ts_dig(TSB(11), bad) * 10 + ts_dig(TSB(12), bad);
+    mi = ts_dig(TSB(14), bad) * 10 + ts_dig(TSB(15), bad);
+    sec = ts_dig(TSB(17), bad) * 10 + ts_dig(TSB(18), bad);
+  } else if (n == 26) {
+    bad |= TSB(2) != '/' || TSB(6) != '/' || TSB(11) != ':' || TSB(14) != ':' || TSB(17) != ':' || TSB(20) != ' ' ||
+           (TSB(21) != '+' && TSB(21) != '-');
+    const uint32_t key = (uint32_t)TSB(3) | ((uint32_t)TSB(4) << 8) | ((uint32_t)TSB(5) << 16);
+    switch (key) {
+      case 'J' | 'a' << 8 | 'n' << 16: M = 1; break;
+      case 'F' | 'e' << 8 | 'b' << 16: M = 2; break;
+      case 'M' | 'a' << 8 | 'r' << 16: M = 3; break;
+      case 'A' | 'p' << 8 | 'r' << 16: M = 4; break;
+      case 'M' | 'a' << 8 | 'y' << 16: M = 5; break;
+      case 'J' | 'u' << 8 | 'n' << 16: M = 6; break;
+      case 'J' | 'u' << 8 | 'l' << 16: M = 7; break;
+      case 'A' | 'u' << 8 | 'g' << 16: M = 8; break;
+      case 'S' | 'e' << 8 | 'p' << 16: M = 9; break;
+      case 'O' | 'c' << 8 | 't' << 16: M = 10; break;
+      case 'N' | 'o' << 8 | 'v' << 16: M = 11; break;
+      case 'D' | 'e' << 8 | 'c' << 16: M = 12; break;
+      default: M = 0; bad = 1;
+    }
+    D = ts_dig(TSB(0), bad) * 10 + ts_dig(TSB(1), bad);
+    Y = ts_dig(TSB(7), bad) * 1000 + ts_dig(TSB(8), bad) * 100 + ts_dig(TSB(9), bad) * 10 + ts_dig(TSB(10), bad);
+    h = ts_dig(TSB(12), bad) * 10 + ts_dig(TSB(13), bad);
+    mi = ts_dig(TSB(15), bad) * 10 + ts_dig(TSB(16), bad);
+    sec = ts_dig(TSB(18), bad) * 10 + ts_dig(TSB(19), bad);
+    const int zh = ts_dig(TSB(22), bad) * 10 + ts_dig(TSB(23), bad);
+    const int zm = ts_dig(TSB(24), bad) * 10 + ts_dig(TSB(25), bad);
+    bad |= zh > 23 || zm > 59;
+    zoff = (zh * 3600 + zm * 60) * (TSB(21) == '-' ? -1 : 1);
+  } else {
+    return 0;
+  }
+  if (bad || M < 1 || M > 12 || D < 1 || h > 23 || mi > 59 || sec > 59) return 0;
+  const bool leap = ts_leap(Y);
+  const int dim = M == 2 ? 28 + (leap ? 1 : 0) : 30 + ((M + (M >> 3)) & 1);
+  if (D > dim) return 0;
+  out = (ts_days_shifted(Y, M, D, leap) - TS_EPOCH_DAYS) * 86400LL + h * 3600 + mi * 60 + sec - zoff;
+  return 1;
+}
+#undef TSB
+// byte-source form (the rare paths: fields outside a register window, device tier)
+template <class Src>
+__device__ __noinline__ int conv_timestamp(Src &s, long long &out) {
+  uint32_t x[7] = {0, 0, 0, 0, 0, 0, 0};
+  int n = 0;
+  uint8_t c;
+#pragma unroll 1
+  while (s.next(c)) {
+    if (n >= 26) return 0;                                 // longer than any accepted shape
+    x[n >> 2] |= (uint32_t)c << (8 * (n & 3));
+    n++;
+  }
+  return conv_timestamp_words(x, n, out);
+}
+
 // ---- exact slow path ------------------------------------------------------------------------
 constexpr int DEC_MAX = 800;
 struct Decimal {

@@ -20,7 +20,20 @@
 namespace parpa {
 
 enum { MODE_TAU = 0, MODE_COUNT = 1, MODE_EMIT = 2 };
-enum { T_SPAN = 0, T_INT64 = 1, T_FLOAT64 = 2 };
+enum { T_SPAN = 0, T_INT64 = 1, T_FLOAT64 = 2, T_TIMESTAMP = 3 };
+// TS = the schema has timestamp columns: the emission kernels are instantiated with and without
+// them so that schemas without timestamps carry none of that code (registers, stack).
+template <bool TS, class Src>
+__device__ __forceinline__ int conv_typed(Src &s, uint32_t type, long long &v) {
+  if (TS && type == T_TIMESTAMP) return conv_timestamp(s, v);
+  return type == T_INT64 ? conv_int64(s, v) : conv_float64_fast(s, v);
+}
+// device tier: exact for every type
+template <bool TS, class Src>
+__device__ __forceinline__ int conv_typed_exact(Src &s, uint32_t type, long long &v) {
+  if (TS && type == T_TIMESTAMP) return conv_timestamp(s, v);
+  return type == T_INT64 ? conv_int64(s, v) : conv_float64_exact(s, v);
+}
 enum { EOI_NONE = 0, EOI_RECORD = 1, EOI_ERROR = 2 };
 enum { ST_OK = 0, ST_EFORMAT = -4, ST_ECOLUMNS = -5, ST_EUNSUPPORTED = -6, ST_ENEEDMORE = -7 };
 
@@ -393,6 +406,7 @@ __device__ __forceinline__ void push_defer(const KArgs &a, unsigned long long fd
   else atomicOr(&a.ctrl->defer_overflow, 1u);
 }
 
+template <bool TS>
 __device__ void emit_field(const KArgs &a, const ColDesc *cols, unsigned long long r, uint32_t c, unsigned long long fd,
                            unsigned long long ld, uint32_t fl, unsigned long long dpos, EmitCounters &cnt) {
   if (c >= a.C) { cnt.extra++; return; }
@@ -422,7 +436,7 @@ __device__ void emit_field(const KArgs &a, const ColDesc *cols, unsigned long lo
     return;
   } else {
     RawSrc src{&a, fd, ld, true};
-    int res = type == T_INT64 ? conv_int64(src, v) : conv_float64_fast(src, v);
+    int res = conv_typed<TS>(src, type, v);
     if (!src.ok) res = 2;                           // bytes outside this range: device tier
     if (res == 2) { push_defer(a, fd, ld, row, c, 0u); return; }
     ok = res;
@@ -464,6 +478,7 @@ __device__ __forceinline__ void open_combine(unsigned long long &fd, unsigned lo
   }
 }
 
+template <bool TS>
 __device__ void emit_chunk(const KArgs &a, const ColDesc *cols, const Seg &st, unsigned long long Dm, unsigned long long Fm,
                            unsigned long long Rm, unsigned long long Vm, unsigned long long cbase,
                            EmitCounters &cnt) {
@@ -484,7 +499,7 @@ __device__ void emit_chunk(const KArgs &a, const ColDesc *cols, const Seg &st, u
     unsigned long long sld = fd < 0 ? NONE : cbase + (unsigned)ld;
     if (prev >= 0) { cfd = sfd; cld = sld; cfl = fl; }
     else open_combine(cfd, cld, cfl, sfd, sld, fl);
-    emit_field(a, cols, r, c, cfd, cld, cfl, cbase + (unsigned)p, cnt);
+    emit_field<TS>(a, cols, r, c, cfd, cld, cfl, cbase + (unsigned)p, cnt);
     if ((Rm >> p) & 1ull) {
       fill_missing(a, cols, r, c + 1, cbase + (unsigned)p, cnt);
       r++;
@@ -544,6 +559,7 @@ struct TileSrc {                       // raw field bytes: shared-memory tile co
   }
 };
 
+template <bool TS>
 __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, uint32_t c, unsigned long long row,
                                             unsigned long long fd, unsigned long long ld, bool ic, bool empty,
                                             const uint8_t *tb, unsigned long long tbase) {
@@ -557,16 +573,35 @@ __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, u
   } else {
     int res = 2;
     const unsigned long long L = ld + 1 - fd;
-    if (fd >= tbase && L <= 16) {                       // field inside the tile copy: register window
-      const uint32_t o = (uint32_t)(fd - tbase), i0 = o >> 2, sh = (o & 3u) * 8u;
-      const uint32_t *w = reinterpret_cast<const uint32_t *>(tb) + i0;
+    // the field's first bytes as a register window: from the tile copy in shared memory, or — for
+    // the field that began in an earlier tile — from global memory with independent 4-byte loads
+    const uint32_t *w = nullptr;
+    uint32_t sh = 0;
+    const bool is_ts = TS && cd->type == T_TIMESTAMP;
+    if (L <= (is_ts ? 26ull : 16ull)) {
+      if (fd >= tbase) {
+        const uint32_t o = (uint32_t)(fd - tbase);
+        w = reinterpret_cast<const uint32_t *>(tb) + (o >> 2);
+        sh = (o & 3u) * 8u;
+      } else if (fd >= a.base && fd - a.base + 32 <= a.len) {
+        const unsigned long long o = fd - a.base;
+        w = reinterpret_cast<const uint32_t *>(a.in + (o & ~3ull));
+        sh = (uint32_t)(o & 3ull) * 8u;
+      }
+    }
+    if (w && is_ts) {
+      uint32_t x[7] = {0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int k = 0; k < 7; k++) x[k] = __funnelshift_r(w[k], w[k + 1], sh);
+      res = conv_timestamp_words(x, (int)L, v);
+    } else if (w) {
       const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
       res = conv_window(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
                         __funnelshift_r(w3, w4, sh), (uint32_t)L, cd->type == T_FLOAT64, v);
     }
     if (res == 2) {
       TileSrc src{&a, tb, tbase, fd, ld, true};
-      res = cd->type == T_INT64 ? conv_int64(src, v) : conv_float64_fast(src, v);
+      res = conv_typed<TS>(src, cd->type, v);
       if (!src.ok) res = 2;
     }
     if (res == 2) { push_defer(a, fd, ld, row, c, 0u); return; }
@@ -604,6 +639,7 @@ __device__ __forceinline__ int tile_item(const KArgs &a, const WarpScratch *ws, 
 __device__ __forceinline__ uint32_t kcount(const WarpScratch *ws, uint32_t x) {   // CTRL bytes before x
   return ws->kpre[x >> 5] + __popc(ws->kmask[x >> 5] & ((1u << (x & 31u)) - 1u));
 }
+template <bool TS>
 __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, const Seg &prefix,
                           unsigned long long Dm, unsigned long long Fm, unsigned long long Rm,
                           unsigned long long Vm, unsigned long long tbase_g, unsigned long long cbase,
@@ -624,7 +660,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   if (nf > (uint32_t)FCAP || nrec >= (uint32_t)RCAP) {       // warp-uniform: dense tile, direct path
     SegT sagg;
     const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
-    emit_chunk(a, cols, seg_op(prefix, segt_to_seg(sex, tbase_g)), Dm, Fm, Rm, Vm, cbase, cnt);
+    emit_chunk<TS>(a, cols, seg_op(prefix, segt_to_seg(sex, tbase_g)), Dm, Fm, Rm, Vm, cbase, cnt);
     return;
   }
   // ---- E1a ----
@@ -715,7 +751,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
             if (rel >= 0 && L <= (unsigned long long)WT) {
               e = (uint32_t)rel | ((uint32_t)L << 11) | icf;
             } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
-              emit_field(a, cols, prefix.recs + jr, c, cfd, cld, cfl, tbase_g + p, cnt);
+              emit_field<TS>(a, cols, prefix.recs + jr, c, cfd, cld, cfl, tbase_g + p, cnt);
               e = FIELD_WRITTEN;
               if (c >= a.C) cnt.extra--;                      // emit_field counted it already
             } else {
@@ -780,7 +816,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
       }
       __stcs(cd->off + row, off);
       __stcs(cd->len + row, len);
-      if (cd->type != T_SPAN) write_value(a, cd, ci, row, off, off + len - 1, ic, len == 0, tb, tbase_g);
+      if (cd->type != T_SPAN) write_value<TS>(a, cd, ci, row, off, off + len - 1, ic, len == 0, tb, tbase_g);
     } else if (ji < nrec) {                                 // record closed with fewer fields
       if (k == end) cnt.missing++;
       __stcs(cd->off + row, tbase_g + (ws->rows[ji] >> 16));
@@ -804,6 +840,7 @@ constexpr size_t EMIT_SMEM = EMIT_WARPS * sizeof(WarpScratch);
 
 // S6+S7 per warp tile from what the scan half stored: the DATA / DELIM / RECORD masks of every chunk
 // (k_pass2) and the tile prefix (k_seg_scan).  No LUT, no re-simulation: 2 CTAs per SM.
+template <bool TS>
 __global__ void __launch_bounds__(EMIT_WARPS * 32, 2) k_emit(const KArgs a, const ColsK colsk) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ ColDesc s_cols[MAX_COLS];
@@ -825,7 +862,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 2) k_emit(const KArgs a, cons
     const unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;
     const unsigned long long Dm = mk[0], Fm = mk[32], Rm = mk[64];
     const unsigned long long Vm = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull);
-    emit_tile(a, s_cols, ws, seg_op(a.seed, a.tinfo[t].excl), Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
+    emit_tile<TS>(a, s_cols, ws, seg_op(a.seed, a.tinfo[t].excl), Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
   }
   flush_counters(a, cnt);
 }
@@ -843,7 +880,7 @@ __global__ void k_finalize(const KArgs a, const DfaK dfa, const ColsK colsk) {
     uint32_t act = dfa.eoi[fin];
     unsigned long long end = a.base + a.len;
     if (act == EOI_RECORD) {                               // implicit record delimiter at EOI
-      emit_field(a, colsk.c, R, tot.col, tot.fd, tot.ld, tot.flags & (F_IC | F_PC | F_PRE), end, cnt);
+      emit_field<true>(a, colsk.c, R, tot.col, tot.fd, tot.ld, tot.flags & (F_IC | F_PC | F_PRE), end, cnt);
       fill_missing(a, colsk.c, R, tot.col + 1, end, cnt);
       R++;
       nf++;
@@ -891,6 +928,7 @@ struct DfaDataSrc {                   // DATA bytes of [fd, ld], re-simulated fr
   }
 };
 
+template <bool TS>
 __global__ void k_deferred(const KArgs a, const DfaK dfa, const ColsK colsk) {
   unsigned int n = min(a.ctrl->n_defer, a.dq_cap);
   for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -910,11 +948,11 @@ __global__ void k_deferred(const KArgs a, const DfaK dfa, const ColsK colsk) {
           x = prmt(dfa.lut[b][2], dfa.lut[b][3], x);
         }
         DfaDataSrc src{&a, &dfa, it.fd, it.ld, x, true};
-        ok = cd->type == T_INT64 ? conv_int64(src, v) : conv_float64_exact(src, v);
+        ok = conv_typed_exact<TS>(src, cd->type, v);
       }
     } else {
       RawSrc src{&a, it.fd, it.ld, true};
-      ok = cd->type == T_INT64 ? conv_int64(src, v) : conv_float64_exact(src, v);
+      ok = conv_typed_exact<TS>(src, cd->type, v);
       if (!src.ok) { ok = 0; atomicOr(&a.ctrl->unsupported, 1u); }
     }
     if (ok != 1) { ok = 0; v = 0; }

@@ -269,3 +269,30 @@ def test_parse_host_streaming_needmore_and_format_error(monkeypatch):
     stats, _ = parpa.parse_host(dfa("csv"), parpa.Schema(list(wt.types)), bytes(bad), tg.records + 1)
     assert orab.status == oracle.EFORMAT
     assert stats["status"] == parpa.EFORMAT and stats["first_invalid"] == orab.first_invalid
+
+
+TS_COLS = {"taxi": [1, 2], "yelp": [8], "clf": [3]}
+
+
+@pytest.mark.parametrize("name", ["taxi", "yelp", "clf"])
+def test_timestamp_columns(name):
+    """the workloads' datetime columns parsed as TIMESTAMP (int64 epoch seconds)."""
+    w = datagen.WORKLOADS[name]
+    types = list(w.types)
+    for c in TS_COLS[name]:
+        types[c] = oracle.TIMESTAMP
+    data, g = datagen.generate(name, 1_500_000)
+    ora = run_all_paths(w.dialect, data, types, label=name + "/ts")
+    assert ora.R == g.records
+    for c in TS_COLS[name]:
+        assert ora.valid[c].mean() > 0.95, (name, c)                 # the generator writes valid datetimes
+
+
+def test_timestamp_edge_cases():
+    rows = [b"1970-01-01 00:00:00", b"2000-02-29 23:59:59", b"1900-02-29 00:00:00", b"2019-04-31 10:00:00",
+            b"2038-01-19T03:14:08", b"0001-01-01 00:00:00", b"9999-12-31 23:59:59", b"2019-1-01 00:00:00",
+            b"", b"x", b"2019-01-01 00:00:00.5", b'"2019-01-01 00:00:00"', b'"2019-01-01 ""00:00:00"']
+    data = b"".join(b"%d,%s\n" % (i, r) for i, r in enumerate(rows)) * 50
+    types = [oracle.INT64, oracle.TIMESTAMP]
+    run_all_paths("csv", data, types, label="ts-edge")
+    run_all_paths("csv", data, types, defaults=[None, 12345], label="ts-edge-default")
