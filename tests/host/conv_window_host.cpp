@@ -12,6 +12,7 @@
 #define __device__
 #define __host__
 #define __forceinline__ inline
+#define __noinline__
 #define __constant__
 static inline int __ffs(uint32_t x) { return __builtin_ffs(x); }
 static inline int __popc(uint32_t x) { return __builtin_popcount(x); }
