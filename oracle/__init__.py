@@ -71,6 +71,11 @@ def _load():
             lib.oracle_conv_int64.argtypes = [u8p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int64)]
             lib.oracle_conv_float64.argtypes = [u8p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int64)]
             lib.oracle_conv_timestamp.argtypes = [u8p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_int64)]
+            lib.oracle_parse_strings.argtypes = [ctypes.c_int, u8p, ctypes.c_uint64, ctypes.c_uint32, u8p, ctypes.c_uint32]
+            lib.oracle_parse_strings.restype = ctypes.c_void_p
+            lib.oracle_strings_size.argtypes = [ctypes.c_void_p]
+            lib.oracle_strings_size.restype = ctypes.c_uint64
+            lib.oracle_strings.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
             _lib = lib
     return _lib
 
@@ -203,6 +208,27 @@ def conv_int64(s: bytes):
     v = ctypes.c_int64(0)
     ok = lib.oracle_conv_int64(_u8(a), len(s), ctypes.byref(v))
     return bool(ok), v.value if ok else 0
+
+
+def strings(dialect, data, C: int, col: int, types=None):
+    """SURVEY N3 (the paper's CSS): the DATA bytes of every field of column ``col``
+    concatenated in row order (control bytes dropped; missing fields empty).  Returns
+    (offsets int64[R + 1], data bytes)."""
+    lib = _load()
+    d = _as_bytes(data)
+    dialect = DIALECTS[dialect] if isinstance(dialect, str) else int(dialect)
+    t, _, _, _ = _schema_arrays(C, types, None)
+    dd = d if len(d) else np.zeros(1, np.uint8)
+    h = lib.oracle_parse_strings(dialect, _u8(dd), len(d), C, _u8(t), col)
+    st = (ctypes.c_uint64 * 8)()
+    lib.oracle_stats(h, st)
+    R = int(st[0])
+    n = int(lib.oracle_strings_size(h))
+    offs = np.zeros(R + 1, np.int64)
+    buf = np.zeros(max(n, 1), np.uint8)
+    lib.oracle_strings(h, offs.ctypes.data, buf.ctypes.data)
+    lib.oracle_free(h)
+    return offs, bytes(buf[:n])
 
 
 def conv_timestamp(s: bytes):

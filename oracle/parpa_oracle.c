@@ -206,7 +206,28 @@ typedef struct {
   /* open field's DATA bytes */
   uint8_t *fbuf;
   uint64_t fcap, flen;
+  /* string capture (the paper's CSS P:439-457): the DATA bytes of every field of one
+   * column, concatenated in row order; soff[r] = start of row r (soff[R] = total) */
+  int64_t str_col;
+  uint8_t *sbuf;
+  uint64_t scap, slen, *soff, socap;
 } or_result;
+static int64_t g_str_col = -1;          /* set by oracle_parse_strings for the duration of one call */
+static void *xrealloc(void *p, size_t n);
+
+static void str_row(or_result *r, const uint8_t *b, uint64_t n) {   /* append row R's string */
+  if (r->R + 2 > r->socap) {
+    r->socap = r->socap ? r->socap * 2 : 1024;
+    r->soff = (uint64_t *)xrealloc(r->soff, r->socap * 8);
+  }
+  r->soff[r->R] = r->slen;
+  if (r->slen + n > r->scap) {
+    while (r->slen + n > r->scap) r->scap = r->scap ? r->scap * 2 : 4096;
+    r->sbuf = (uint8_t *)xrealloc(r->sbuf, r->scap);
+  }
+  if (n) memcpy(r->sbuf + r->slen, b, n);
+  r->slen += n;
+}
 
 static void *xrealloc(void *p, size_t n) {
   void *q = realloc(p, n ? n : 1);
@@ -369,6 +390,7 @@ static void close_field(or_result *r, uint32_t c, uint64_t pos, uint64_t first, 
   if (!ok) v = 0;
   r->val[c][row] = v;
   r->valid[c][row] = (uint8_t)(r->types[c] == T_SPAN ? 0 : ok);
+  if ((int64_t)c == r->str_col) str_row(r, r->fbuf, r->flen);
   r->flen = 0;
 }
 
@@ -384,6 +406,7 @@ static void close_record(or_result *r, uint32_t c_next, uint64_t pos) {
       int def = r->types[k] != T_SPAN && r->has_def[k];
       r->val[k][r->R] = def ? r->def_bits[k] : 0;
       r->valid[k][r->R] = (uint8_t)def;
+      if ((int64_t)k == r->str_col) str_row(r, NULL, 0);       /* missing field: empty string */
     }
   }
   r->R++;
@@ -396,6 +419,7 @@ static or_result *run(int dialect, const walker *w, const uint8_t *in, uint64_t 
                       int strict, uint8_t *trace_state, uint8_t *trace_kind) {
   or_result *r = (or_result *)calloc(1, sizeof(or_result));
   r->C = C;
+  r->str_col = g_str_col < (int64_t)C ? g_str_col : -1;
   r->off = calloc(C ? C : 1, sizeof(void *));
   r->len = calloc(C ? C : 1, sizeof(void *));
   r->val = calloc(C ? C : 1, sizeof(void *));
@@ -512,7 +536,24 @@ void oracle_free(or_result *r) {
   }
   free(r->off); free(r->len); free(r->val); free(r->valid);
   free(r->types); free(r->has_def); free(r->def_bits);
+  free(r->sbuf); free(r->soff);
   free(r);
+}
+
+/* parse with string capture of column str_col (then oracle_strings_size / oracle_strings) */
+or_result *oracle_parse_strings(int dialect, const uint8_t *in, uint64_t n, uint32_t C, const uint8_t *types,
+                                uint32_t str_col) {
+  g_str_col = str_col;
+  or_result *r = run(dialect, NULL, in, n, C, types, NULL, NULL, 0, NULL, NULL);
+  g_str_col = -1;
+  return r;
+}
+uint64_t oracle_strings_size(const or_result *r) { return r->slen; }
+/* offsets[R + 1] (int64) and data[slen] */
+void oracle_strings(const or_result *r, int64_t *offsets, uint8_t *data) {
+  for (uint64_t i = 0; i < r->R; i++) offsets[i] = (int64_t)r->soff[i];
+  offsets[r->R] = (int64_t)r->slen;
+  if (r->slen) memcpy(data, r->sbuf, r->slen);
 }
 
 /* Conversion routines exposed for the number pins (R14/R15). */
