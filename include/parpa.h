@@ -210,6 +210,21 @@ int parpa_count(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint
                 uint32_t entry_state, void *stream, parpa_counts *out, parpa_tau *tau_out);
 int parpa_compose_tau(const parpa_dfa *dfa, const parpa_tau *a, const parpa_tau *b, parpa_tau *out);
 int parpa_compose_counts(const parpa_counts *a, const parpa_counts *b, parpa_counts *out);
+/* ---- string materialisation (the paper's CSS) ------------------ *
+ * For one column of a completed parse of the same device bytes (column->offset / ->length, device
+ * arrays of `rows` entries): the DATA bytes of every field — control bytes such as the escaping
+ * quote of "" or CLF's brackets and quotes dropped — concatenated in row order, Arrow layout.
+ * parpa_strings_size fills d_offsets (device, rows + 1 int64; d_offsets[0] = 0, d_offsets[rows] =
+ * total) and *total (host).  parpa_strings_copy then writes the bytes to d_data (device, >= total).
+ * Missing fields are empty strings.  Both re-run the scan half to locate DATA bytes and are
+ * synchronous on `stream`.  Errors: PARPA_EINVAL on null pointers. */
+int parpa_strings_size(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len,
+                       const parpa_column *column, uint64_t rows, int64_t *d_offsets, uint64_t *total,
+                       void *stream);
+int parpa_strings_copy(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len,
+                       const parpa_column *column, uint64_t rows, const int64_t *d_offsets,
+                       uint8_t *d_data, void *stream);
+
 /* ---- staged range plan: the same exchange with every pass run once per rank ------------- *
  * parpa_range_begin  runs S1-S3 on the device range [d_bytes, d_bytes+len) at global offset
  *                    `base` and returns the range's transition vector (host *tau_out) — the

@@ -385,6 +385,26 @@ def parse_range(dfa: Dfa, schema: Schema, data, entry_state: int, base: int, pre
                                ctypes.c_void_p(stats_tensor.data_ptr()), _stream_handle(stream)), "parpa_parse_range")
 
 
+def strings(dfa: Dfa, data, column, rows: int, stream=None):
+    """String materialisation of one parsed column (parpa_strings_size / _copy): returns
+    (offsets int64[rows + 1], data uint8[total]) on the GPU — the DATA bytes of every field with
+    control bytes dropped, Arrow layout."""
+    import torch
+    L = _lib.load()
+    _check_input(data)
+    offs = torch.empty(int(rows) + 1, dtype=torch.int64, device=data.device)
+    total = ctypes.c_uint64(0)
+    col = column.struct()
+    _check(L.parpa_strings_size(dfa.handle, ctypes.c_void_p(data.data_ptr()), data.numel(), ctypes.byref(col),
+                                int(rows), ctypes.c_void_p(offs.data_ptr()), ctypes.byref(total),
+                                _stream_handle(stream)), "parpa_strings_size")
+    buf = torch.empty(max(int(total.value), 1), dtype=torch.uint8, device=data.device)
+    _check(L.parpa_strings_copy(dfa.handle, ctypes.c_void_p(data.data_ptr()), data.numel(), ctypes.byref(col),
+                                int(rows), ctypes.c_void_p(offs.data_ptr()), ctypes.c_void_p(buf.data_ptr()),
+                                _stream_handle(stream)), "parpa_strings_copy")
+    return offs, buf[:int(total.value)]
+
+
 class RangePlan:
     """Staged parse of one byte range (the multi-GPU exchange with every pass run once):
     ``begin`` -> the range's transition vector, ``count(entry_state)`` -> its counts,

@@ -1050,6 +1050,69 @@ int parpa_range_emit(parpa_plan *p, const parpa_schema *sch, const parpa_context
   return rc;
 }
 
+// ---- string materialisation ---------------------------------------------------------------
+static int strings_impl(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, const parpa_column *col,
+                        uint64_t rows, int64_t *d_offsets, uint64_t *total, uint8_t *d_data, cudaStream_t s) {
+  Work w;
+  int rc = work_alloc(w, len, 1, len && misaligned(d_bytes), s);
+  if (rc) return rc;
+  const uint8_t *in = d_bytes;
+  rc = prepare_input(w, in, len, s);
+  KArgs a;
+  make_args(a, w, in, len);
+  a.seed_dev = dfa->dmap[dfa->start];
+  if (!rc) rc = launch_passes(MODE_COUNT, a, dfa->k, s, nullptr);       // the chunk masks
+  DevCfg *dc = nullptr;
+  if (!rc) rc = dev_cfg(&dc);
+  const unsigned long long *off = (const unsigned long long *)col->offset;
+  unsigned long long *v = (unsigned long long *)d_offsets;
+  if (!rc && rows) {
+    if (!d_data) {                                                      // sizes: per-row counts, scan
+      k_str_len<<<dc->sms * 8, 256, 0, s>>>(a, off, col->length, rows, v);
+      if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
+      const uint64_t nb = (rows + SCAN_TILE - 1) / SCAN_TILE;
+      void *sb = nullptr;
+      const size_t o_agg = (16 + nb * 4 + 15) / 16 * 16;                // 8-byte payloads stay aligned
+      const size_t bytes = o_agg + 2 * nb * 8;
+      if (!rc && cudaMallocAsync(&sb, bytes, s) != cudaSuccess) rc = PARPA_ENOMEM;
+      if (!rc && cudaMemsetAsync(sb, 0, bytes, s) != cudaSuccess) rc = PARPA_ECUDA;
+      if (!rc) {
+        uint8_t *b = (uint8_t *)sb;
+        k_scan_u64<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(v, rows, (unsigned int *)b, (uint32_t *)(b + 16),
+                                                          (unsigned long long *)(b + o_agg),
+                                                          (unsigned long long *)(b + o_agg + nb * 8));
+        if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
+      }
+      if (sb) cudaFreeAsync(sb, s);
+      if (!rc && total && cudaMemcpyAsync(total, v + rows, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = PARPA_ECUDA;
+    } else {
+      k_str_copy<<<dc->sms * 8, 256, 0, s>>>(a, off, col->length, rows, v, d_data);
+      if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
+    }
+  } else if (!rc && !d_data) {
+    if (cudaMemsetAsync(d_offsets, 0, 8, s) != cudaSuccess) rc = PARPA_ECUDA;
+    if (total) *total = 0;
+  }
+  work_free(w, s);
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
+  return rc;
+}
+
+int parpa_strings_size(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, const parpa_column *column,
+                       uint64_t rows, int64_t *d_offsets, uint64_t *total, void *stream) {
+  if (!dfa || !column || !d_offsets || !total || (len && !d_bytes) || (rows && (!column->offset || !column->length)))
+    return PARPA_EINVAL;
+  return strings_impl(dfa, d_bytes, len, column, rows, d_offsets, total, nullptr, (cudaStream_t)stream);
+}
+
+int parpa_strings_copy(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, const parpa_column *column,
+                       uint64_t rows, const int64_t *d_offsets, uint8_t *d_data, void *stream) {
+  if (!dfa || !column || !d_offsets || !d_data || (len && !d_bytes) || (rows && (!column->offset || !column->length)))
+    return PARPA_EINVAL;
+  return strings_impl(dfa, d_bytes, len, column, rows, const_cast<int64_t *>(d_offsets), nullptr, d_data,
+                      (cudaStream_t)stream);
+}
+
 // ---- debug ----------------------------------------------------------------------------------------
 int parpa_debug_trace(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint8_t *d_chunk_states,
                       uint8_t *d_kinds, uint8_t *d_states, void *stream) {

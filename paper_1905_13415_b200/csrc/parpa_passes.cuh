@@ -354,3 +354,146 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_seg_scan(const KArgs a) {
 }
 
 }  // namespace parpa
+
+// ---- string materialisation (the paper's CSS P:439-457) ---------------------------------
+// From a completed parse of the same bytes: for row r of a column (span offset / length), the DATA
+// bytes inside the span (control bytes such as the escaping quote of "" dropped), concatenated in row
+// order: offsets[R + 1] (Arrow layout) and the bytes.  The DATA bytes are located with the chunk
+// masks that k_pass2 stores.
+namespace parpa {
+
+constexpr uint32_t MISSING_LEN_DEV = 0xFFFFFFFFu;
+
+__device__ __forceinline__ unsigned long long dmask_of_chunk(const KArgs &a, unsigned long long k) {
+  return a.masks[(k >> 5) * 96 + (k & 31)];                  // [tile][D,F,R][lane]
+}
+// number of DATA bytes in [p, p + n) of the range
+__device__ unsigned long long data_bytes_in(const KArgs &a, unsigned long long p, unsigned long long n) {
+  unsigned long long cnt = 0, end = p + n;
+  while (p < end) {
+    const unsigned long long k = p >> 6, lo = p & 63, hi = min(64ull, end - (k << 6));
+    unsigned long long m = dmask_of_chunk(a, k) >> lo;
+    const unsigned long long w = hi - lo;
+    if (w < 64) m &= (1ull << w) - 1ull;
+    cnt += __popcll(m);
+    p = (k + 1) << 6;
+  }
+  return cnt;
+}
+
+__global__ void k_str_len(const KArgs a, const unsigned long long *off, const uint32_t *len, unsigned long long rows,
+                          unsigned long long *lens) {
+  for (unsigned long long r = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; r < rows;
+       r += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t L = len[r];
+    lens[r] = (L == MISSING_LEN_DEV || L == 0) ? 0ull : data_bytes_in(a, off[r] - a.base, L);
+  }
+}
+
+// in-place exclusive scan of v[0, n) (unsigned 64-bit), v[n] = total: single pass, decoupled look-back
+// over blocks of SCAN_TILE elements (flags: 1 aggregate, 2 inclusive; payload then release-flag)
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_u64(unsigned long long *v, unsigned long long n,
+                                                          unsigned int *ticket, uint32_t *flag,
+                                                          unsigned long long *agg, unsigned long long *incl) {
+  __shared__ uint32_t s_bid;
+  __shared__ unsigned long long s_warp[SCAN_THREADS / 32], s_prefix;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t b = s_bid;
+  const unsigned long long i0 = (unsigned long long)b * SCAN_TILE + (unsigned long long)threadIdx.x * SCAN_ITEMS;
+  unsigned long long x[SCAN_ITEMS], loc = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; k++) {
+    x[k] = i0 + k < n ? v[i0 + k] : 0ull;
+    loc += x[k];
+  }
+  unsigned long long inc = loc;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < SCAN_THREADS / 32 ? s_warp[lane] : 0ull;
+#pragma unroll
+    for (int d = 1; d < SCAN_THREADS / 32; d <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w += o;
+    }
+    const unsigned long long bagg = __shfl_sync(0xffffffffu, w, SCAN_THREADS / 32 - 1);
+    const unsigned long long bex = __shfl_up_sync(0xffffffffu, w, 1);
+    if (lane < SCAN_THREADS / 32) s_warp[lane] = lane == 0 ? 0ull : bex;
+    unsigned long long prefix = 0;
+    if (b == 0) {
+      if (lane == 0) { __stcg(incl, bagg); st_release_u32(flag, FLAG_INCL); }
+    } else {
+      if (lane == 0) { __stcg(agg + b, bagg); st_release_u32(flag + b, FLAG_AGG); }
+      long long base = (long long)b - 1;
+      while (true) {                                          // look-back, one block per lane
+        const long long j = base - lane;
+        uint32_t f = j >= 0 ? ld_acquire_u32(flag + j) : FLAG_INCL;
+        unsigned incm, zero;
+        int L;
+        while (true) {
+          incm = __ballot_sync(0xffffffffu, f == FLAG_INCL);
+          zero = __ballot_sync(0xffffffffu, f == 0u);
+          L = incm ? __ffs(incm) - 1 : 31;
+          const unsigned need = L == 31 ? 0xFFFFFFFFu : ((2u << L) - 1u);
+          if (!(zero & need)) break;
+          __nanosleep(32);
+          if (f == 0u) f = ld_acquire_u32(flag + j);
+        }
+        unsigned long long val = 0;
+        if (lane <= L && j >= 0) val = f == FLAG_INCL ? __ldcg(incl + j) : __ldcg(agg + j);
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) val += __shfl_down_sync(0xffffffffu, val, d);
+        prefix += __shfl_sync(0xffffffffu, val, 0);
+        if (incm) break;
+        base -= 32;
+      }
+      if (lane == 0) { __stcg(incl + b, prefix + bagg); st_release_u32(flag + b, FLAG_INCL); }
+    }
+    if (lane == 0) {
+      s_prefix = prefix;
+      if ((unsigned long long)(b + 1) * SCAN_TILE >= n) v[n] = prefix + bagg;   // total
+    }
+  }
+  __syncthreads();
+  const unsigned long long wex = __shfl_up_sync(0xffffffffu, inc, 1);
+  unsigned long long cur = s_prefix + s_warp[warp] + (lane == 0 ? 0ull : wex) ;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; k++) {
+    if (i0 + k < n) v[i0 + k] = cur;
+    cur += x[k];
+  }
+}
+
+// one warp per row: copy the DATA bytes of the span to data[offsets[r] ...]
+__global__ void k_str_copy(const KArgs a, const unsigned long long *off, const uint32_t *len, unsigned long long rows,
+                           const unsigned long long *offsets, uint8_t *data) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long nw = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  for (unsigned long long r = blockIdx.x * (unsigned long long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
+       r += nw) {
+    const uint32_t L = len[r];
+    if (L == MISSING_LEN_DEV || L == 0) continue;
+    const unsigned long long p0 = off[r] - a.base, o0 = offsets[r];
+    const bool all = offsets[r + 1] - o0 == L;                 // no control byte inside: plain copy
+    unsigned long long o = o0;
+    for (unsigned long long q = 0; q < L; q += 32) {
+      const unsigned long long p = p0 + q + lane;
+      const bool in = q + lane < L;
+      const uint8_t c = in ? a.in[p] : 0;
+      bool keep = in;
+      if (!all && in) keep = (dmask_of_chunk(a, p >> 6) >> (p & 63)) & 1ull;
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) data[o + __popc(m & ((1u << lane) - 1u))] = c;
+      o += __popc(m);
+    }
+  }
+}
+
+}  // namespace parpa

@@ -296,3 +296,30 @@ def test_timestamp_edge_cases():
     types = [oracle.INT64, oracle.TIMESTAMP]
     run_all_paths("csv", data, types, label="ts-edge")
     run_all_paths("csv", data, types, defaults=[None, 12345], label="ts-edge-default")
+
+
+@pytest.mark.parametrize("name,cols", [("cfg1", range(8)), ("yelp", [0, 7, 8]), ("clf", [2, 3, 4]),
+                                       ("taxi", [1, 6])])
+def test_strings_materialisation(name, cols):
+    """DATA bytes of every field of a column (control bytes dropped), Arrow layout."""
+    w = datagen.WORKLOADS[name]
+    data, g = datagen.generate(name, 2_000_000)
+    d = dev(data)
+    res = parpa.parse(dfa(w.dialect), parpa.Schema(list(w.types)), d)
+    R = res.records
+    for c in cols:
+        ro, rs = oracle.strings(w.dialect, data, w.C, c, list(w.types))
+        offs, buf = parpa.strings(dfa(w.dialect), d, res.columns[c], R)
+        assert np.array_equal(offs.cpu().numpy(), ro), (name, c)
+        assert bytes(buf.cpu().numpy()) == rs, (name, c)
+
+
+def test_strings_escapes_missing_and_empty():
+    data = b'a,"x""y",z\n"p,q"\n,,\n"multi\nline",""\n' * 3000 + b'"tail ""quoted"" text, with, commas",9'
+    types = [oracle.SPAN] * 3
+    d = dev(data)
+    res = parpa.parse(dfa("csv"), parpa.Schema(types), d)
+    for c in range(3):
+        ro, rs = oracle.strings("csv", data, 3, c)
+        offs, buf = parpa.strings(dfa("csv"), d, res.columns[c], res.records)
+        assert np.array_equal(offs.cpu().numpy(), ro) and bytes(buf.cpu().numpy()) == rs, c
