@@ -210,6 +210,14 @@ int parpa_count(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint
                 uint32_t entry_state, void *stream, parpa_counts *out, parpa_tau *tau_out);
 int parpa_compose_tau(const parpa_dfa *dfa, const parpa_tau *a, const parpa_tau *b, parpa_tau *out);
 int parpa_compose_counts(const parpa_counts *a, const parpa_counts *b, parpa_counts *out);
+/* ---- column-count inference ------------------------------------------------ *
+ * parpa_infer_columns — the number of records and the minimum / maximum number of fields per record
+ * of the device bytes under the DFA (host outputs; synchronous on `stream`): what a schema's C
+ * should be (reading R13 takes C from the schema).  Returns PARPA_EFORMAT (outputs still set for
+ * the bytes before the first invalid one is reached) if the input reaches the invalid state. */
+int parpa_infer_columns(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, void *stream,
+                        uint32_t *min_fields, uint32_t *max_fields, uint64_t *records);
+
 /* ---- string materialisation (the paper's CSS) ------------------ *
  * For one column of a completed parse of the same device bytes (column->offset / ->length, device
  * arrays of `rows` entries): the DATA bytes of every field — control bytes such as the escaping

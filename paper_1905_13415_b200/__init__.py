@@ -385,6 +385,16 @@ def parse_range(dfa: Dfa, schema: Schema, data, entry_state: int, base: int, pre
                                ctypes.c_void_p(stats_tensor.data_ptr()), _stream_handle(stream)), "parpa_parse_range")
 
 
+def infer_columns(dfa: Dfa, data, stream=None):
+    """(records, min fields per record, max fields per record) of the device bytes (parpa_infer_columns)."""
+    L = _lib.load()
+    _check_input(data)
+    mn, mx, r = ctypes.c_uint32(0), ctypes.c_uint32(0), ctypes.c_uint64(0)
+    _check(L.parpa_infer_columns(dfa.handle, ctypes.c_void_p(data.data_ptr()), data.numel(), _stream_handle(stream),
+                                 ctypes.byref(mn), ctypes.byref(mx), ctypes.byref(r)), "parpa_infer_columns")
+    return int(r.value), int(mn.value), int(mx.value)
+
+
 def strings(dfa: Dfa, data, column, rows: int, stream=None):
     """String materialisation of one parsed column (parpa_strings_size / _copy): returns
     (offsets int64[rows + 1], data uint8[total]) on the GPU — the DATA bytes of every field with

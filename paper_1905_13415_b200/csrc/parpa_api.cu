@@ -1050,6 +1050,46 @@ int parpa_range_emit(parpa_plan *p, const parpa_schema *sch, const parpa_context
   return rc;
 }
 
+// ---- column-count inference ---------------------------------------------------------------
+int parpa_infer_columns(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, void *stream,
+                        uint32_t *min_fields, uint32_t *max_fields, uint64_t *records) {
+  if (!dfa || !min_fields || !max_fields || !records || (len && !d_bytes)) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  parpa_plan p;
+  int rc = plan_scan(dfa, d_bytes, len, dfa->dmap[dfa->start], seg_identity(), 0, 1, s, &p);
+  unsigned int *d_mm = nullptr;
+  unsigned int mm[2] = {0xFFFFFFFFu, 0u};
+  if (!rc && cudaMallocAsync(&d_mm, 8, s) != cudaSuccess) rc = PARPA_ENOMEM;
+  if (!rc && cudaMemcpyAsync(d_mm, mm, 8, cudaMemcpyHostToDevice, s) != cudaSuccess) rc = PARPA_ECUDA;
+  if (!rc && p.w.ntiles) {
+    DevCfg *dc;
+    if (!(rc = dev_cfg(&dc))) {
+      k_infer_cols<<<dc->sms * 4, 256, 0, s>>>(p.a, d_mm);
+      if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
+    }
+  }
+  if (!rc && cudaMemcpyAsync(mm, d_mm, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = PARPA_ECUDA;
+  Seg tot;
+  uint32_t tau;
+  uint64_t fi;
+  if (!rc) rc = plan_totals(&p, tot, tau, fi);               // synchronises
+  if (d_mm) cudaFreeAsync(d_mm, s);
+  work_free(p.w, s);
+  if (rc) return rc;
+  uint64_t R = tot.recs;
+  const uint32_t fin = nib_at(tau, p.a.seed_dev);
+  if (dfa->k.eoi[fin] == EOI_RECORD) {                         // the implicit last record
+    const uint32_t n = tot.col + 1;
+    mm[0] = std::min(mm[0], n);
+    mm[1] = std::max(mm[1], n);
+    R++;
+  }
+  *records = R;
+  *min_fields = R ? mm[0] : 0;
+  *max_fields = mm[1];
+  return fi != NONE ? PARPA_EFORMAT : PARPA_OK;
+}
+
 // ---- string materialisation ---------------------------------------------------------------
 static int strings_impl(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, const parpa_column *col,
                         uint64_t rows, int64_t *d_offsets, uint64_t *total, uint8_t *d_data, cudaStream_t s) {

@@ -497,3 +497,44 @@ __global__ void k_str_copy(const KArgs a, const unsigned long long *off, const u
 }
 
 }  // namespace parpa
+
+// ---- column-count inference (reading R13's NEXT) ------------------------------------------
+// Fields per record over the whole input: each lane walks its delimiters from its exact starting
+// column (the tile prefix composed with the lane-exclusive chunk summaries), and every record
+// delimiter contributes column + 1.  Warp min / max, then one atomic per warp.
+namespace parpa {
+__global__ void k_infer_cols(const KArgs a, unsigned int *minmax) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+  uint32_t mn = 0xFFFFFFFFu, mx = 0;
+  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < a.ntiles; t += nw) {
+    const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
+    const int nv = chunk_valid(a, cstart);
+    const unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;
+    const unsigned long long Dm = mk[0], Fm = mk[32], Rm = mk[64];
+    const unsigned long long Vm = nv >= 64 ? ~0ull : ((1ull << nv) - 1ull);
+    SegT sagg;
+    const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
+    const Seg st = seg_op(seg_op(a.seed, a.tinfo[t].excl), segt_to_seg(sex, a.base + (unsigned long long)t * WT));
+    uint32_t c = st.col;
+    unsigned long long fm = Fm;
+    while (fm) {
+      const int p = lsb64(fm);
+      fm &= fm - 1ull;
+      if ((Rm >> p) & 1ull) {
+        mn = min(mn, c + 1u);
+        mx = max(mx, c + 1u);
+        c = 0;
+      } else {
+        c++;
+      }
+    }
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) {
+    if (mn != 0xFFFFFFFFu) atomicMin(minmax, mn);
+    atomicMax(minmax + 1, mx);
+  }
+}
+}  // namespace parpa

@@ -323,3 +323,38 @@ def test_strings_escapes_missing_and_empty():
         ro, rs = oracle.strings("csv", data, 3, c)
         offs, buf = parpa.strings(dfa("csv"), d, res.columns[c], res.records)
         assert np.array_equal(offs.cpu().numpy(), ro) and bytes(buf.cpu().numpy()) == rs, c
+
+
+def _oracle_field_counts(dialect, data):
+    """Fields per record from the oracle's per-byte emission kinds (a sequential walk)."""
+    r = oracle.parse(dialect, data, 1, trace=True)
+    counts, c = [], 0
+    for k in r.trace_kind.tolist():
+        if k == 2:
+            c += 1
+        elif k == 3:
+            counts.append(c + 1)
+            c = 0
+    if r.eoi_action == 1:
+        counts.append(c + 1)
+    return counts
+
+
+@pytest.mark.parametrize("name", ["cfg1", "yelp", "clf", "taxi"])
+def test_infer_columns_workloads(name):
+    w = datagen.WORKLOADS[name]
+    data, g = datagen.generate(name, 1_200_000)
+    R, mn, mx = parpa.infer_columns(dfa(w.dialect), dev(data))
+    assert (R, mn, mx) == (g.records, w.C, w.C)
+
+
+def test_infer_columns_ragged():
+    rng = random.Random(5)
+    rows = []
+    for i in range(20000):
+        n = rng.choice([1, 2, 3, 7, 40]) if i % 97 else rng.randint(1, 300)
+        rows.append(",".join(('"a,\n"' if rng.random() < 0.1 else str(rng.randint(0, 999))) for _ in range(n)))
+    data = ("\n".join(rows)).encode()                          # no trailing newline: EOI record
+    counts = _oracle_field_counts("csv", data)
+    R, mn, mx = parpa.infer_columns(dfa("csv"), dev(data))
+    assert (R, mn, mx) == (len(counts), min(counts), max(counts))
