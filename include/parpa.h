@@ -102,7 +102,9 @@ typedef struct {
  *              missing field the position of the record delimiter that ended the record)
  *   length[r]  uint32: last DATA byte + 1 - offset; 0 if empty; PARPA_MISSING_LENGTH if missing
  *   value[r]   int64 / double (typed columns only; NULL for spans); 0 when invalid
- *   valid[r]   uint8: 1 if value holds a converted or default value (typed columns only) */
+ *   valid[r]   uint8: 1 if value holds a converted or default value (typed columns only)
+ * A column whose four pointers are all NULL is skipped: it still counts as a column of
+ * the record (missing / extra accounting unchanged) but nothing is converted or written for it. */
 typedef struct {
   uint64_t *offset;
   uint32_t *length;

@@ -136,6 +136,8 @@ class Column:
         self.offset, self.length, self.value, self.valid = offset, length, value, valid
 
     def struct(self):
+        if self.offset is None:                                   # skipped column
+            return _lib.Column_t(None, None, None, None)
         return _lib.Column_t(self.offset.data_ptr(), self.length.data_ptr(),
                              self.value.data_ptr() if self.value is not None else None,
                              self.valid.data_ptr() if self.valid is not None else None)

@@ -266,6 +266,10 @@ int set_columns(const parpa_schema *sch, const parpa_column *cols, uint32_t C, C
     d.has_def = sch->has_default ? sch->has_default[c] : 0;
     d.def_bits = sch->default_bits ? sch->default_bits[c] : 0;
     if (d.type > PARPA_TIMESTAMP) return PARPA_EINVAL;
+    if (!d.off && !d.len && !d.val && !d.valid) {            // skipped column: counted, not written
+      d.type = T_SKIP;
+      continue;
+    }
     if (!d.off || !d.len) return PARPA_EINVAL;
     if (d.type != PARPA_SPAN && (!d.val || !d.valid)) return PARPA_EINVAL;
   }

@@ -20,7 +20,7 @@
 namespace parpa {
 
 enum { MODE_TAU = 0, MODE_COUNT = 1, MODE_EMIT = 2 };
-enum { T_SPAN = 0, T_INT64 = 1, T_FLOAT64 = 2, T_TIMESTAMP = 3 };
+enum { T_SPAN = 0, T_INT64 = 1, T_FLOAT64 = 2, T_TIMESTAMP = 3, T_SKIP = 4 };   // T_SKIP: internal
 // TS = the schema has timestamp columns: the emission kernels are instantiated with and without
 // them so that schemas without timestamps carry none of that code (registers, stack).
 template <bool TS, class Src>
@@ -413,6 +413,7 @@ __device__ void emit_field(const KArgs &a, const ColDesc *cols, unsigned long lo
   unsigned long long row = r - a.row_base;
   if (row >= a.cap) return;                         // capacity exceeded: reported by k_finalize
   const ColDesc *cd = cols + c;
+  if (cd->type == T_SKIP) return;
   unsigned long long off;
   uint32_t len;
   if (fd == NONE) {
@@ -454,6 +455,7 @@ __device__ void fill_missing(const KArgs &a, const ColDesc *cols, unsigned long 
   if (row >= a.cap) return;
   for (uint32_t k = from; k < a.C; k++) {
     const ColDesc *cd = cols + k;
+    if (cd->type == T_SKIP) continue;
     cd->off[row] = dpos;
     cd->len[row] = 0xFFFFFFFFu;
     if (cd->type != T_SPAN) {
@@ -798,9 +800,10 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     if (row >= a.cap) continue;
     const uint32_t k = start + (ci - cs);
     const ColDesc *cd = cols + ci;
+    const bool skip = cd->type == T_SKIP;
     if (k < end) {
       const uint32_t e = ws->fields[k];
-      if (e == FIELD_WRITTEN) continue;
+      if (e == FIELD_WRITTEN || skip) continue;
       uint32_t len;
       unsigned long long off;
       bool ic;
@@ -819,6 +822,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
       if (cd->type != T_SPAN) write_value<TS>(a, cd, ci, row, off, off + len - 1, ic, len == 0, tb, tbase_g);
     } else if (ji < nrec) {                                 // record closed with fewer fields
       if (k == end) cnt.missing++;
+      if (skip) continue;
       __stcs(cd->off + row, tbase_g + (ws->rows[ji] >> 16));
       __stcs(cd->len + row, 0xFFFFFFFFu);
       if (cd->type != T_SPAN) {

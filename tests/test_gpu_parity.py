@@ -358,3 +358,38 @@ def test_infer_columns_ragged():
     counts = _oracle_field_counts("csv", data)
     R, mn, mx = parpa.infer_columns(dfa("csv"), dev(data))
     assert (R, mn, mx) == (len(counts), min(counts), max(counts))
+
+
+def test_skipped_columns():
+    """columns with NULL pointers are skipped; the others equal the full parse."""
+    w = datagen.WORKLOADS["cfg1"]
+    data, g = datagen.generate("cfg1", 400_000)
+    ora = oracle.parse("csv", data, w.C, list(w.types))
+    schema = parpa.Schema(list(w.types))
+    cap = ora.R + 1
+    cols = parpa.alloc_columns(schema, cap)
+    keep = [0, 2, 5]
+    cols = [c if i in keep else parpa.Column(None, None) for i, c in enumerate(cols)]
+    st = parpa.new_stats_tensor()
+    parpa.parse_into(dfa("csv"), schema, dev(data), cols, cap, st)
+    s = parpa.stats_from_tensor(st)
+    assert s["status"] == 0 and s["records"] == ora.R and s["missing_records"] == ora.n_missing
+    for c in keep:
+        assert np.array_equal(to_np(cols[c].offset).view(np.uint64)[:ora.R], ora.offset[c])
+        assert np.array_equal(to_np(cols[c].length).view(np.uint32)[:ora.R], ora.length[c])
+        if w.types[c] != oracle.SPAN:
+            assert np.array_equal(to_np(cols[c].value).view(np.int64)[:ora.R], ora.value[c])
+
+
+@pytest.mark.parametrize("big", [3_000_000, 9_000_001])
+def test_giant_field_spanning_tiles_and_scan_blocks(big):
+    """SURVEY N4 (the paper's 200 MB-record experiment, scaled): one quoted field of several MB, with
+    escaped quotes and newlines inside, between ordinary records; plus a long numeric field."""
+    rng = random.Random(big)
+    body = bytearray()
+    while len(body) < big:
+        body += rng.choice([b"word ", b"x,y ", b'""q"" ', b"\n", b"zz "])
+    data = (b"1,a,2.5\n" * 1000 + b'2,"' + bytes(body) + b'",3.25\n' + b"3,b,0." + b"1" * 5000 + b"\n" +
+            b"4,c,7\n" * 1000)
+    types = [oracle.INT64, oracle.SPAN, oracle.FLOAT64]
+    run_all_paths("csv", data, types, label=f"giant-{big}")
