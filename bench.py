@@ -46,13 +46,15 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic(config):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+def load_traffic(config, nbytes, timestamps=False):
+    """DRAM bytes per launch of the dominant kernel: the committed ncu --set full measurement
+    (profiles/ncu_traffic.json, bytes per input byte of that config) times this launch's input."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(config)
+        r = d.get(config + ("+ts" if timestamps else ""))
+        return int(r["dram_bytes_per_input_byte"] * nbytes) if r else None
     except Exception:
         return None
 
@@ -228,11 +230,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # test switch: every rank on cuda:0 with gloo collectives (validates the sharded path on one GPU;
+    # never used for a reported number)
+    shared = os.environ.get("PARPA_BENCH_SHARED_GPU") == "1"
+    gpu = 0 if shared else local
+    coll = "cpu" if shared else "cuda"
+    torch.cuda.set_device(gpu)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = workload(args.config, args.timestamps)
     dfa = parpa.Dfa.dialect(w.dialect)
     schema = parpa.Schema(list(w.types))
@@ -246,7 +256,7 @@ def main():
     left = left_host.cuda() if left_host is not None else None
     base = 0
     if world > 1:
-        lens = torch.tensor([block_len], dtype=torch.int64, device="cuda")
+        lens = torch.tensor([block_len], dtype=torch.int64, device=coll)
         all_lens = [torch.zeros_like(lens) for _ in range(world)]
         dist.all_gather(all_lens, lens)
         base = sum(int(x.item()) for x in all_lens[:rank]) + cut0
@@ -268,7 +278,8 @@ def main():
     def step():
         if world == 1:
             return parpa.parse_into(dfa, schema, d, cols, cap, st)
-        pdist.parse_sharded(dfa, schema, d, base, cols, cap, st, left=left, is_last=is_last)
+        pdist.parse_sharded(dfa, schema, d, base, cols, cap, st, left=left, is_last=is_last,
+                            exchange_device=coll)
         return 7                                  # range_begin 2 + range_count 2 + range_emit 3
 
     for _ in range(args.warmup):
@@ -278,9 +289,13 @@ def main():
     assert stats["status"] == 0, stats
     if world == 1:
         assert stats["records"] == g.records, (stats, g.records)
+    else:                                                     # the ranks' records add up exactly
+        tr = torch.tensor([stats["records"], g.records], dtype=torch.float64, device=coll)
+        dist.all_reduce(tr, op=dist.ReduceOp.SUM)
+        assert int(tr[0].item()) == int(tr[1].item()), (stats, tr)
 
     clocks = Clocks()
-    clocks.start(local)
+    clocks.start(gpu)
     parpa.set_profiling(True)
     if dist:
         dist.barrier()
@@ -300,10 +315,10 @@ def main():
     clk = clocks.stop()
     ms_step = ms_total / args.steps
     if dist:
-        t = torch.tensor([ms_step], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms_step], dtype=torch.float64, device=coll)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
-        tb = torch.tensor([n], dtype=torch.float64, device="cuda")
+        tb = torch.tensor([n], dtype=torch.float64, device=coll)
         dist.all_reduce(tb, op=dist.ReduceOp.SUM)
         total_bytes = float(tb.item())
     else:
@@ -325,7 +340,7 @@ def main():
     if kt:
         kms = statistics.mean(kt)
         achieved = alg_bytes / (kms * 1e-3) / 1e9
-        tr = load_traffic(args.config)
+        tr = load_traffic(args.config, n, args.timestamps)
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": tr, "kernel": dom, "kernel_ms": round(kms, 4),
                 "algorithmic_bytes_per_launch": int(alg_bytes), "peak_source": peak_src,
@@ -348,7 +363,7 @@ def main():
                 "config": {"workload": args.config, "description": CONFIG_LABEL[args.config], "timestamps": bool(args.timestamps),
                            "bytes_per_gpu": n, "records_per_gpu": R, "columns": w.C, "typed_columns": T,
                            "dialect": w.dialect, "path": "parse_into (k_pass1, k_tau_scan, k_pass2, k_seg_scan, k_emit, k_finalize, k_deferred)" if world == 1 else
-                           "summarize + allgather + count + allgather + parse_range",
+                           "range_begin + allgather(tau) + range_count + allgather(counts) + range_emit",
                            "l2": "input >> 126 MB L2 (no flush needed)", "generate_s": round(t_gen, 1),
                            "kernel_ms": {k: round(statistics.mean(v), 4) for k, v in per_kernel.items()}},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}

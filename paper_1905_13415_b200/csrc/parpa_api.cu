@@ -1011,6 +1011,7 @@ int parpa_range_begin(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len
   if (!rc && p->w.ntiles && cudaMemcpyAsync(&tau, p->w.tot_tau, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess)
     rc = PARPA_ECUDA;
   if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
+  prof_end();
   if (rc) { work_free(p->w, s); delete p; return rc; }
   host_tau_dfa(dfa, tau, tau_out);
   *out = p;
@@ -1021,6 +1022,7 @@ int parpa_range_count(parpa_plan *p, uint32_t entry_state, parpa_counts *out) {
   if (!p || !out || entry_state >= p->dfa->S) return PARPA_EINVAL;
   p->a.seed_dev = p->dfa->dmap[entry_state];
   int rc = launch_half2(p->a, p->dfa->k, p->s, nullptr);
+  prof_end();
   if (rc) return rc;
   Seg tot;
   uint32_t tau;
@@ -1051,6 +1053,7 @@ int parpa_range_emit(parpa_plan *p, const parpa_schema *sch, const parpa_context
   a.is_last = is_last;
   rc = launch_emit(a, p->dfa->k, ck, s, nullptr);
   if (!rc) rc = launch_tail(a, p->dfa->k, ck, s, nullptr);
+  prof_end();
   return rc;
 }
 

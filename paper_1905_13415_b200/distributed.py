@@ -80,14 +80,15 @@ def exchange(dfa, local_tau: list, count_fn, group=None, device=None):
 
 
 def parse_sharded(dfa, schema, data, base: int, columns, capacity: int, stats_tensor, left=None,
-                  is_last: bool = True, group=None, stream=None):
+                  is_last: bool = True, group=None, stream=None, exchange_device=None):
     """Parse this rank's range after the summary exchange.  data / left: CUDA uint8 tensors.
     Every pass runs once per rank: S1-S3 (range_begin) -> allgather τ -> S4-S5 from the entry
     state (range_count) -> allgather counts -> S6-S7 with the ⊕-prefix (range_emit)."""
     from . import RangePlan
     plan = RangePlan(dfa, data, base, stream)
     try:
-        e, prefix, _ = exchange(dfa, plan.tau, plan.count, group, data.device)
+        e, prefix, _ = exchange(dfa, plan.tau, plan.count, group,
+                                exchange_device if exchange_device is not None else data.device)
         plan.emit(schema, prefix, columns, capacity, stats_tensor, left=left, is_last=is_last)
     finally:
         plan.close()
