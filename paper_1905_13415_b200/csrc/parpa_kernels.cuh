@@ -118,6 +118,15 @@ struct KArgs {
 constexpr uint32_t FLAG_AGG = 1, FLAG_INCL = 2;
 
 // ---- shared-memory LUT ------------------------------------------------------------------------
+// The pass kernels place the LUT at a 64 KB-aligned shared-window address S, so that one PRMT builds
+// the whole 32-bit LDS address of an input byte: (S >> 16) << 16 | b << 8 | lane slot  ("laneaddr"
+// holds the lane slot in byte 0 and S >> 16 in byte 2; selector 0x56k4).
+template <int OFF>
+__device__ __forceinline__ uint2 lds_u2(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2+%3];" : "=r"(v.x), "=r"(v.y) : "r"(addr), "n"(OFF));
+  return v;
+}
 __device__ __forceinline__ void build_lut(uint8_t *lut, const DfaK &d) {
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
     int b = i >> 5, half = (i >> 4) & 1, slot = i & 15;
@@ -155,8 +164,7 @@ __device__ __forceinline__ uint32_t gather4(uint32_t x, uint32_t bitmask, uint32
 }
 
 template <bool FULL>
-__device__ __forceinline__ uint32_t chunk_masks(const uint8_t *lut, const uint32_t (&v)[16], int nvalid,
-                                                uint32_t laneoff, uint32_t entry,
+__device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_t (&v)[16], int nvalid, uint32_t entry,
                                                 unsigned long long &Dm, unsigned long long &Fm,
                                                 unsigned long long &Rm) {
   uint32_t x = 0x80u | entry;
@@ -168,8 +176,7 @@ __device__ __forceinline__ uint32_t chunk_masks(const uint8_t *lut, const uint32
     for (int k = 0; k < 4; k++) {
       int i = 4 * w + k;
       if (FULL || i < nvalid) {
-        uint32_t addr = prmt(v[w], laneoff, 0x5504u | ((uint32_t)k << 4));
-        uint2 st = *reinterpret_cast<const uint2 *>(lut + addr + 128);
+        const uint2 st = lds_u2<128>(prmt(v[w], laneaddr, 0x5604u | ((uint32_t)k << 4)));
         x = prmt(st.x, st.y, x);
         xs[k] = x;
       } else {
@@ -192,8 +199,8 @@ __device__ __forceinline__ uint32_t chunk_masks(const uint8_t *lut, const uint32
 // ---- 4-way ILP τ: the chunk is cut into four 16-byte quarters with independent PRMT chains, composed
 // at the end.  qt[q] = nibble τ of quarter q (q = 0..2).
 template <bool FULL>
-__device__ __forceinline__ void chunk_tau4(const uint8_t *lut, const uint32_t (&v)[16], int nvalid,
-                                           uint32_t laneoff, uint32_t &t0, uint32_t &t1, uint32_t (&qt)[3]) {
+__device__ __forceinline__ void chunk_tau4(uint32_t laneaddr, const uint32_t (&v)[16], int nvalid,
+                                           uint32_t &t0, uint32_t &t1, uint32_t (&qt)[3]) {
   uint32_t a0[4], a1[4];
 #pragma unroll
   for (int q = 0; q < 4; q++) { a0[q] = 0x83828180u; a1[q] = 0x87868584u; }
@@ -203,8 +210,7 @@ __device__ __forceinline__ void chunk_tau4(const uint8_t *lut, const uint32_t (&
     for (int q = 0; q < 4; q++) {
       const int b = 16 * q + i;
       if (!FULL && b >= nvalid) continue;
-      uint32_t addr = prmt(v[b >> 2], laneoff, 0x5504u | ((uint32_t)(b & 3) << 4));
-      uint2 e = *reinterpret_cast<const uint2 *>(lut + addr);
+      const uint2 e = lds_u2<0>(prmt(v[b >> 2], laneaddr, 0x5604u | ((uint32_t)(b & 3) << 4)));
       uint32_t n0 = prmt(a0[q], a1[q], e.x);
       uint32_t n1 = prmt(a0[q], a1[q], e.y);
       a0[q] = n0;

@@ -23,7 +23,29 @@
 namespace parpa {
 
 constexpr int PASS_WARPS = 32;                       // k_pass1 / k_pass2: one 1024-thread CTA per SM
-constexpr size_t PASS_SMEM = LUT_BYTES + PASS_WARPS * 2 * WT;   // LUT + two tile buffers per warp
+constexpr size_t PASS_SMEM = LUT_BYTES + (PASS_WARPS + 1) * 2 * WT;   // LUT + two tile buffers per warp (+1 slack)
+
+// Shared-memory layout of the pass kernels: the LUT at the first 64 KB-aligned shared address of the
+// dynamic region (so a PRMT yields full LDS addresses, see lds_u2), the per-warp tile buffers in the
+// space before and after it.
+struct PassSmem {
+  uint8_t *lut;
+  uint4 *bufs;
+  uint32_t laneaddr, laneoff;
+};
+__device__ __forceinline__ PassSmem pass_smem(uint8_t *smem, int warp, int lane) {
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t lut_off = ((sb + 0xFFFFu) & ~0xFFFFu) - sb;
+  const uint32_t nfirst = lut_off / (2 * WT);
+  const uint32_t boff = (uint32_t)warp < nfirst ? (uint32_t)warp * 2 * WT
+                                                : lut_off + LUT_BYTES + ((uint32_t)warp - nfirst) * 2 * WT;
+  PassSmem p;
+  p.lut = smem + lut_off;
+  p.bufs = reinterpret_cast<uint4 *>(smem + boff);
+  p.laneoff = (uint32_t)(lane & 15) * 8u;
+  p.laneaddr = p.laneoff | (((sb + lut_off) >> 16) << 16);
+  return p;
+}
 constexpr int SCAN_THREADS = 256, SCAN_ITEMS = 8;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS; // warp tiles per scan block (4 MB of input)
 
@@ -62,11 +84,11 @@ __device__ __forceinline__ void read_chunk(const uint4 *buf, int lane, uint32_t 
 // ---- K1: pass 1 ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass1(const KArgs a, const DfaK dfa) {
   extern __shared__ __align__(16) uint8_t smem[];
-  build_lut(smem, dfa);
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint4 *bufs = reinterpret_cast<uint4 *>(smem + LUT_BYTES) + (size_t)warp * 2 * (WT / 16);
-  const uint32_t laneoff = (uint32_t)(lane & 15) * 8u;
+  const PassSmem ps = pass_smem(smem, warp, lane);
+  build_lut(ps.lut, dfa);
+  __syncthreads();
+  uint4 *bufs = ps.bufs;
   const uint32_t nw = gridDim.x * PASS_WARPS;
   uint32_t t = blockIdx.x * PASS_WARPS + warp;
   if (t < a.ntiles) stage_chunk(a, bufs, t, lane);
@@ -79,8 +101,8 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass1(const KArgs a, con
     const int nv = chunk_valid(a, cstart);
     uint32_t v[16], t0, t1, qt[3];
     read_chunk(bufs + i * (WT / 16), lane, v);
-    if (nv == CHUNK) chunk_tau4<true>(smem, v, nv, laneoff, t0, t1, qt);
-    else chunk_tau4<false>(smem, v, nv, laneoff, t0, t1, qt);
+    if (nv == CHUNK) chunk_tau4<true>(ps.laneaddr, v, nv, t0, t1, qt);
+    else chunk_tau4<false>(ps.laneaddr, v, nv, t0, t1, qt);
     uint32_t agg;
     const uint32_t ex = warp_scan_tau(t0, t1, agg);
     a.lex[(unsigned long long)t * 32 + lane] = ex;
@@ -202,11 +224,11 @@ __device__ __forceinline__ SegT warp_tile_segt(unsigned long long Dm, unsigned l
 // ---- K3: pass 2 ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, const DfaK dfa) {
   extern __shared__ __align__(16) uint8_t smem[];
-  build_lut(smem, dfa);
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint4 *bufs = reinterpret_cast<uint4 *>(smem + LUT_BYTES) + (size_t)warp * 2 * (WT / 16);
-  const uint32_t laneoff = (uint32_t)(lane & 15) * 8u;
+  const PassSmem ps = pass_smem(smem, warp, lane);
+  build_lut(ps.lut, dfa);
+  __syncthreads();
+  uint4 *bufs = ps.bufs;
   const uint32_t nw = gridDim.x * PASS_WARPS;
   uint32_t t = blockIdx.x * PASS_WARPS + warp;
   if (t < a.ntiles) stage_chunk(a, bufs, t, lane);
@@ -223,10 +245,10 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, con
     a.chunk_state[(unsigned long long)t * 32 + lane] = (uint8_t)entry;
     unsigned long long Dm, Fm, Rm;
     uint32_t fin;
-    if (nv == CHUNK) fin = chunk_masks<true>(smem, v, nv, laneoff, entry, Dm, Fm, Rm);
-    else fin = chunk_masks<false>(smem, v, nv, laneoff, entry, Dm, Fm, Rm);
+    if (nv == CHUNK) fin = chunk_masks<true>(ps.laneaddr, v, nv, entry, Dm, Fm, Rm);
+    else fin = chunk_masks<false>(ps.laneaddr, v, nv, entry, Dm, Fm, Rm);
     if (fin == INV_DEV && entry != INV_DEV && nv > 0) {
-      int p = first_inv_in_chunk(smem, a.in + cstart, nv, laneoff, entry);
+      int p = first_inv_in_chunk(ps.lut, a.in + cstart, nv, ps.laneoff, entry);
       if (p >= 0) atomicMax(&a.ctrl->inv_neg, ~(a.base + cstart + (unsigned)p));
     }
     unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;   // for k_emit
