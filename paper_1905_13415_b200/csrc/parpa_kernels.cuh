@@ -581,31 +581,30 @@ __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, u
   } else {
     int res = 2;
     const unsigned long long L = ld + 1 - fd;
-    // the field's first bytes as a register window: from the tile copy in shared memory, or — for
-    // the field that began in an earlier tile — from global memory with independent 4-byte loads
-    const uint32_t *w = nullptr;
-    uint32_t sh = 0;
+    // the field's first bytes as a register window from the tile copy in shared memory (a field that
+    // began in an earlier tile — at most field 0 of the tile — takes the byte-wise path below)
     const bool is_ts = TS && cd->type == T_TIMESTAMP;
-    if (L <= (is_ts ? 26ull : 16ull)) {
-      if (fd >= tbase) {
-        const uint32_t o = (uint32_t)(fd - tbase);
-        w = reinterpret_cast<const uint32_t *>(tb) + (o >> 2);
-        sh = (o & 3u) * 8u;
-      } else if (fd >= a.base && fd - a.base + 32 <= a.len) {
-        const unsigned long long o = fd - a.base;
-        w = reinterpret_cast<const uint32_t *>(a.in + (o & ~3ull));
-        sh = (uint32_t)(o & 3ull) * 8u;
-      }
-    }
-    if (w && is_ts) {
-      uint32_t x[7] = {0, 0, 0, 0, 0, 0, 0};
+    if (fd >= tbase && L <= (is_ts ? 26ull : 16ull)) {
+      const uint32_t o = (uint32_t)(fd - tbase), sh = (o & 3u) * 8u;
+      const uint32_t *w = reinterpret_cast<const uint32_t *>(tb) + (o >> 2);
+      const bool isf = cd->type == T_FLOAT64;
+      if (is_ts) {
+        uint32_t x[7] = {0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-      for (int k = 0; k < 7; k++) x[k] = __funnelshift_r(w[k], w[k + 1], sh);
-      res = conv_timestamp_words(x, (int)L, v);
-    } else if (w) {
-      const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
-      res = conv_window(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
-                        __funnelshift_r(w3, w4, sh), (uint32_t)L, cd->type == T_FLOAT64, v);
+        for (int k = 0; k < 7; k++) x[k] = __funnelshift_r(w[k], w[k + 1], sh);
+        res = conv_timestamp_words(x, (int)L, v);
+      } else if (L <= 4ull) {
+        res = conv_window4(__funnelshift_r(w[0], w[1], sh), (uint32_t)L, isf, v);
+      } else if (L <= 8ull) {
+        const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+        const unsigned long long x8 = (unsigned long long)__funnelshift_r(w0, w1, sh) |
+                                      ((unsigned long long)__funnelshift_r(w1, w2, sh) << 32);
+        res = conv_window8(x8, (uint32_t)L, isf, v);
+      } else {
+        const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
+        res = conv_window(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh), __funnelshift_r(w2, w3, sh),
+                          __funnelshift_r(w3, w4, sh), (uint32_t)L, isf, v);
+      }
     }
     if (res == 2) {
       TileSrc src{&a, tb, tbase, fd, ld, true};
@@ -673,13 +672,15 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   }
   // ---- E1a ----
   {
-    uint32_t k = (inc - mine) >> 16;
+    uint32_t k = (inc - mine) >> 16, jr = (inc - mine) & 0xFFFFu;
     const uint32_t base = (uint32_t)lane * CHUNK;
     unsigned long long fm = Fm;
     while (fm) {
       const int p = lsb64(fm);
       fm &= fm - 1ull;
-      ws->dlist[k++] = (uint16_t)((base + (uint32_t)p) | ((uint32_t)((Rm >> p) & 1ull) << 15));
+      const uint32_t pos = base + (uint32_t)p, isrec = (uint32_t)(Rm >> p) & 1u;
+      ws->dlist[k++] = (uint16_t)(pos | (isrec << 15));
+      if (isrec) ws->rows[jr++] = k | (pos << 16);       // end field index | record delimiter position
     }
     ws->dmask[2 * lane] = (uint32_t)Dm;
     ws->dmask[2 * lane + 1] = (uint32_t)(Dm >> 32);
@@ -690,9 +691,50 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     ws->kpre[2 * lane + 1] = (uint16_t)(kex + __popc((uint32_t)Km));
   }
   __syncwarp();
+  const uint32_t ktot = __shfl_sync(0xffffffffu, kinc, 31);    // CTRL bytes in the tile (warp-uniform)
+  const bool plain = ktot == 0u;
+  if (plain) {
+    // E1b' (no CTRL byte in the tile): field k is the byte range between delimiters k-1 and k, all DATA,
+    // so E2 reads it straight from the delimiter list.  Only field 0 (which may continue a field of an
+    // earlier tile) needs an entry; extra fields (column >= C) are counted per row.
+    const uint32_t c0 = prefix.col;
+    uint32_t extra = 0;
+    const uint32_t last_end = nrec ? (ws->rows[nrec - 1] & 0xFFFFu) : 0u;
+    const uint32_t nrows = nrec + (nf > last_end ? 1u : 0u);
+    for (uint32_t j = lane; j < nrows; j += 32) {
+      const uint32_t start = j ? (ws->rows[j - 1] & 0xFFFFu) : 0u, end = j < nrec ? (ws->rows[j] & 0xFFFFu) : nf;
+      const uint32_t cs = j ? 0u : c0, hi = cs + (end - start), lo = max(a.C, cs);
+      if (hi > lo) extra += hi - lo;
+    }
+    if (lane == 0 && nf) {
+      const uint32_t p = ws->dlist[0] & 0x7FFu;
+      unsigned long long cfd = prefix.fd, cld = prefix.ld;
+      uint32_t cfl = prefix.flags & (F_IC | F_PC | F_PRE);
+      open_combine(cfd, cld, cfl, p ? tbase_g : NONE, p ? tbase_g + p - 1u : NONE, 0u);
+      uint32_t e;
+      if (cfd == NONE) {
+        e = p;
+      } else {
+        const unsigned long long L = cld + 1 - cfd;
+        const long long rel = (long long)cfd - (long long)tbase_g;
+        const uint32_t icf = (cfl & F_IC) ? 0x80000000u : 0u;
+        if (rel >= 0 && L <= (unsigned long long)WT) {
+          e = (uint32_t)rel | ((uint32_t)L << 11) | icf;
+        } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
+          emit_field<TS>(a, cols, prefix.recs, c0, cfd, cld, cfl, tbase_g + p, cnt);
+          e = FIELD_WRITTEN;
+          if (c0 >= a.C) cnt.extra--;                           // emit_field counted it already
+        } else {
+          ws->f0 = make_uint2((uint32_t)(int32_t)rel, (uint32_t)L | icf);
+          e = FIELD_FAR;
+        }
+      }
+      ws->fields[0] = e;
+    }
+    cnt.extra += extra;
+  } else {
   // ---- E1b ----
   {
-    const uint32_t ktot = __shfl_sync(0xffffffffu, kinc, 31);  // CTRL bytes in the tile (warp-uniform)
     const uint32_t c0 = prefix.col;
     uint32_t jcarry = 0, extra = 0;
     int lastrec = -1;
@@ -769,12 +811,12 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
           }
         }
         ws->fields[k] = e;
-        if (isrec) ws->rows[jr] = (k + 1u) | (p << 16);
       }
       jcarry += (uint32_t)__popc(recm);
       if (recm) lastrec = (int)(kb + 31u - __clz(recm));
     }
     if (lane == 0) cnt.extra += extra;
+  }
   }
   __syncwarp();
   // ---- E2 ----
@@ -808,7 +850,13 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     const ColDesc *cd = cols + ci;
     const bool skip = cd->type == T_SKIP;
     if (k < end) {
-      const uint32_t e = ws->fields[k];
+      uint32_t e;
+      if (plain && k) {                                     // [x, p) between two delimiters, all DATA
+        const uint32_t x = (ws->dlist[k - 1] & 0x7FFu) + 1u, p = ws->dlist[k] & 0x7FFu;
+        e = x < p ? x | ((p - x) << 11) : p;
+      } else {
+        e = ws->fields[k];
+      }
       if (e == FIELD_WRITTEN || skip) continue;
       uint32_t len;
       unsigned long long off;

@@ -16,6 +16,7 @@
 #define __constant__
 static inline int __ffs(uint32_t x) { return __builtin_ffs(x); }
 static inline int __popc(uint32_t x) { return __builtin_popcount(x); }
+static inline int __ffsll(long long x) { return __builtin_ffsll(x); }
 static inline double __ddiv_rn(double a, double b) { return a / b; }
 static inline double __dmul_rn(double a, double b) { return a * b; }
 static inline double __fma_rn(double a, double b, double c) { return __builtin_fma(a, b, c); }
@@ -31,7 +32,7 @@ using std::max;
 int main(int argc, char **argv) {
   const long iters = argc > 1 ? atol(argv[1]) : 2000000;
   std::mt19937_64 r(12345);
-  long bad = 0, n = 0;
+  long bad = 0, n = 0, n8 = 0;
   const char *fixed[] = {"12.5", "1234.567", "123.4567", ".5", "5.", "-0.0", "+7", "-73.987654", "0.001", "100",
                          "9007199254740993", "1.2.3", "-", ".", "1e5", "1234567.12345678", "99999999999999.9",
                          "-.5", "+.", "0", "-0", "007", "1234", "12345", "123456789012345"};
@@ -51,7 +52,23 @@ int main(int argc, char **argv) {
     memcpy(x, buf, 16);
     for (int isf = 0; isf < 2; isf++) {
       long long out = 0;
-      const int res = parpa::conv_window(x[0], x[1], x[2], x[3], (uint32_t)f.size(), isf != 0, out);
+      int res = parpa::conv_window(x[0], x[1], x[2], x[3], (uint32_t)f.size(), isf != 0, out);
+      if (f.size() <= 8) {                         // the 8-character window must agree where both accept
+        unsigned long long x8;
+        memcpy(&x8, buf, 8);
+        long long out8 = 0;
+        const int res8 = parpa::conv_window8(x8, (uint32_t)f.size(), isf != 0, out8);
+        if (f.size() <= 4) {                       // and the 4-character one
+          uint32_t x4;
+          memcpy(&x4, buf, 4);
+          long long out4 = 0;
+          const int res4 = parpa::conv_window4(x4, (uint32_t)f.size(), isf != 0, out4);
+          if (res4 != res8 || (res4 == 1 && out4 != out8)) { if (bad < 10) printf("BAD4 '%s' isf=%d %d %d\n", buf, isf, res4, res8); bad++; }
+        }
+        if (res8 == 1 && res == 2) { res = 1; out = out8; n8++; }
+        else if (res8 == 1 && out8 != out) { if (bad < 10) printf("BAD8 '%s' isf=%d %lld %lld\n", buf, isf, out8, out); bad++; }
+        else if (res8 == 1) n8++;
+      }
       if (res == 2) continue;                      // deferred to the exact converters
       char *e;
       bool ok;
@@ -85,6 +102,6 @@ int main(int argc, char **argv) {
     }
     n++;
   }
-  printf("checked %ld fast-path conversions, %ld mismatches\n", n, bad);
+  printf("checked %ld fast-path conversions (%ld by the 8-character window), %ld mismatches\n", n, n8, bad);
   return bad != 0;
 }
