@@ -544,6 +544,7 @@ struct alignas(16) WarpScratch {
   uint32_t dmask[WT / 32], kmask[WT / 32];  // DATA / CTRL bits of the tile, 32 per word
   uint16_t kpre[WT / 32];                   // CTRL bits before each word
 };
+constexpr uint32_t E2_ROWS_MIN = 16;              // tiles with at least this many rows: column-uniform E2
 constexpr uint32_t FIELD_WRITTEN = 0xFFFFFFFFu;   // E1 already wrote this field
 constexpr uint32_t FIELD_FAR = 0xFFFFFFFEu;       // field 0 began before the tile: see WarpScratch::f0
 
@@ -617,6 +618,41 @@ __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, u
   }
   __stcs(reinterpret_cast<long long *>(cd->val) + row, v);
   __stcs(cd->valid + row, (uint8_t)ok);
+}
+
+// The common case of write_value, inline: a non-empty field inside the tile copy, without inner control
+// bytes, of at most 8 characters (26 for a timestamp), converted from a register window.  o = tile offset
+// of its first byte.  Everything else goes to write_value (empty / default, deferred, long fields).
+template <bool TS>
+__device__ __forceinline__ void write_value_tile(const KArgs &a, const ColDesc *cd, uint32_t type, uint32_t c,
+                                                 unsigned long long row, uint32_t o, uint32_t len, bool ic, bool far,
+                                                 unsigned long long off, const uint8_t *tb, unsigned long long tbase) {
+  long long v = 0;
+  int res = 2;
+  if (!(ic || far) && len - 1u < (TS && type == T_TIMESTAMP ? 26u : 8u)) {
+    const uint32_t sh = (o & 3u) * 8u;
+    const uint32_t *w = reinterpret_cast<const uint32_t *>(tb) + (o >> 2);
+    const bool isf = type == T_FLOAT64;
+    if (TS && type == T_TIMESTAMP) {
+      uint32_t x[7] = {0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int k = 0; k < 7; k++) x[k] = __funnelshift_r(w[k], w[k + 1], sh);
+      res = conv_timestamp_words(x, (int)len, v);
+    } else if (len <= 4u) {
+      res = conv_window4(__funnelshift_r(w[0], w[1], sh), len, isf, v);
+    } else {
+      const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+      const unsigned long long x8 = (unsigned long long)__funnelshift_r(w0, w1, sh) |
+                                    ((unsigned long long)__funnelshift_r(w1, w2, sh) << 32);
+      res = conv_window8(x8, len, isf, v);
+    }
+  }
+  if (res == 2) {
+    write_value<TS>(a, cd, c, row, off, off + len - 1, ic, len == 0, tb, tbase);
+    return;
+  }
+  __stcs(reinterpret_cast<long long *>(cd->val) + row, v);
+  __stcs(cd->valid + row, (uint8_t)res);
 }
 
 // (column c, tile row jr) -> the field index k in the warp's field list, or "missing" / "skip"
@@ -829,6 +865,74 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   }
   const uint32_t c0 = prefix.col;
   const unsigned long long r0 = prefix.recs;
+  if (nrows >= E2_ROWS_MIN) {
+    // Column-uniform writes (tiles with many short records, e.g. taxi / clf): lanes = tile rows, one
+    // column per step.  The row bookkeeping is done once per lane, the column descriptor and type are
+    // warp-uniform (no type divergence, span columns skip conversion as a whole warp), and each store
+    // covers consecutive rows of one column.
+    for (uint32_t jb = 0; jb < nrows; jb += 32) {
+      const uint32_t ji = jb + (uint32_t)lane;
+      const bool closed = ji < nrec;
+      uint32_t start = 0u, end = 0u, cs = 0u, dpos = 0u;
+      unsigned long long row = 0ull;
+      bool live = ji < nrows;
+      if (live) {
+        start = ji == 0 ? 0u : (ws->rows[ji - 1] & 0xFFFFu);
+        const uint32_t rw = closed ? ws->rows[ji] : 0u;
+        end = closed ? (rw & 0xFFFFu) : nf;
+        dpos = rw >> 16;
+        cs = ji == 0 ? c0 : 0u;
+        row = r0 + ji - a.row_base;
+        live = row < a.cap;
+      }
+      if (live && closed && end - start + cs < a.C) cnt.missing++;   // record closed with fewer fields
+      for (uint32_t c = 0; c < a.C; c++) {                     // warp-uniform
+        const ColDesc *cd = cols + c;
+        const uint32_t type = cd->type;
+        if (type == T_SKIP) continue;
+        if (!live || c < cs) continue;                        // c < cs: written by an earlier tile
+        const uint32_t k = start + (c - cs);
+        if (k < end) {
+          uint32_t e;
+          if (plain && k) {
+            const uint32_t x = (ws->dlist[k - 1] & 0x7FFu) + 1u, p = ws->dlist[k] & 0x7FFu;
+            e = x < p ? x | ((p - x) << 11) : p;
+          } else {
+            e = ws->fields[k];
+          }
+          if (e == FIELD_WRITTEN) continue;
+          uint32_t len, o;
+          unsigned long long off;
+          bool ic;
+          const bool far = e == FIELD_FAR;
+          if (far) {
+            const uint2 f = ws->f0;
+            off = tbase_g + (unsigned long long)(long long)(int32_t)f.x;
+            len = f.y & 0x7FFFFFFFu;
+            ic = (f.y >> 31) != 0;
+            o = 0u;
+          } else {
+            o = e & 0x7FFu;
+            off = tbase_g + o;
+            len = (e >> 11) & 0xFFFu;
+            ic = (e >> 31) != 0;
+          }
+          __stcs(cd->off + row, off);
+          __stcs(cd->len + row, len);
+          if (type != T_SPAN) write_value_tile<TS>(a, cd, type, c, row, o, len, ic, far, off, tb, tbase_g);
+        } else if (closed) {
+          __stcs(cd->off + row, tbase_g + dpos);
+          __stcs(cd->len + row, 0xFFFFFFFFu);
+          if (type != T_SPAN) {
+            __stcs(reinterpret_cast<long long *>(cd->val) + row, cd->has_def ? cd->def_bits : 0ll);
+            __stcs(cd->valid + row, (uint8_t)(cd->has_def ? 1 : 0));
+          }
+        }
+      }
+    }
+    __syncwarp();
+    return;
+  }
   // Column-major writes: (column, tile row) items flattened over the lanes, rows fastest, so a warp
   // step stores consecutive rows of one or two columns (coalesced) with every lane busy; numeric
   // columns share one converter, so mixed int / float steps do not diverge.
@@ -858,22 +962,25 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
         e = ws->fields[k];
       }
       if (e == FIELD_WRITTEN || skip) continue;
-      uint32_t len;
+      uint32_t len, o;
       unsigned long long off;
       bool ic;
-      if (e == FIELD_FAR) {
+      const bool far = e == FIELD_FAR;
+      if (far) {
         const uint2 f = ws->f0;
         off = tbase_g + (unsigned long long)(long long)(int32_t)f.x;
         len = f.y & 0x7FFFFFFFu;
         ic = (f.y >> 31) != 0;
+        o = 0u;
       } else {
-        off = tbase_g + (e & 0x7FFu);
+        o = e & 0x7FFu;
+        off = tbase_g + o;
         len = (e >> 11) & 0xFFFu;
         ic = (e >> 31) != 0;
       }
       __stcs(cd->off + row, off);
       __stcs(cd->len + row, len);
-      if (cd->type != T_SPAN) write_value<TS>(a, cd, ci, row, off, off + len - 1, ic, len == 0, tb, tbase_g);
+      if (cd->type != T_SPAN) write_value_tile<TS>(a, cd, cd->type, ci, row, o, len, ic, far, off, tb, tbase_g);
     } else if (ji < nrec) {                                 // record closed with fewer fields
       if (k == end) cnt.missing++;
       if (skip) continue;
