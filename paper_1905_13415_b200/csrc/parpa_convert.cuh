@@ -193,82 +193,88 @@ __device__ __forceinline__ int conv_window(uint32_t x0, uint32_t x1, uint32_t x2
   return 1;
 }
 
-// ---- eight-character window (the common case: every numeric field of the taxi / yelp / clf shapes) -----
-// x = the field's first 8 bytes (byte i = field byte i), 1 <= L <= 8.  The same grammar subset as
-// conv_window, in one 64-bit word: the sign becomes a leading '0', the '.' is squeezed out (the bytes after
-// it move down one place), the n remaining characters are checked to be digits in one carry-free test,
-// shifted up so that 8 - n zero digits lead, and folded pairwise (1+1, 2+2, 4+4 digits: three multiply-adds).
-// m < 10^8 is exact in a double; the float is m / 10^frac with frac <= 7 (div_pow10, correctly rounded).
-// Returns 1 valid, 2 "not handled here" (the byte-wise converters decide validity exactly).
-__device__ __forceinline__ int conv_window8(unsigned long long x, uint32_t L, bool isf, long long &out) {
-  const uint32_t c0 = (uint32_t)x & 0xFFu;
-  const bool neg = c0 == '-';
+// ---- four- / eight-character windows (the common case: every numeric field of the taxi / yelp / clf
+// shapes) ---------------------------------------------------------------------------------------------
+// x = the field's first 4 / 8 bytes (byte i = field byte i), 1 <= L <= 4 / 8.  The same grammar subset as
+// conv_window, in one 32- / 64-bit word: the sign becomes a leading '0', the '.' is squeezed out (the bytes
+// after it move down one place), the n remaining characters are checked to be digits in one carry-free
+// test, shifted up so that 4 - n / 8 - n zero digits lead, and folded pairwise (1+1, 2+2, 4+4 digits).
+// Split in two so that the kernels can parse with one lane per field and finish in the column-major
+// writes: parse -> packed (m | frac << 27 | neg << 30), m < 10^8 < 2^27, frac <= 7 digits after the '.'.
+// Returns 1 (parsed) or 2 ("not handled here": the byte-wise converters decide validity exactly).
+constexpr uint32_t PK_FRAC_SHIFT = 27, PK_NEG = 1u << 30, PK_SLOW = 1u << 31;
+__device__ __forceinline__ int parse_window4(uint32_t x, uint32_t L, bool isf, uint32_t &pk) {
+  const uint32_t c0 = x & 0xFFu;
   const uint32_t sgn = (c0 == '-' || c0 == '+') ? 1u : 0u;
-  const unsigned long long H = 0x8080808080808080ull, M7 = 0x7F7F7F7F7F7F7F7Full;
-  const unsigned long long vm = L >= 8u ? ~0ull : (1ull << (8u * L)) - 1ull;
-  unsigned long long d = (x ^ 0x3030303030303030ull) & vm;       // digits -> 0..9
-  if (sgn) d &= ~0xFFull;                                        // sign -> leading zero digit
-  const unsigned long long t = d ^ 0x1E1E1E1E1E1E1E1Eull;        // '.' (0x2E ^ 0x30) -> 0
-  const unsigned long long dotm = ~(((t & M7) + M7) | t) & H & vm;
+  const uint32_t vm = 0xFFFFFFFFu >> (32u - 8u * L);
+  uint32_t d = (x ^ 0x30303030u) & vm;
+  if (sgn) d &= 0xFFFFFF00u;                                     // sign -> leading zero digit
+  const uint32_t t = d ^ 0x1E1E1E1Eu;                            // '.' (0x2E ^ 0x30) -> 0
+  const uint32_t dotm = ~(((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & 0x80808080u & vm;
   uint32_t n = L, frac = 0;
   if (dotm) {
-    const uint32_t q = (uint32_t)(__ffsll((long long)dotm) - 1) >> 3;   // byte of the first '.'
-    const unsigned long long lo = (1ull << (8u * q)) - 1ull;
+    const uint32_t q = (uint32_t)(__ffs(dotm) - 1) >> 3;        // byte of the first '.'
+    const uint32_t lo = (1u << (8u * q)) - 1u;
     d = (d & lo) | ((d >> 8) & ~lo);                             // squeeze it out
     n = L - 1u;
     frac = n - q;
   }
-  const unsigned long long nm = n >= 8u ? ~0ull : (1ull << (8u * n)) - 1ull;
-  const unsigned long long bad = (((d & M7) + 0x7676767676767676ull) | d) & H & nm;
-  if (bad || n <= sgn || (dotm && !isf)) return 2;               // stray byte, 2nd '.', no digit, int '.'
-  d <<= 8u * (8u - n);                                           // right-align: 8 - n leading zeros
-  d = (d * 10u + (d >> 8)) & 0x00FF00FF00FF00FFull;
-  d = (d * 100u + (d >> 16)) & 0x0000FFFF0000FFFFull;
-  const uint32_t m = (uint32_t)((d * 10000u + (d >> 32)) & 0xFFFFFFFFull);
-  if (!isf) {
-    out = neg ? -(long long)m : (long long)m;
-    return 1;
-  }
-  double v = (double)m;
-  if (frac) v = div_pow10(v, frac);
-  if (neg) v = -v;
-  out = __double_as_longlong(v);
+  if (n <= sgn || (dotm && !isf)) return 2;                      // no digit, or '.' in an int64
+  const uint32_t nm = 0xFFFFFFFFu >> (32u - 8u * n);
+  if ((((d & 0x7F7F7F7Fu) + 0x76767676u) | d) & 0x80808080u & nm) return 2;   // stray byte / 2nd '.'
+  d <<= 8u * (4u - n);                                           // right-align: 4 - n leading zeros
+  d = (d * 10u + (d >> 8)) & 0x00FF00FFu;
+  const uint32_t m = (d & 0xFFFFu) * 100u + (d >> 16);
+  pk = m | (frac << PK_FRAC_SHIFT) | (c0 == '-' ? PK_NEG : 0u);
   return 1;
 }
-
-// The same for 1 <= L <= 4 in one 32-bit word (about half the instructions of the 64-bit form): most
-// numeric fields of the workloads (ids, counts, codes, short amounts) are at most four characters.
-__device__ __forceinline__ int conv_window4(uint32_t x, uint32_t L, bool isf, long long &out) {
-  const uint32_t c0 = x & 0xFFu;
-  const bool neg = c0 == '-';
+__device__ __forceinline__ int parse_window8(unsigned long long x, uint32_t L, bool isf, uint32_t &pk) {
+  const uint32_t c0 = (uint32_t)x & 0xFFu;
   const uint32_t sgn = (c0 == '-' || c0 == '+') ? 1u : 0u;
-  const uint32_t vm = 0xFFFFFFFFu >> (32u - 8u * L);
-  uint32_t d = (x ^ 0x30303030u) & vm;
-  if (sgn) d &= 0xFFFFFF00u;
-  const uint32_t t = d ^ 0x1E1E1E1Eu;
-  const uint32_t dotm = ~(((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & 0x80808080u & vm;
+  const unsigned long long H = 0x8080808080808080ull, M7 = 0x7F7F7F7F7F7F7F7Full;
+  const unsigned long long vm = L >= 8u ? ~0ull : (1ull << (8u * L)) - 1ull;
+  unsigned long long d = (x ^ 0x3030303030303030ull) & vm;
+  if (sgn) d &= ~0xFFull;
+  const unsigned long long t = d ^ 0x1E1E1E1E1E1E1E1Eull;
+  const unsigned long long dotm = ~(((t & M7) + M7) | t) & H & vm;
   uint32_t n = L, frac = 0;
   if (dotm) {
-    const uint32_t q = (uint32_t)(__ffs(dotm) - 1) >> 3;
-    const uint32_t lo = (1u << (8u * q)) - 1u;
+    const uint32_t q = (uint32_t)(__ffsll((long long)dotm) - 1) >> 3;
+    const unsigned long long lo = (1ull << (8u * q)) - 1ull;
     d = (d & lo) | ((d >> 8) & ~lo);
     n = L - 1u;
     frac = n - q;
   }
   if (n <= sgn || (dotm && !isf)) return 2;
-  const uint32_t nm = 0xFFFFFFFFu >> (32u - 8u * n);
-  if ((((d & 0x7F7F7F7Fu) + 0x76767676u) | d) & 0x80808080u & nm) return 2;
-  d <<= 8u * (4u - n);
-  d = (d * 10u + (d >> 8)) & 0x00FF00FFu;
-  const uint32_t m = (d & 0xFFFFu) * 100u + (d >> 16);
-  if (!isf) {
-    out = neg ? -(long long)m : (long long)m;
-    return 1;
-  }
+  const unsigned long long nm = n >= 8u ? ~0ull : (1ull << (8u * n)) - 1ull;
+  if ((((d & M7) + 0x7676767676767676ull) | d) & H & nm) return 2;
+  d <<= 8u * (8u - n);
+  d = (d * 10u + (d >> 8)) & 0x00FF00FF00FF00FFull;
+  d = (d * 100u + (d >> 16)) & 0x0000FFFF0000FFFFull;
+  const uint32_t m = (uint32_t)((d * 10000u + (d >> 32)) & 0xFFFFFFFFull);
+  pk = m | (frac << PK_FRAC_SHIFT) | (c0 == '-' ? PK_NEG : 0u);
+  return 1;
+}
+// packed -> int64 / float64 bits: the float is m / 10^frac, one correctly rounded division (div_pow10)
+__device__ __forceinline__ long long finish_window(uint32_t pk, bool isf) {
+  const uint32_t m = pk & ((1u << PK_FRAC_SHIFT) - 1u), frac = (pk >> PK_FRAC_SHIFT) & 7u;
+  const bool neg = (pk & PK_NEG) != 0;
+  if (!isf) return neg ? -(long long)m : (long long)m;
   double v = (double)m;
   if (frac) v = div_pow10(v, frac);
   if (neg) v = -v;
-  out = __double_as_longlong(v);
+  return __double_as_longlong(v);
+}
+__device__ __forceinline__ int conv_window4(uint32_t x, uint32_t L, bool isf, long long &out) {
+  uint32_t pk;
+  if (parse_window4(x, L, isf, pk) != 1) return 2;
+  out = finish_window(pk, isf);
+  return 1;
+}
+__device__ __forceinline__ int conv_window8(unsigned long long x, uint32_t L, bool isf, long long &out) {
+  uint32_t pk;
+  if (parse_window8(x, L, isf, pk) != 1) return 2;
+  out = finish_window(pk, isf);
   return 1;
 }
 
