@@ -710,13 +710,17 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   {
     uint32_t k = (inc - mine) >> 16, jr = (inc - mine) & 0xFFFFu;
     const uint32_t base = (uint32_t)lane * CHUNK;
-    unsigned long long fm = Fm;
-    while (fm) {
-      const int p = lsb64(fm);
-      fm &= fm - 1ull;
-      const uint32_t pos = base + (uint32_t)p, isrec = (uint32_t)(Rm >> p) & 1u;
-      ws->dlist[k++] = (uint16_t)(pos | (isrec << 15));
-      if (isrec) ws->rows[jr++] = k | (pos << 16);       // end field index | record delimiter position
+#pragma unroll
+    for (int h = 0; h < 2; h++) {                        // 32-bit halves: no 64-bit bit arithmetic per step
+      uint32_t fm = (uint32_t)(Fm >> (32 * h));
+      const uint32_t rm = (uint32_t)(Rm >> (32 * h)), hb = base + 32u * (uint32_t)h;
+      while (fm) {
+        const uint32_t p = (uint32_t)__ffs(fm) - 1u;
+        fm &= fm - 1u;
+        const uint32_t pos = hb + p, isrec = (rm >> p) & 1u;
+        ws->dlist[k++] = (uint16_t)(pos | (isrec << 15));
+        if (isrec) ws->rows[jr++] = k | (pos << 16);     // end field index | record delimiter position
+      }
     }
     ws->dmask[2 * lane] = (uint32_t)Dm;
     ws->dmask[2 * lane + 1] = (uint32_t)(Dm >> 32);
