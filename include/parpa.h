@@ -220,6 +220,27 @@ int parpa_compose_counts(const parpa_counts *a, const parpa_counts *b, parpa_cou
 int parpa_infer_columns(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, void *stream,
                         uint32_t *min_fields, uint32_t *max_fields, uint64_t *records);
 
+/* ---- type inference ("Type inference", reading R31) --------------- *
+ * parpa_infer_types — the type each of the first num_columns columns needs, from the device bytes
+ * alone ("threads identify the minimum numerical type being required to back their field value. A
+ * subsequent parallel reduction over the minimum type yields the inferred type of a column", P:571-572;
+ * extended to temporal types as P:574 allows).  Class of one field's DATA bytes (control bytes
+ * dropped): PARPA_CLASS_INT8 / _INT16 / _INT32 / _INT64 for an R14 integer by its range, _FLOAT64 for
+ * the R15 grammar (an integer beyond int64 included), _TIMESTAMP for a valid R29 datetime, else
+ * _STRING; empty and missing fields have no class.
+ *   class_masks  host uint32[num_columns]: OR over the column's fields of (1 << class)
+ *   types        host uint8[num_columns]: the resolved type — _EMPTY if no field has a class, _STRING
+ *                if any field is a string or timestamps mix with numbers, _TIMESTAMP if all are
+ *                timestamps, else the widest numeric class present
+ *   records      host, optional: R
+ * Parses the input with num_columns span columns (library-owned, freed before returning) and is
+ * synchronous on `stream`.  Errors: PARPA_EINVAL (null pointers, num_columns > 64), PARPA_ENOMEM;
+ * PARPA_EFORMAT / PARPA_EUNSUPPORTED as the parse reports them (outputs set). */
+enum { PARPA_CLASS_EMPTY = 0, PARPA_CLASS_INT8 = 1, PARPA_CLASS_INT16 = 2, PARPA_CLASS_INT32 = 3,
+       PARPA_CLASS_INT64 = 4, PARPA_CLASS_FLOAT64 = 5, PARPA_CLASS_TIMESTAMP = 6, PARPA_CLASS_STRING = 7 };
+int parpa_infer_types(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint32_t num_columns,
+                      void *stream, uint32_t *class_masks, uint8_t *types, uint64_t *records);
+
 /* ---- string materialisation (the paper's CSS) ------------------ *
  * For one column of a completed parse of the same device bytes (column->offset / ->length, device
  * arrays of `rows` entries): the DATA bytes of every field — control bytes such as the escaping

@@ -247,3 +247,48 @@ def conv_float64(s: bytes):
     v = ctypes.c_int64(0)
     ok = lib.oracle_conv_float64(_u8(a), len(s), ctypes.byref(v))
     return bool(ok), v.value if ok else 0
+
+
+# ---- type inference (reading R31) ------------------------------------------------
+CLASSES = ("empty", "int8", "int16", "int32", "int64", "float64", "timestamp", "string")
+
+
+def field_class(s: bytes) -> str:
+    """R31: the minimal type backing one field's DATA bytes ("the minimum numerical type being
+    required to back their field value"), extended to temporal types."""
+    if not s:
+        return "empty"
+    ok, v = conv_int64(s)
+    if ok:
+        for name, bits in (("int8", 8), ("int16", 16), ("int32", 32)):
+            if -(1 << (bits - 1)) <= v < (1 << (bits - 1)):
+                return name
+        return "int64"
+    if conv_float64(s)[0]:
+        return "float64"
+    if conv_timestamp(s)[0]:
+        return "timestamp"
+    return "string"
+
+
+def resolve_types(classes) -> str:
+    """P:572 "a subsequent parallel reduction over the minimum type yields the inferred type of a
+    column": the widest numeric class; timestamps only with timestamps; anything else a string."""
+    present = set(classes) - {"empty"}
+    if not present:
+        return "empty"
+    if "string" in present or ("timestamp" in present and len(present) > 1):
+        return "string"
+    if present == {"timestamp"}:
+        return "timestamp"
+    return max(present, key=CLASSES.index)
+
+
+def infer_types(dialect, data, C: int):
+    """Per column c < C: (type, set of field classes) from the sequential parse's DATA bytes."""
+    out = []
+    for c in range(C):
+        offs, buf = strings(dialect, data, C, c)
+        cls = {field_class(buf[offs[i]:offs[i + 1]]) for i in range(len(offs) - 1)}
+        out.append((resolve_types(cls), cls - {"empty"}))
+    return out

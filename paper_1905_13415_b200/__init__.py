@@ -397,6 +397,26 @@ def infer_columns(dfa: Dfa, data, stream=None):
     return int(r.value), int(mn.value), int(mx.value)
 
 
+CLASS_NAMES = ("empty", "int8", "int16", "int32", "int64", "float64", "timestamp", "string")
+
+
+def infer_types(dfa: Dfa, data, num_columns: int, stream=None):
+    """Type inference of the first ``num_columns`` columns (parpa_infer_types): returns
+    (types, class_masks, records) — types[c] a class name of CLASS_NAMES, class_masks[c] the OR of
+    1 << class over the column's fields."""
+    import numpy as np
+    L = _lib.load()
+    _check_input(data)
+    n = int(num_columns)
+    masks = np.zeros(max(n, 1), np.uint32)
+    types = np.zeros(max(n, 1), np.uint8)
+    r = ctypes.c_uint64(0)
+    _check(L.parpa_infer_types(dfa.handle, ctypes.c_void_p(data.data_ptr()), data.numel(), n, _stream_handle(stream),
+                               ctypes.c_void_p(masks.ctypes.data), ctypes.c_void_p(types.ctypes.data), ctypes.byref(r)),
+           "parpa_infer_types")
+    return [CLASS_NAMES[t] for t in types[:n]], [int(m) for m in masks[:n]], int(r.value)
+
+
 def strings(dfa: Dfa, data, column, rows: int, stream=None):
     """String materialisation of one parsed column (parpa_strings_size / _copy): returns
     (offsets int64[rows + 1], data uint8[total]) on the GPU — the DATA bytes of every field with

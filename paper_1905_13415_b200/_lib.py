@@ -53,7 +53,7 @@ EXPORTS = [
     "parpa_result_copy_column", "parpa_result_free", "parpa_plan_create", "parpa_plan_records", "parpa_plan_emit", "parpa_plan_destroy",
     "parpa_parse_into", "parpa_parse_host", "parpa_summarize", "parpa_count", "parpa_compose_tau",
     "parpa_compose_counts", "parpa_parse_range", "parpa_range_begin", "parpa_range_count", "parpa_range_emit",
-    "parpa_strings_size", "parpa_strings_copy", "parpa_infer_columns",
+    "parpa_strings_size", "parpa_strings_copy", "parpa_infer_columns", "parpa_infer_types",
     "parpa_debug_trace", "parpa_chunk_bytes", "parpa_tile_bytes",
     "parpa_set_profiling", "parpa_last_kernel_times", "parpa_status_string", "parpa_version",
     "parpa_last_error",
@@ -102,6 +102,7 @@ def load(build_if_missing: bool = True):
         lib.parpa_compose_counts.argtypes = [ctypes.POINTER(Counts_t), ctypes.POINTER(Counts_t),
                                              ctypes.POINTER(Counts_t)]
         lib.parpa_infer_columns.argtypes = [P, P, u64, P, ctypes.POINTER(u32), ctypes.POINTER(u32), ctypes.POINTER(u64)]
+        lib.parpa_infer_types.argtypes = [P, P, u64, u32, P, P, P, ctypes.POINTER(u64)]
         lib.parpa_strings_size.argtypes = [P, P, u64, ctypes.POINTER(Column_t), u64, P, ctypes.POINTER(u64), P]
         lib.parpa_strings_copy.argtypes = [P, P, u64, ctypes.POINTER(Column_t), u64, P, P, P]
         lib.parpa_range_begin.argtypes = [P, P, u64, u64, P, pp, ctypes.POINTER(Tau_t)]

@@ -1097,6 +1097,64 @@ int parpa_infer_columns(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t l
   return fi != NONE ? PARPA_EFORMAT : PARPA_OK;
 }
 
+// ---- type inference (reading R31) ---------------------------------------------
+static uint8_t resolve_class(uint32_t m) {
+  m &= ~1u;                                                   // empty fields carry no type
+  if (!m) return PARPA_CLASS_EMPTY;
+  if (m & (1u << PARPA_CLASS_STRING)) return PARPA_CLASS_STRING;
+  if (m & (1u << PARPA_CLASS_TIMESTAMP)) return m == (1u << PARPA_CLASS_TIMESTAMP) ? PARPA_CLASS_TIMESTAMP : PARPA_CLASS_STRING;
+  return (uint8_t)(31 - __builtin_clz(m));                     // the widest numeric class
+}
+
+int parpa_infer_types(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint32_t num_columns,
+                      void *stream, uint32_t *class_masks, uint8_t *types, uint64_t *records) {
+  if (!dfa || (len && !d_bytes) || (num_columns && (!class_masks || !types)) || num_columns > MAX_COLS)
+    return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  parpa_plan *p = nullptr;
+  int rc = parpa_plan_create(dfa, d_bytes, len, stream, &p);
+  if (rc) return rc;
+  const uint64_t R = p->records, Rc = std::max<uint64_t>(R, 1);
+  void *blk = nullptr;
+  unsigned int *d_mask = nullptr;
+  const size_t col_bytes = Rc * 12;
+  if (cudaMallocAsync(&blk, num_columns * col_bytes + 4 * (size_t)std::max(num_columns, 1u) + 16, s) != cudaSuccess)
+    rc = PARPA_ENOMEM;
+  std::vector<parpa_column> cols(num_columns);
+  std::vector<uint8_t> tspan(num_columns, PARPA_SPAN);
+  if (!rc) {
+    uint8_t *b = (uint8_t *)blk;
+    for (uint32_t c = 0; c < num_columns; c++) {
+      cols[c].offset = (uint64_t *)(b + c * col_bytes);
+      cols[c].length = (uint32_t *)(b + c * col_bytes + Rc * 8);
+      cols[c].value = nullptr;
+      cols[c].valid = nullptr;
+    }
+    d_mask = (unsigned int *)(b + num_columns * col_bytes);
+    if (cudaMemsetAsync(d_mask, 0, 4 * (size_t)std::max(num_columns, 1u), s) != cudaSuccess) rc = PARPA_ECUDA;
+  }
+  parpa_schema sch{num_columns, tspan.data(), nullptr, nullptr, 0};
+  if (!rc && num_columns) rc = parpa_plan_emit(p, &sch, cols.data(), nullptr, stream);   // spans of every column
+  DevCfg *dc = nullptr;
+  if (!rc && R) rc = dev_cfg(&dc);
+  for (uint32_t c = 0; !rc && R && c < num_columns; c++) {
+    k_field_class<<<dc->sms * 8, 256, 0, s>>>(p->a, (const unsigned long long *)cols[c].offset, cols[c].length, R,
+                                              d_mask + c);
+    if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
+  }
+  parpa_stats st{};
+  if (!rc && num_columns && cudaMemcpyAsync(class_masks, d_mask, 4 * num_columns, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+    rc = PARPA_ECUDA;
+  if (!rc && cudaMemcpyAsync(&st, p->w.stats, sizeof(st), cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = PARPA_ECUDA;
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
+  if (blk) cudaFreeAsync(blk, s);
+  parpa_plan_destroy(p);
+  if (rc) return rc;
+  for (uint32_t c = 0; c < num_columns; c++) types[c] = resolve_class(class_masks[c]);
+  if (records) *records = R;
+  return st.status == PARPA_EFORMAT || st.status == PARPA_EUNSUPPORTED ? st.status : PARPA_OK;
+}
+
 // ---- string materialisation ---------------------------------------------------------------
 static int strings_impl(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, const parpa_column *col,
                         uint64_t rows, int64_t *d_offsets, uint64_t *total, uint8_t *d_data, cudaStream_t s) {

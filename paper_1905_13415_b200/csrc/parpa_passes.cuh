@@ -560,3 +560,80 @@ __global__ void k_infer_cols(const KArgs a, unsigned int *minmax) {
   }
 }
 }  // namespace parpa
+
+// ---- type inference (reading R31) -------------------------------------------
+// "threads identify the minimum numerical type being required to back their field value.  A subsequent
+// parallel reduction over the minimum type yields the inferred type of a column", extended to
+// temporal types as P:574 suggests.  Class of one field's DATA bytes: INT8 / INT16 / INT32 / INT64 by the
+// range of an R14 integer, FLOAT64 for the R15 grammar (incl. integers beyond int64), TIMESTAMP for a valid
+// R29 datetime, else STRING; empty / missing fields have no class.  The reduction is a bitwise OR of
+// 1 << class (associative and commutative), resolved on the host (parpa_infer_types).
+namespace parpa {
+enum { TC_EMPTY = 0, TC_INT8 = 1, TC_INT16 = 2, TC_INT32 = 3, TC_INT64 = 4, TC_FLOAT64 = 5, TC_TIMESTAMP = 6,
+       TC_STRING = 7 };
+
+struct DataSrc {                       // the DATA bytes of the raw span [pos, end) (control bytes dropped)
+  const KArgs *a;
+  unsigned long long pos, end;
+  bool all;                            // the span holds no control byte
+  __device__ __forceinline__ bool next(uint8_t &c) {
+    while (pos < end) {
+      const unsigned long long p = pos++;
+      if (all || ((dmask_of_chunk(*a, p >> 6) >> (p & 63)) & 1ull)) {
+        c = a->in[p];
+        return true;
+      }
+    }
+    return false;
+  }
+};
+
+template <class Src>
+__device__ uint32_t field_class(const Src &src) {
+  Src s = src;
+  uint8_t c;
+  if (!s.next(c)) return TC_EMPTY;
+  bool neg = false, isint = true, over = false;
+  if (c == '+' || c == '-') {
+    neg = c == '-';
+    if (!s.next(c)) isint = false;
+  }
+  unsigned long long acc = 0;
+  const unsigned long long lim = neg ? 0x8000000000000000ull : 0x7FFFFFFFFFFFFFFFull;
+  while (isint) {
+    const unsigned d = (unsigned)c - '0';
+    if (d > 9u) { isint = false; break; }
+    if (!over) {
+      if (acc > (lim - d) / 10ull) over = true;
+      else acc = acc * 10ull + d;
+    }
+    if (!s.next(c)) break;
+  }
+  if (isint) {
+    if (over) return TC_FLOAT64;                     // a digit string beyond int64: the float grammar
+    const unsigned long long m = neg ? acc - (acc ? 1ull : 0ull) : acc;   // |v| - 1 for negatives
+    return m <= 0x7Full ? TC_INT8 : m <= 0x7FFFull ? TC_INT16 : m <= 0x7FFFFFFFull ? TC_INT32 : TC_INT64;
+  }
+  long long v;
+  Src f = src;
+  if (conv_float64_fast(f, v) != 0) return TC_FLOAT64;   // 0 = not the R15 grammar
+  Src t = src;
+  if (conv_timestamp(t, v) == 1) return TC_TIMESTAMP;
+  return TC_STRING;
+}
+
+__global__ void k_field_class(const KArgs a, const unsigned long long *off, const uint32_t *len,
+                              unsigned long long rows, unsigned int *mask) {
+  unsigned int m = 0;
+  for (unsigned long long r = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; r < rows;
+       r += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t L = len[r];
+    if (L == MISSING_LEN_DEV || L == 0) continue;
+    const unsigned long long p0 = off[r] - a.base;
+    const DataSrc src{&a, p0, p0 + L, data_bytes_in(a, p0, L) == L};
+    m |= 1u << field_class(src);
+  }
+  m = __reduce_or_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicOr(mask, m);
+}
+}  // namespace parpa

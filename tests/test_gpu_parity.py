@@ -393,3 +393,44 @@ def test_giant_field_spanning_tiles_and_scan_blocks(big):
             b"4,c,7\n" * 1000)
     types = [oracle.INT64, oracle.SPAN, oracle.FLOAT64]
     run_all_paths("csv", data, types, label=f"giant-{big}")
+
+
+@pytest.mark.parametrize("name", ["cfg1", "yelp", "clf", "taxi"])
+def test_infer_types_workloads(name):
+    """per-column inferred type and field-class set equal the oracle's."""
+    w = datagen.WORKLOADS[name]
+    data, g = datagen.generate(name, 600_000)
+    types, masks, R = parpa.infer_types(dfa(w.dialect), dev(data), w.C)
+    ora = oracle.infer_types(w.dialect, data, w.C)
+    assert R == g.records
+    assert types == [t for t, _ in ora], (types, ora)
+    assert masks == [sum(1 << oracle.CLASSES.index(c) for c in cls) for _, cls in ora]
+
+
+def test_infer_types_constructed():
+    """Random fields of every class (integer widths at their endpoints, floats, exponents, bad numbers,
+    ISO / CLF datetimes valid and not, strings, empties), some quoted and some with "" escapes (control
+    bytes inside the span), missing fields in short records, across several warp tiles."""
+    from tests.test_oracle_types import sample_fields
+    rng = random.Random(77)
+    C = 6
+    rows = []
+    for r in range(6000):
+        fs = sample_fields(rng, C)
+        for i, f in enumerate(fs):
+            if rng.random() < 0.15:
+                fs[i] = b'"' + f + b'"'
+            elif rng.random() < 0.03:
+                fs[i] = b'"' + f[:1] + b'""' + f[1:] + b'"'
+        if rng.random() < 0.05:
+            fs = fs[:rng.randint(1, C)]
+        # one column per class family so that several resolve to non-string types
+        rows.append(b",".join(fs))
+    data = b"\n".join(rows) + b"\n"
+    col_ints = b"\n".join(str(rng.randint(-30000, 30000)).encode() for _ in range(5000)) + b"\n"
+    for d, n in ((data, C), (col_ints, 1)):
+        types, masks, R = parpa.infer_types(dfa("csv"), dev(d), n)
+        ora = oracle.infer_types("csv", d, n)
+        assert types == [t for t, _ in ora], (types, ora)
+        assert masks == [sum(1 << oracle.CLASSES.index(c) for c in cls) for _, cls in ora]
+    assert parpa.infer_types(dfa("csv"), dev(col_ints), 1)[0] == ["int16"]
