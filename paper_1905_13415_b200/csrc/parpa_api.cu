@@ -1117,7 +1117,7 @@ int parpa_infer_types(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len
   const uint64_t R = p->records, Rc = std::max<uint64_t>(R, 1);
   void *blk = nullptr;
   unsigned int *d_mask = nullptr;
-  const size_t col_bytes = Rc * 12;
+  const size_t len_off = (Rc * 8 + 255) / 256 * 256, col_bytes = (len_off + Rc * 4 + 255) / 256 * 256;
   if (cudaMallocAsync(&blk, num_columns * col_bytes + 4 * (size_t)std::max(num_columns, 1u) + 16, s) != cudaSuccess)
     rc = PARPA_ENOMEM;
   std::vector<parpa_column> cols(num_columns);
@@ -1126,7 +1126,7 @@ int parpa_infer_types(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len
     uint8_t *b = (uint8_t *)blk;
     for (uint32_t c = 0; c < num_columns; c++) {
       cols[c].offset = (uint64_t *)(b + c * col_bytes);
-      cols[c].length = (uint32_t *)(b + c * col_bytes + Rc * 8);
+      cols[c].length = (uint32_t *)(b + c * col_bytes + len_off);
       cols[c].value = nullptr;
       cols[c].valid = nullptr;
     }
