@@ -19,6 +19,16 @@
 
 namespace parpa {
 
+// column stores of the emission kernels (streaming by default; PARPA_COL_STORE_WB: write-back)
+template <class T>
+__device__ __forceinline__ void st_col(T *p, T v) {
+#ifdef PARPA_COL_STORE_WB
+  *p = v;
+#else
+  __stcs(p, v);
+#endif
+}
+
 enum { MODE_TAU = 0, MODE_COUNT = 1, MODE_EMIT = 2 };
 enum { T_SPAN = 0, T_INT64 = 1, T_FLOAT64 = 2, T_TIMESTAMP = 3, T_SKIP = 4 };   // T_SKIP: internal
 // TS = the schema has timestamp columns: the emission kernels are instantiated with and without
@@ -430,8 +440,8 @@ __device__ void emit_field(const KArgs &a, const ColDesc *cols, unsigned long lo
     if (L >= 0xFFFFFFFFull) { cnt.unsupported = 1; L = 0xFFFFFFFEull; }
     len = (uint32_t)L;
   }
-  __stcs(cd->off + row, off);
-  __stcs(cd->len + row, len);
+  st_col(cd->off + row, off);
+  st_col(cd->len + row, len);
   uint32_t type = cd->type;
   if (type == T_SPAN) return;
   long long v = 0;
@@ -544,7 +554,10 @@ struct alignas(16) WarpScratch {
   uint32_t dmask[WT / 32], kmask[WT / 32];  // DATA / CTRL bits of the tile, 32 per word
   uint16_t kpre[WT / 32];                   // CTRL bits before each word
 };
-constexpr uint32_t E2_ROWS_MIN = 16;              // tiles with at least this many rows: column-uniform E2
+#ifndef PARPA_E2_ROWS_MIN
+#define PARPA_E2_ROWS_MIN 16
+#endif
+constexpr uint32_t E2_ROWS_MIN = PARPA_E2_ROWS_MIN;  // tiles with at least this many rows: column-uniform E2
 constexpr uint32_t FIELD_WRITTEN = 0xFFFFFFFFu;   // E1 already wrote this field
 constexpr uint32_t FIELD_FAR = 0xFFFFFFFEu;       // field 0 began before the tile: see WarpScratch::f0
 
@@ -616,8 +629,8 @@ __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, u
     ok = res;
     if (!ok) v = 0;
   }
-  __stcs(reinterpret_cast<long long *>(cd->val) + row, v);
-  __stcs(cd->valid + row, (uint8_t)ok);
+  st_col(reinterpret_cast<long long *>(cd->val) + row, v);
+  st_col(cd->valid + row, (uint8_t)ok);
 }
 
 // The common case of write_value, inline: a non-empty field inside the tile copy, without inner control
@@ -651,8 +664,8 @@ __device__ __forceinline__ void write_value_tile(const KArgs &a, const ColDesc *
     write_value<TS>(a, cd, c, row, off, off + len - 1, ic, len == 0, tb, tbase);
     return;
   }
-  __stcs(reinterpret_cast<long long *>(cd->val) + row, v);
-  __stcs(cd->valid + row, (uint8_t)res);
+  st_col(reinterpret_cast<long long *>(cd->val) + row, v);
+  st_col(cd->valid + row, (uint8_t)res);
 }
 
 // (column c, tile row jr) -> the field index k in the warp's field list, or "missing" / "skip"
@@ -921,15 +934,15 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
             len = (e >> 11) & 0xFFFu;
             ic = (e >> 31) != 0;
           }
-          __stcs(cd->off + row, off);
-          __stcs(cd->len + row, len);
+          st_col(cd->off + row, off);
+          st_col(cd->len + row, len);
           if (type != T_SPAN) write_value_tile<TS>(a, cd, type, c, row, o, len, ic, far, off, tb, tbase_g);
         } else if (closed) {
-          __stcs(cd->off + row, tbase_g + dpos);
-          __stcs(cd->len + row, 0xFFFFFFFFu);
+          st_col(cd->off + row, tbase_g + dpos);
+          st_col(cd->len + row, 0xFFFFFFFFu);
           if (type != T_SPAN) {
-            __stcs(reinterpret_cast<long long *>(cd->val) + row, cd->has_def ? cd->def_bits : 0ll);
-            __stcs(cd->valid + row, (uint8_t)(cd->has_def ? 1 : 0));
+            st_col(reinterpret_cast<long long *>(cd->val) + row, cd->has_def ? cd->def_bits : 0ll);
+            st_col(cd->valid + row, (uint8_t)(cd->has_def ? 1 : 0));
           }
         }
       }
@@ -982,17 +995,17 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
         len = (e >> 11) & 0xFFFu;
         ic = (e >> 31) != 0;
       }
-      __stcs(cd->off + row, off);
-      __stcs(cd->len + row, len);
+      st_col(cd->off + row, off);
+      st_col(cd->len + row, len);
       if (cd->type != T_SPAN) write_value_tile<TS>(a, cd, cd->type, ci, row, o, len, ic, far, off, tb, tbase_g);
     } else if (ji < nrec) {                                 // record closed with fewer fields
       if (k == end) cnt.missing++;
       if (skip) continue;
-      __stcs(cd->off + row, tbase_g + (ws->rows[ji] >> 16));
-      __stcs(cd->len + row, 0xFFFFFFFFu);
+      st_col(cd->off + row, tbase_g + (ws->rows[ji] >> 16));
+      st_col(cd->len + row, 0xFFFFFFFFu);
       if (cd->type != T_SPAN) {
-        __stcs(reinterpret_cast<long long *>(cd->val) + row, cd->has_def ? cd->def_bits : 0ll);
-        __stcs(cd->valid + row, (uint8_t)(cd->has_def ? 1 : 0));
+        st_col(reinterpret_cast<long long *>(cd->val) + row, cd->has_def ? cd->def_bits : 0ll);
+        st_col(cd->valid + row, (uint8_t)(cd->has_def ? 1 : 0));
       }
     }
   }
@@ -1019,7 +1032,8 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 2) k_emit(const KArgs a, cons
   EmitCounters cnt{0ull, 0ull, 0u};
   __syncthreads();
   const uint32_t gw = blockIdx.x * EMIT_WARPS + warp, nw = gridDim.x * EMIT_WARPS;
-  for (uint32_t t = gw; t < a.ntiles; t += nw) {
+  for (uint32_t t = gw; t < a.ntiles; t += nw) {        // grid stride: adjacent tiles in flight together
+                                                        // (measured faster than contiguous runs per warp)
     const unsigned long long tstart = (unsigned long long)t * WT;
     const unsigned long long cstart = tstart + (unsigned long long)lane * CHUNK;
     const int nvalid = cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
