@@ -1042,6 +1042,11 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, 2) k_emit(const KArgs a, cons
       load_chunk(a.in + cstart, nvalid, v);
       stash_chunk(ws->bytes, lane, v);
     }
+    if (t + nw < a.ntiles) {                              // the warp's next tile into L2 (2 KB + 768 B masks):
+      const unsigned long long tn = (unsigned long long)(t + nw);   // its loads then wait on L2, not DRAM
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in + tn * WT + (unsigned long long)lane * CHUNK));
+      if (lane < 6) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.masks + tn * 96 + lane * 16));
+    }
     const unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;
     const unsigned long long Dm = mk[0], Fm = mk[32], Rm = mk[64];
     const unsigned long long Vm = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull);
