@@ -558,6 +558,10 @@ struct alignas(16) WarpScratch {
 #define PARPA_E2_ROWS_MIN 16
 #endif
 constexpr uint32_t E2_ROWS_MIN = PARPA_E2_ROWS_MIN;  // tiles with at least this many rows: column-uniform E2
+#ifndef PARPA_E1A_SELECT_MAX
+#define PARPA_E1A_SELECT_MAX 32
+#endif
+constexpr uint32_t E1A_SELECT_MAX = PARPA_E1A_SELECT_MAX;   // tiles with at most this many delimiters: select
 constexpr uint32_t FIELD_WRITTEN = 0xFFFFFFFFu;   // E1 already wrote this field
 constexpr uint32_t FIELD_FAR = 0xFFFFFFFEu;       // field 0 began before the tile: see WarpScratch::f0
 
@@ -720,7 +724,40 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     return;
   }
   // ---- E1a ----
-  {
+  if (nf <= E1A_SELECT_MAX) {
+    // few delimiters (long fields, e.g. yelp text): lane k selects the k-th delimiter of the tile — the
+    // owning chunk by a shuffle binary search over the lanes' exclusive counts, the bit by a popcount
+    // binary search — instead of every lane walking its own mask with most lanes idle.
+    const uint32_t ex = (inc - mine) >> 16;
+    const uint32_t flo = (uint32_t)Fm, fhi = (uint32_t)(Fm >> 32), rlo = (uint32_t)Rm, rhi = (uint32_t)(Rm >> 32);
+    const unsigned lt = (1u << lane) - 1u;
+    uint32_t jb = 0;
+    for (uint32_t kb = 0; kb < nf; kb += 32) {
+      const uint32_t k = kb + (uint32_t)lane;
+      uint32_t o = 0;
+#pragma unroll
+      for (uint32_t st = 16; st; st >>= 1)
+        if (__shfl_sync(0xffffffffu, ex, o + st) <= k) o += st;
+      const uint32_t r = k - __shfl_sync(0xffffffffu, ex, o);
+      const uint32_t ol = __shfl_sync(0xffffffffu, flo, o), oh = __shfl_sync(0xffffffffu, fhi, o);
+      const uint32_t rl = __shfl_sync(0xffffffffu, rlo, o), rh = __shfl_sync(0xffffffffu, rhi, o);
+      const uint32_t cl = (uint32_t)__popc(ol);
+      const bool upper = r >= cl;
+      uint32_t word = upper ? oh : ol, rr = upper ? r - cl : r, q = 0;
+#pragma unroll
+      for (uint32_t sh = 16; sh; sh >>= 1) {
+        const uint32_t c = (uint32_t)__popc(word & ((1u << sh) - 1u));
+        if (rr >= c) { rr -= c; word >>= sh; q += sh; }
+      }
+      const bool act = k < nf;
+      const uint32_t pos = o * CHUNK + (upper ? 32u : 0u) + q;
+      const uint32_t isrec = act ? (((upper ? rh : rl) >> q) & 1u) : 0u;
+      const unsigned recm = __ballot_sync(0xffffffffu, isrec != 0u);
+      if (act) ws->dlist[k] = (uint16_t)(pos | (isrec << 15));
+      if (isrec) ws->rows[jb + (uint32_t)__popc(recm & lt)] = (k + 1u) | (pos << 16);
+      jb += (uint32_t)__popc(recm);
+    }
+  } else {
     uint32_t k = (inc - mine) >> 16, jr = (inc - mine) & 0xFFFFu;
     const uint32_t base = (uint32_t)lane * CHUNK;
 #pragma unroll
@@ -735,6 +772,8 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
         if (isrec) ws->rows[jr++] = k | (pos << 16);     // end field index | record delimiter position
       }
     }
+  }
+  {
     ws->dmask[2 * lane] = (uint32_t)Dm;
     ws->dmask[2 * lane + 1] = (uint32_t)(Dm >> 32);
     ws->kmask[2 * lane] = (uint32_t)Km;
@@ -1017,13 +1056,17 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
 namespace parpa {
 
 // ---- two-phase emit kernel (per warp tile, from the stored prefixes; no look-back) ------------------
-constexpr int EMIT_WARPS = 16;
+#ifndef PARPA_EMIT_WARPS
+#define PARPA_EMIT_WARPS 16
+#define PARPA_EMIT_MINB 2
+#endif
+constexpr int EMIT_WARPS = PARPA_EMIT_WARPS;
 constexpr size_t EMIT_SMEM = EMIT_WARPS * sizeof(WarpScratch);
 
 // S6+S7 per warp tile from what the scan half stored: the DATA / DELIM / RECORD masks of every chunk
 // (k_pass2) and the tile prefix (k_seg_scan).  No LUT, no re-simulation: 2 CTAs per SM.
 template <bool TS>
-__global__ void __launch_bounds__(EMIT_WARPS * 32, 2) k_emit(const KArgs a, const ColsK colsk) {
+__global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const KArgs a, const ColsK colsk) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ ColDesc s_cols[MAX_COLS];
   for (int c = threadIdx.x; c < (int)a.C; c += blockDim.x) s_cols[c] = colsk.c[c];
