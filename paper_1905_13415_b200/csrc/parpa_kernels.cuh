@@ -558,10 +558,7 @@ struct alignas(16) WarpScratch {
 #define PARPA_E2_ROWS_MIN 16
 #endif
 constexpr uint32_t E2_ROWS_MIN = PARPA_E2_ROWS_MIN;  // tiles with at least this many rows: column-uniform E2
-#ifndef PARPA_E1A_SELECT_MAX
-#define PARPA_E1A_SELECT_MAX 32
-#endif
-constexpr uint32_t E1A_SELECT_MAX = PARPA_E1A_SELECT_MAX;   // tiles with at most this many delimiters: select
+constexpr uint32_t E1A_SELECT_MAX = 32;              // tiles with at most this many delimiters: one select round
 constexpr uint32_t FIELD_WRITTEN = 0xFFFFFFFFu;   // E1 already wrote this field
 constexpr uint32_t FIELD_FAR = 0xFFFFFFFEu;       // field 0 began before the tile: see WarpScratch::f0
 
@@ -731,9 +728,8 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     const uint32_t ex = (inc - mine) >> 16;
     const uint32_t flo = (uint32_t)Fm, fhi = (uint32_t)(Fm >> 32), rlo = (uint32_t)Rm, rhi = (uint32_t)(Rm >> 32);
     const unsigned lt = (1u << lane) - 1u;
-    uint32_t jb = 0;
-    for (uint32_t kb = 0; kb < nf; kb += 32) {
-      const uint32_t k = kb + (uint32_t)lane;
+    {
+      const uint32_t k = (uint32_t)lane;
       uint32_t o = 0;
 #pragma unroll
       for (uint32_t st = 16; st; st >>= 1)
@@ -754,8 +750,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
       const uint32_t isrec = act ? (((upper ? rh : rl) >> q) & 1u) : 0u;
       const unsigned recm = __ballot_sync(0xffffffffu, isrec != 0u);
       if (act) ws->dlist[k] = (uint16_t)(pos | (isrec << 15));
-      if (isrec) ws->rows[jb + (uint32_t)__popc(recm & lt)] = (k + 1u) | (pos << 16);
-      jb += (uint32_t)__popc(recm);
+      if (isrec) ws->rows[__popc(recm & lt)] = (k + 1u) | (pos << 16);
     }
   } else {
     uint32_t k = (inc - mine) >> 16, jr = (inc - mine) & 0xFFFFu;
