@@ -10,6 +10,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/parpa.h"
@@ -276,6 +277,28 @@ int set_columns(const parpa_schema *sch, const parpa_column *cols, uint32_t C, C
   return PARPA_OK;
 }
 
+// Launch with programmatic stream serialisation (PDL, see PdlTrigger): the kernel may start its prologue
+// while its stream predecessor drains.  PARPA_NO_PDL=1 in the environment launches normally (A/B).
+static bool pdl_enabled() {
+  static const bool on = !(getenv("PARPA_NO_PDL") && getenv("PARPA_NO_PDL")[0] == '1');
+  return on;
+}
+template <typename... P, typename... A>
+cudaError_t launch_k(void (*k)(P...), unsigned grid, unsigned block, size_t smem, cudaStream_t s, bool pdl,
+                     A &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl && pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+
 int grid_for(int occ, int sms, uint32_t ntiles, int warps_per_cta) {
   long long g = (long long)std::max(occ, 1) * sms;
   long long need = ((long long)ntiles + warps_per_cta - 1) / warps_per_cta;
@@ -293,12 +316,12 @@ int launch_passes(int mode, const KArgs &a, const DfaK &k, cudaStream_t s, uint3
   const uint32_t nblk = (a.ntiles + SCAN_TILE - 1) / SCAN_TILE;
   {
     Launch L(s, "k_pass1");
-    k_pass1<<<grid_for(dc->occ_pass1, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, PASS_SMEM, s>>>(a, k);
+    CK(launch_k(k_pass1, grid_for(dc->occ_pass1, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, PASS_SMEM, s, false, a, k));
   }
   CK(cudaGetLastError());
   {
     Launch L(s, "k_tau_scan");
-    k_tau_scan<<<nblk, SCAN_THREADS, 0, s>>>(a);
+    CK(launch_k(k_tau_scan, nblk, SCAN_THREADS, 0, s, true, a));
   }
   CK(cudaGetLastError());
   if (launches) *launches += 2;
@@ -313,12 +336,12 @@ int launch_half2(const KArgs &a, const DfaK &k, cudaStream_t s, uint32_t *launch
   const uint32_t nblk = (a.ntiles + SCAN_TILE - 1) / SCAN_TILE;
   {
     Launch L(s, "k_pass2");
-    k_pass2<<<grid_for(dc->occ_pass2, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, PASS_SMEM, s>>>(a, k);
+    CK(launch_k(k_pass2, grid_for(dc->occ_pass2, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, PASS_SMEM, s, true, a, k));
   }
   CK(cudaGetLastError());
   {
     Launch L(s, "k_seg_scan");
-    k_seg_scan<<<nblk, SCAN_THREADS, 0, s>>>(a);
+    CK(launch_k(k_seg_scan, nblk, SCAN_THREADS, 0, s, true, a));
   }
   CK(cudaGetLastError());
   if (launches) *launches += 2;
@@ -339,9 +362,9 @@ int launch_emit(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, 
   {
     Launch L(s, "k_emit");
     if (has_timestamps(a, ck))
-      k_emit<true><<<grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s>>>(a, ck);
+      CK(launch_k(k_emit<true>, grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s, true, a, ck));
     else
-      k_emit<false><<<grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s>>>(a, ck);
+      CK(launch_k(k_emit<false>, grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s, true, a, ck));
   }
   CK(cudaGetLastError());
   if (launches) (*launches)++;
@@ -354,13 +377,13 @@ int launch_tail(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, 
   if (rc) return rc;
   {
     Launch L(s, "k_finalize");
-    k_finalize<<<1, 32, 0, s>>>(a, k, ck);
+    CK(launch_k(k_finalize, 1, 32, 0, s, a.ntiles != 0, a, k, ck));
   }
   CK(cudaGetLastError());
   {
     Launch L(s, "k_deferred");
-    if (has_timestamps(a, ck)) k_deferred<true><<<dc->sms * 2, 128, 0, s>>>(a, k, ck);
-    else k_deferred<false><<<dc->sms * 2, 128, 0, s>>>(a, k, ck);
+    if (has_timestamps(a, ck)) CK(launch_k(k_deferred<true>, dc->sms * 2, 128, 0, s, true, a, k, ck));
+    else CK(launch_k(k_deferred<false>, dc->sms * 2, 128, 0, s, true, a, k, ck));
   }
   CK(cudaGetLastError());
   if (launches) *launches += 2;

@@ -230,6 +230,17 @@ __device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Programmatic dependent launch (the parse's kernels after the first are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel runs its prologue (LUT build, descriptor
+// copies) while its predecessor drains, then waits for the predecessor's completion and memory before
+// touching its outputs.  Every CTA signals its dependents only when it leaves (PdlTrigger), so a
+// dependent grid never takes SM resources from unfinished CTAs of its predecessor (the ticket-ordered
+// look-back scans need every block to get an SM).  Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+struct PdlTrigger {
+  __device__ __forceinline__ ~PdlTrigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+};
+
 }  // namespace parpa
 
 namespace parpa {

@@ -1064,11 +1064,13 @@ template <bool TS>
 __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const KArgs a, const ColsK colsk) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ ColDesc s_cols[MAX_COLS];
+  PdlTrigger pdl_trigger;
   for (int c = threadIdx.x; c < (int)a.C; c += blockDim.x) s_cols[c] = colsk.c[c];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpScratch *ws = reinterpret_cast<WarpScratch *>(smem) + warp;
   EmitCounters cnt{0ull, 0ull, 0u};
   __syncthreads();
+  pdl_wait();
   const uint32_t gw = blockIdx.x * EMIT_WARPS + warp, nw = gridDim.x * EMIT_WARPS;
   for (uint32_t t = gw; t < a.ntiles; t += nw) {        // grid stride: adjacent tiles in flight together
                                                         // (measured faster than contiguous runs per warp)
@@ -1095,6 +1097,8 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const
 
 // ---- finalize ---------------------------------------------------------------------------------------
 __global__ void k_finalize(const KArgs a, const DfaK dfa, const ColsK colsk) {
+  PdlTrigger pdl_trigger;
+  pdl_wait();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   Seg tot = a.ntiles ? seg_op(a.seed, *a.tot_seg) : a.seed;
   uint32_t tau = a.ntiles ? *a.tot_tau : NIB_IDENT;
@@ -1156,6 +1160,8 @@ struct DfaDataSrc {                   // DATA bytes of [fd, ld], re-simulated fr
 
 template <bool TS>
 __global__ void k_deferred(const KArgs a, const DfaK dfa, const ColsK colsk) {
+  PdlTrigger pdl_trigger;
+  pdl_wait();
   unsigned int n = min(a.ctrl->n_defer, a.dq_cap);
   for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     DeferItem it = a.dq[i];

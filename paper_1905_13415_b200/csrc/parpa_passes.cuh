@@ -86,8 +86,10 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass1(const KArgs a, con
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const PassSmem ps = pass_smem(smem, warp, lane);
+  PdlTrigger pdl_trigger;
   build_lut(ps.lut, dfa);
   __syncthreads();
+  pdl_wait();
   uint4 *bufs = ps.bufs;
   const uint32_t nw = gridDim.x * PASS_WARPS;
   uint32_t t = blockIdx.x * PASS_WARPS + warp;
@@ -115,6 +117,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_tau_scan(const KArgs a) {
   __shared__ uint32_t s_bid, s_prefix;
   __shared__ uint32_t s_warp[SCAN_THREADS / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  PdlTrigger pdl_trigger;
+  pdl_wait();
   if (threadIdx.x == 0) s_bid = atomicAdd(&a.ctrl->ticket, 1u);   // ticket order: look-backs only
   __syncthreads();                                                   // wait on started blocks
   const uint32_t b = s_bid;
@@ -226,8 +230,10 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, con
   extern __shared__ __align__(16) uint8_t smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const PassSmem ps = pass_smem(smem, warp, lane);
+  PdlTrigger pdl_trigger;
   build_lut(ps.lut, dfa);
   __syncthreads();
+  pdl_wait();
   uint4 *bufs = ps.bufs;
   const uint32_t nw = gridDim.x * PASS_WARPS;
   uint32_t t = blockIdx.x * PASS_WARPS + warp;
@@ -315,6 +321,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_seg_scan(const KArgs a) {
   __shared__ Seg s_prefix;
   __shared__ Seg s_warp[SCAN_THREADS / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  PdlTrigger pdl_trigger;
+  pdl_wait();
   if (threadIdx.x == 0) s_bid = atomicAdd(&a.ctrl->ticket2, 1u);
   __syncthreads();
   const uint32_t b = s_bid;
