@@ -944,13 +944,15 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
         if (!live || c < cs) continue;                        // c < cs: written by an earlier tile
         const uint32_t k = start + (c - cs);
         if (k < end) {
-          uint32_t e;
-          if (plain && k) {
-            const uint32_t x = (ws->dlist[k - 1] & 0x7FFu) + 1u, p = ws->dlist[k] & 0x7FFu;
-            e = x < p ? x | ((p - x) << 11) : p;
-          } else {
-            e = ws->fields[k];
+          if (plain && k) {                                    // the common case: [x, p), all DATA, in the tile
+            const uint32_t x = (ws->dlist[k - 1] & 0x7FFu) + 1u, len = (ws->dlist[k] & 0x7FFu) - x;
+            const unsigned long long off = tbase_g + x;        // empty (x == p): (delimiter position, 0)
+            st_col(cd->off + row, off);
+            st_col(cd->len + row, len);
+            if (type != T_SPAN) write_value_tile<TS>(a, cd, type, c, row, x, len, false, false, off, tb, tbase_g);
+            continue;
           }
+          const uint32_t e = ws->fields[k];
           if (e == FIELD_WRITTEN) continue;
           uint32_t len, o;
           unsigned long long off;
