@@ -81,7 +81,9 @@ struct Ctrl {
   unsigned long long inv_neg;        // ~(first invalid byte position), 0 = none (atomicMax)
   unsigned long long n_missing;
   unsigned long long n_extra;
-  unsigned long long pad[2];
+  unsigned int deferred_done;        // k_deferred blocks finished (the last one settles the status)
+  unsigned int pad0;
+  unsigned long long pad[1];
 };
 
 struct TileInfo {
@@ -415,11 +417,19 @@ struct RawSrc {                       // the raw span [pos, end] of a field with
   }
 };
 
-__device__ __forceinline__ void push_defer(const KArgs &a, unsigned long long fd, unsigned long long ld,
-                                           unsigned long long row, uint32_t c, uint32_t ic) {
+// The device tier's queue holds dq_cap items (len / 512, at least 4096).  A field that finds it full marks
+// its valid byte (VALID_REDO_IC / VALID_REDO) and k_deferred, seeing defer_overflow, converts every marked
+// row of the typed columns from its span: any number of deferred fields parses.
+constexpr uint8_t VALID_REDO = 0xFF, VALID_REDO_IC = 0xFE;
+__device__ __forceinline__ void push_defer(const KArgs &a, const ColDesc *cd, unsigned long long fd,
+                                           unsigned long long ld, unsigned long long row, uint32_t c, uint32_t ic) {
   uint32_t idx = atomicAdd(&a.ctrl->n_defer, 1u);
-  if (idx < a.dq_cap) a.dq[idx] = DeferItem{fd, ld, row, c, ic};
-  else atomicOr(&a.ctrl->defer_overflow, 1u);
+  if (idx < a.dq_cap) {
+    a.dq[idx] = DeferItem{fd, ld, row, c, ic};
+  } else {
+    cd->valid[row] = ic ? VALID_REDO_IC : VALID_REDO;
+    atomicOr(&a.ctrl->defer_overflow, 1u);
+  }
 }
 
 template <bool TS>
@@ -449,13 +459,13 @@ __device__ void emit_field(const KArgs &a, const ColDesc *cols, unsigned long lo
   if (fd == NONE) {
     if (cd->has_def) { v = cd->def_bits; ok = 1; }
   } else if (fl & F_IC) {
-    push_defer(a, fd, ld, row, c, 1u);
+    push_defer(a, cd, fd, ld, row, c, 1u);
     return;
   } else {
     RawSrc src{&a, fd, ld, true};
     int res = conv_typed<TS>(src, type, v);
     if (!src.ok) res = 2;                           // bytes outside this range: device tier
-    if (res == 2) { push_defer(a, fd, ld, row, c, 0u); return; }
+    if (res == 2) { push_defer(a, cd, fd, ld, row, c, 0u); return; }
     ok = res;
     if (!ok) v = 0;
   }
@@ -591,7 +601,7 @@ __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, u
   if (empty) {
     if (cd->has_def) { v = cd->def_bits; ok = 1; }
   } else if (ic) {
-    push_defer(a, fd, ld, row, c, 1u);
+    push_defer(a, cd, fd, ld, row, c, 1u);
     return;
   } else {
     int res = 2;
@@ -626,7 +636,7 @@ __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, u
       res = conv_typed<TS>(src, cd->type, v);
       if (!src.ok) res = 2;
     }
-    if (res == 2) { push_defer(a, fd, ld, row, c, 0u); return; }
+    if (res == 2) { push_defer(a, cd, fd, ld, row, c, 0u); return; }
     ok = res;
     if (!ok) v = 0;
   }
@@ -1125,7 +1135,7 @@ __global__ void k_finalize(const KArgs a, const DfaK dfa, const ColsK colsk) {
   unsigned int n_defer = a.ctrl->n_defer;
   int status = ST_OK;
   if (first_inv != NONE) status = ST_EFORMAT;
-  else if (a.ctrl->unsupported || cnt.unsupported || a.ctrl->defer_overflow) status = ST_EUNSUPPORTED;
+  else if (a.ctrl->unsupported || cnt.unsupported) status = ST_EUNSUPPORTED;
   else if (R - a.row_base > a.cap) status = ST_ENEEDMORE;
   else if ((missing || extra) && a.strict) status = ST_ECOLUMNS;
   if (a.stats) {
@@ -1160,42 +1170,70 @@ struct DfaDataSrc {                   // DATA bytes of [fd, ld], re-simulated fr
   }
 };
 
+// one deferred field: the exact device-tier conversion of its DATA bytes
+template <bool TS>
+__device__ void convert_deferred(const KArgs &a, const DfaK &dfa, const ColDesc *cd, unsigned long long fd,
+                                 unsigned long long ld, unsigned long long row, uint32_t ic) {
+  long long v = 0;
+  int ok = 0;
+  if (ic) {
+    if (fd < a.base) {
+      atomicOr(&a.ctrl->unsupported, 1u);            // a span crossing into a previous range with inner
+    } else {                                          // control bytes (multi-GPU) is not handled
+      unsigned long long local = fd - a.base;
+      unsigned long long k = local / CHUNK;
+      uint32_t x = 0x80u | a.chunk_state[k];
+      for (unsigned long long p = k * CHUNK; p < local; p++) {
+        uint8_t b = a.in[p];
+        x = prmt(dfa.lut[b][2], dfa.lut[b][3], x);
+      }
+      DfaDataSrc src{&a, &dfa, fd, ld, x, true};
+      ok = conv_typed_exact<TS>(src, cd->type, v);
+    }
+  } else {
+    RawSrc src{&a, fd, ld, true};
+    ok = conv_typed_exact<TS>(src, cd->type, v);
+    if (!src.ok) { ok = 0; atomicOr(&a.ctrl->unsupported, 1u); }
+  }
+  if (ok != 1) { ok = 0; v = 0; }
+  reinterpret_cast<long long *>(cd->val)[row] = v;
+  cd->valid[row] = (uint8_t)ok;
+}
+
 template <bool TS>
 __global__ void k_deferred(const KArgs a, const DfaK dfa, const ColsK colsk) {
   PdlTrigger pdl_trigger;
   pdl_wait();
+  const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
   unsigned int n = min(a.ctrl->n_defer, a.dq_cap);
-  for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    DeferItem it = a.dq[i];
-    const ColDesc *cd = colsk.c + it.col;
-    long long v = 0;
-    int ok = 0;
-    if (it.ic) {
-      if (it.fd < a.base) {
-        atomicOr(&a.ctrl->unsupported, 1u);          // a span crossing into a previous range with inner
-      } else {                                        // control bytes (multi-GPU) is not handled
-        unsigned long long local = it.fd - a.base;
-        unsigned long long k = local / CHUNK;
-        uint32_t x = 0x80u | a.chunk_state[k];
-        for (unsigned long long p = k * CHUNK; p < local; p++) {
-          uint8_t b = a.in[p];
-          x = prmt(dfa.lut[b][2], dfa.lut[b][3], x);
-        }
-        DfaDataSrc src{&a, &dfa, it.fd, it.ld, x, true};
-        ok = conv_typed_exact<TS>(src, cd->type, v);
-      }
-    } else {
-      RawSrc src{&a, it.fd, it.ld, true};
-      ok = conv_typed_exact<TS>(src, cd->type, v);
-      if (!src.ok) { ok = 0; atomicOr(&a.ctrl->unsupported, 1u); }
-    }
-    if (ok != 1) { ok = 0; v = 0; }
-    reinterpret_cast<long long *>(cd->val)[it.row] = v;
-    cd->valid[it.row] = (uint8_t)ok;
+  for (unsigned long long i = tid; i < n; i += nth) {
+    const DeferItem it = a.dq[i];
+    convert_deferred<TS>(a, dfa, colsk.c + it.col, it.fd, it.ld, it.row, it.ic);
   }
-  if (a.stats && blockIdx.x == 0 && threadIdx.x == 0 && (a.ctrl->unsupported || a.ctrl->defer_overflow) &&
-      a.stats->status == ST_OK)
-    a.stats->status = ST_EUNSUPPORTED;
+  if (a.ctrl->defer_overflow) {                     // the queue was full: convert the marked rows
+    const unsigned long long R = a.stats ? min((unsigned long long)a.stats->records, a.cap) : a.cap;
+    for (uint32_t c = 0; c < a.C; c++) {
+      const ColDesc *cd = colsk.c + c;
+      if (cd->type == T_SPAN || cd->type == T_SKIP) continue;
+      for (unsigned long long r = tid; r < R; r += nth) {
+        const uint8_t m = cd->valid[r];
+        if (m == VALID_REDO || m == VALID_REDO_IC) {
+          const unsigned long long fd = cd->off[r];
+          convert_deferred<TS>(a, dfa, cd, fd, fd + cd->len[r] - 1, r, m == VALID_REDO_IC ? 1u : 0u);
+        }
+      }
+    }
+  }
+  // the last block to finish settles the status (every block's conversions are done by then)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    // (modulo the grid: a plan emitted more than once keeps counting)
+    if ((atomicAdd(&a.ctrl->deferred_done, 1u) + 1u) % gridDim.x == 0u && a.stats &&
+        *reinterpret_cast<volatile unsigned int *>(&a.ctrl->unsupported) && a.stats->status == ST_OK)
+      a.stats->status = ST_EUNSUPPORTED;
+  }
 }
 
 // ---- debug trace (tests): per-byte state-before and emission kind ---------------------------------

@@ -434,3 +434,45 @@ def test_infer_types_constructed():
         assert types == [t for t, _ in ora], (types, ora)
         assert masks == [sum(1 << oracle.CLASSES.index(c) for c in cls) for _, cls in ora]
     assert parpa.infer_types(dfa("csv"), dev(col_ints), 1)[0] == ["int16"]
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_plain_tiles_ragged_empty_and_giant(seed):
+    """Tiles without control bytes (the direct delimiter-list paths of k_emit): many short records per tile
+    (column-uniform writes) with empty fields (defaults on some typed columns), records with missing and
+    extra fields, numbers of every window length (1-20 characters), and unquoted giant fields of 3-70 KB
+    (field 0 of later tiles begins tiles earlier) in span and typed columns."""
+    rng = random.Random(seed)
+    types = [oracle.INT64, oracle.FLOAT64, oracle.SPAN, oracle.INT64, oracle.FLOAT64, oracle.SPAN, oracle.INT64,
+             oracle.FLOAT64]
+    C = len(types)
+
+    def num(t):
+        L = rng.choice([1, 1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 16, 20])
+        digits = "".join(rng.choice("0123456789") for _ in range(L))
+        s = rng.choice(["", "", "-", "+"]) + digits
+        if t == oracle.FLOAT64 and rng.random() < 0.6:
+            q = rng.randint(0, len(s))
+            s = s[:q] + "." + s[q:]
+        return s
+
+    rows = []
+    for r in range(40000):
+        n = C if rng.random() < 0.9 else rng.choice([1, 3, C - 1, C + 1, C + 3])
+        fs = []
+        for c in range(n):
+            t = types[c % C]
+            if rng.random() < 0.08:
+                fs.append("")
+            elif t == oracle.SPAN:
+                fs.append("".join(rng.choice("abcxyz XYZ-:.") for _ in range(rng.randint(0, 12))))
+            else:
+                fs.append(num(t))
+        if rng.random() < 0.0015:                           # giant unquoted field
+            c = rng.randrange(len(fs))
+            big = rng.randint(3000, 70000)
+            fs[c] = "".join(rng.choice("0123456789") for _ in range(big)) if types[c % C] != oracle.SPAN else "g" * big
+        rows.append(",".join(fs))
+    data = ("\n".join(rows) + ("\n" if seed != 2 else "")).encode()
+    run_all_paths("csv", data, types, label=f"plain{seed}")
+    run_all_paths("csv", data, types, defaults=[-7, 0.5, None, None, -0.0, None, 3, None], label=f"plain{seed}/defaults")
