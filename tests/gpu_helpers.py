@@ -34,3 +34,41 @@ def compare(res, ora, types, label=""):
             v = to_np(col.value).view(np.int64)[:ora.R]
             bad = np.flatnonzero(v != ora.value[c])
             assert bad.size == 0, (label, "value", c, bad[:5], v[bad[:5]], ora.value[c][bad[:5]])
+
+
+def adversarial_plain(seed, nrows=40000):
+    """CSV without control bytes: 8 columns (int / float / span), 90% complete records, the rest short or
+    long; 8% empty fields; numbers of 1-20 characters (signs, '.' anywhere in floats); ~0.15% of records with
+    one unquoted giant field of 3-70 KB (digits in typed columns, letters in spans)."""
+    import random
+    rng = random.Random(seed)
+    types = [oracle.INT64, oracle.FLOAT64, oracle.SPAN, oracle.INT64, oracle.FLOAT64, oracle.SPAN, oracle.INT64,
+             oracle.FLOAT64]
+    C = len(types)
+
+    def num(t):
+        L = rng.choice([1, 1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 16, 20])
+        s = rng.choice(["", "", "-", "+"]) + "".join(rng.choice("0123456789") for _ in range(L))
+        if t == oracle.FLOAT64 and rng.random() < 0.6:
+            q = rng.randint(0, len(s))
+            s = s[:q] + "." + s[q:]
+        return s
+
+    rows = []
+    for _ in range(nrows):
+        n = C if rng.random() < 0.9 else rng.choice([1, 3, C - 1, C + 1, C + 3])
+        fs = []
+        for c in range(n):
+            t = types[c % C]
+            if rng.random() < 0.08:
+                fs.append("")
+            elif t == oracle.SPAN:
+                fs.append("".join(rng.choice("abcxyz XYZ-:.") for _ in range(rng.randint(0, 12))))
+            else:
+                fs.append(num(t))
+        if rng.random() < 0.0015:
+            c = rng.randrange(len(fs))
+            big = rng.randint(3000, 70000)
+            fs[c] = "".join(rng.choice("0123456789") for _ in range(big)) if types[c % C] != oracle.SPAN else "g" * big
+        rows.append(",".join(fs))
+    return ("\n".join(rows) + ("\n" if seed % 2 else "")).encode(), types

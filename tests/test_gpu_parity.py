@@ -440,39 +440,45 @@ def test_infer_types_constructed():
 def test_plain_tiles_ragged_empty_and_giant(seed):
     """Tiles without control bytes (the direct delimiter-list paths of k_emit): many short records per tile
     (column-uniform writes) with empty fields (defaults on some typed columns), records with missing and
-    extra fields, numbers of every window length (1-20 characters), and unquoted giant fields of 3-70 KB
-    (field 0 of later tiles begins tiles earlier) in span and typed columns."""
-    rng = random.Random(seed)
-    types = [oracle.INT64, oracle.FLOAT64, oracle.SPAN, oracle.INT64, oracle.FLOAT64, oracle.SPAN, oracle.INT64,
-             oracle.FLOAT64]
-    C = len(types)
-
-    def num(t):
-        L = rng.choice([1, 1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 16, 20])
-        digits = "".join(rng.choice("0123456789") for _ in range(L))
-        s = rng.choice(["", "", "-", "+"]) + digits
-        if t == oracle.FLOAT64 and rng.random() < 0.6:
-            q = rng.randint(0, len(s))
-            s = s[:q] + "." + s[q:]
-        return s
-
-    rows = []
-    for r in range(40000):
-        n = C if rng.random() < 0.9 else rng.choice([1, 3, C - 1, C + 1, C + 3])
-        fs = []
-        for c in range(n):
-            t = types[c % C]
-            if rng.random() < 0.08:
-                fs.append("")
-            elif t == oracle.SPAN:
-                fs.append("".join(rng.choice("abcxyz XYZ-:.") for _ in range(rng.randint(0, 12))))
-            else:
-                fs.append(num(t))
-        if rng.random() < 0.0015:                           # giant unquoted field
-            c = rng.randrange(len(fs))
-            big = rng.randint(3000, 70000)
-            fs[c] = "".join(rng.choice("0123456789") for _ in range(big)) if types[c % C] != oracle.SPAN else "g" * big
-        rows.append(",".join(fs))
-    data = ("\n".join(rows) + ("\n" if seed != 2 else "")).encode()
+    extra fields, numbers of every window length (1-20 characters, far more device-tier fields than the
+    defer queue holds), and unquoted giant fields of 3-70 KB (field 0 of later tiles begins tiles
+    earlier) in span and typed columns."""
+    from tests.gpu_helpers import adversarial_plain
+    data, types = adversarial_plain(seed)
     run_all_paths("csv", data, types, label=f"plain{seed}")
     run_all_paths("csv", data, types, defaults=[-7, 0.5, None, None, -0.0, None, 3, None], label=f"plain{seed}/defaults")
+
+
+@pytest.mark.parametrize("seed", [4, 5])
+def test_quoted_tiles_deferred_overflow(seed):
+    """Tiles with control bytes and far more device-tier fields than the defer queue holds (len / 512):
+    quoted numbers, numbers with "" inside (inner control bytes: invalid, decided by the device tier),
+    exponents beyond the fast path, 20+ digit floats, ragged records, quoted giant fields."""
+    rng = random.Random(seed)
+    types = [oracle.FLOAT64, oracle.INT64, oracle.SPAN, oracle.FLOAT64]
+    rows = []
+    for r in range(30000):
+        fs = []
+        for t in types:
+            k = rng.random()
+            if t == oracle.SPAN:
+                f = '"' + "".join(rng.choice('ab,\n ') for _ in range(rng.randint(0, 20))) + '"'
+            elif k < 0.25:
+                f = '"' + str(rng.randint(-999, 999)) + '"'
+            elif k < 0.45:
+                f = '"' + str(rng.randint(0, 99)) + '""' + str(rng.randint(0, 9)) + '"'
+            elif k < 0.65 and t == oracle.FLOAT64:
+                f = f"{rng.randint(1, 9)}e{rng.choice([23, 50, -30, 300, -320])}"
+            elif k < 0.8 and t == oracle.FLOAT64:
+                f = "".join(rng.choice("0123456789") for _ in range(rng.randint(17, 30))) + "." + str(rng.randint(0, 99))
+            else:
+                f = str(rng.randint(-10**6, 10**6))
+            fs.append(f)
+        if rng.random() < 0.05:
+            fs = fs[:rng.randint(1, 3)]
+        if rng.random() < 0.001:
+            fs[0] = '"' + "x" * rng.randint(3000, 40000) + '""' + '"'
+        rows.append(",".join(fs))
+    data = ("\n".join(rows) + "\n").encode()
+    ora = run_all_paths("csv", data, types, label=f"quoted{seed}")
+    assert sum(1 for c in (0, 1, 3) for v in ora.valid[c] if v == 0) > 5000      # many invalid (device tier)

@@ -124,3 +124,22 @@ def test_cuts_at_delimiters_and_inside_quotes():
             assert np.array_equal(cols[c][0], ora.offset[c])
             assert np.array_equal(cols[c][1], ora.length[c])
         assert np.array_equal(cols[2][2], ora.value[2])
+
+
+@pytest.mark.parametrize("staged", [False, True])
+def test_virtual_ranks_adversarial_plain(staged):
+    """Ranges over CTRL-free data with giant fields and long numbers crossing the cuts (their leading bytes
+    come from the left context), far more device-tier fields than the queue holds, ragged records."""
+    from tests.gpu_helpers import adversarial_plain
+    data, types = adversarial_plain(11, nrows=30000)
+    ora = oracle.parse("csv", data, len(types), types)
+    rng = random.Random(12)
+    cuts = [0] + sorted(rng.sample(range(1, len(data) - 1), 4)) + [len(data)]
+    cols = sharded_parse("csv", data, types, cuts, left_bytes=80000, staged=staged)
+    for c, t in enumerate(types):
+        off, ln, val, ok = cols[c]
+        assert np.array_equal(off, ora.offset[c]), c
+        assert np.array_equal(ln, ora.length[c]), c
+        if t != oracle.SPAN:
+            assert np.array_equal(ok, ora.valid[c]), c
+            assert np.array_equal(val, ora.value[c]), c
