@@ -72,3 +72,37 @@ def adversarial_plain(seed, nrows=40000):
             fs[c] = "".join(rng.choice("0123456789") for _ in range(big)) if types[c % C] != oracle.SPAN else "g" * big
         rows.append(",".join(fs))
     return ("\n".join(rows) + ("\n" if seed % 2 else "")).encode(), types
+
+
+def adversarial_clf(seed, nlines=30000):
+    """Common-Log-Format-like lines (reading R20): space-delimited tokens, [..] and "..." enclosed fields with
+    spaces, \\" and \\\\ escapes inside quotes, '#' directive lines (with quotes and brackets) and '#' inside
+    tokens, ragged token counts, typed columns holding long numbers, '-', empties and quoted numbers."""
+    import random
+    rng = random.Random(seed)
+    types = [oracle.SPAN, oracle.SPAN, oracle.SPAN, oracle.SPAN, oracle.SPAN, oracle.INT64, oracle.INT64]
+    lines = []
+    for _ in range(nlines):
+        if rng.random() < 0.01:
+            lines.append("#" + "".join(rng.choice('ab "[]x #') for _ in range(rng.randint(0, 30))))
+            continue
+        n = 7 if rng.random() < 0.9 else rng.choice([1, 2, 5, 8, 9])
+        fs = []
+        for c in range(n):
+            k = rng.random()
+            if c == 3 or (c > 6 and k < 0.3):
+                fs.append("[" + "".join(rng.choice("0123456789/:+- abc") for _ in range(rng.randint(0, 26))) + "]")
+            elif c == 4 or (c > 6 and k < 0.6):
+                body = ""
+                for _ in range(rng.randint(0, 30)):
+                    r = rng.random()
+                    body += '\\"' if r < 0.05 else "\\\\" if r < 0.08 else rng.choice("GET /a?b=1 HTTP/1.0#")
+                fs.append('"' + body + '"')
+            elif c in (5, 6):
+                fs.append(rng.choice(["-", "", str(rng.randint(0, 999)), str(rng.randint(0, 10 ** 12)),
+                                      "".join(rng.choice("0123456789") for _ in range(rng.randint(15, 25))),
+                                      '"' + str(rng.randint(0, 99)) + '"']))
+            else:
+                fs.append("".join(rng.choice("0123456789.-abc#") for _ in range(rng.randint(1, 15))))
+        lines.append(" ".join(fs))
+    return ("\n".join(lines) + "\n").encode(), types

@@ -482,3 +482,13 @@ def test_quoted_tiles_deferred_overflow(seed):
     data = ("\n".join(rows) + "\n").encode()
     ora = run_all_paths("csv", data, types, label=f"quoted{seed}")
     assert sum(1 for c in (0, 1, 3) for v in ora.valid[c] if v == 0) > 5000      # many invalid (device tier)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_clf_adversarial(seed):
+    """The 9-state CLF DFA on adversarial lines (tests/gpu_helpers.adversarial_clf): enclosed fields with
+    escapes, directive lines, '#' inside tokens and at line start, ragged lines, long / quoted / '-' numbers."""
+    from tests.gpu_helpers import adversarial_clf
+    data, types = adversarial_clf(seed)
+    ora = run_all_paths("clf", data, types, label=f"clf{seed}")
+    assert ora.status == 0 and ora.n_missing > 0 and ora.n_extra > 0

@@ -143,3 +143,20 @@ def test_virtual_ranks_adversarial_plain(staged):
         if t != oracle.SPAN:
             assert np.array_equal(ok, ora.valid[c]), c
             assert np.array_equal(val, ora.value[c]), c
+
+
+def test_virtual_ranks_adversarial_clf():
+    """Ranges over the adversarial CLF lines, cuts anywhere (inside brackets, quotes, escapes, comments)."""
+    from tests.gpu_helpers import adversarial_clf
+    data, types = adversarial_clf(3, nlines=20000)
+    ora = oracle.parse("clf", data, len(types), types)
+    rng = random.Random(13)
+    cuts = [0] + sorted(rng.sample(range(1, len(data) - 1), 5)) + [len(data)]
+    cols = sharded_parse("clf", data, types, cuts, staged=True)
+    for c, t in enumerate(types):
+        off, ln, val, ok = cols[c]
+        assert np.array_equal(off, ora.offset[c]), c
+        assert np.array_equal(ln, ora.length[c]), c
+        if t != oracle.SPAN:
+            assert np.array_equal(ok, ora.valid[c]), c
+            assert np.array_equal(val, ora.value[c]), c
