@@ -492,3 +492,29 @@ def test_clf_adversarial(seed):
     data, types = adversarial_clf(seed)
     ora = run_all_paths("clf", data, types, label=f"clf{seed}")
     assert ora.status == 0 and ora.n_missing > 0 and ora.n_extra > 0
+
+
+def test_csv_comment_adversarial():
+    """CSV + '#' comment lines (reading R19): comments with quotes, commas and brackets between records,
+    '#' inside fields and quoted fields, quoted multi-line fields that contain '\\n#' (not a comment)."""
+    rng = random.Random(21)
+    lines = []
+    for _ in range(25000):
+        r = rng.random()
+        if r < 0.05:
+            lines.append("#" + "".join(rng.choice('a,"#[] x') for _ in range(rng.randint(0, 40))))
+        else:
+            fs = []
+            for c in range(4):
+                k = rng.random()
+                if k < 0.3:
+                    fs.append('"' + "".join(rng.choice('ab,#\n x') for _ in range(rng.randint(0, 15))).replace('"', '""') + '"')
+                elif k < 0.5 and c > 0:                       # (a leading '#' would make the line a comment)
+                    fs.append("#" + str(rng.randint(0, 99)))
+                else:
+                    fs.append(str(rng.randint(-10 ** 9, 10 ** 9)))
+            lines.append(",".join(fs[:rng.choice([4, 4, 4, 2, 5])] if rng.random() < 0.1 else fs))
+    data = ("\n".join(lines) + "\n").encode()
+    types = [oracle.SPAN, oracle.INT64, oracle.SPAN, oracle.INT64]
+    ora = run_all_paths("csv_comment", data, types, label="csvc")
+    assert ora.status == 0
