@@ -518,3 +518,24 @@ def test_csv_comment_adversarial():
     types = [oracle.SPAN, oracle.INT64, oracle.SPAN, oracle.INT64]
     ora = run_all_paths("csv_comment", data, types, label="csvc")
     assert ora.status == 0
+
+
+@pytest.mark.parametrize("kind", ["clf", "plain"])
+def test_strings_and_types_adversarial(kind):
+    """String columns (N3) and type inference (N2) on the adversarial generators: enclosed fields with
+    escapes, giant fields across tiles, ragged records (missing fields give empty strings)."""
+    from tests.gpu_helpers import adversarial_clf, adversarial_plain
+    data, types = adversarial_clf(4, 15000) if kind == "clf" else adversarial_plain(5, 15000)
+    dialect = "clf" if kind == "clf" else "csv"
+    C = len(types)
+    d = dev(data)
+    res = parpa.parse(dfa(dialect), parpa.Schema([oracle.SPAN] * C), d)
+    for c in range(C):
+        ro, rs = oracle.strings(dialect, data, C, c)
+        offs, buf = parpa.strings(dfa(dialect), d, res.columns[c], res.records)
+        assert np.array_equal(offs.cpu().numpy(), ro), (kind, c)
+        assert bytes(buf.cpu().numpy()) == rs, (kind, c)
+    got, masks, R = parpa.infer_types(dfa(dialect), d, C)
+    ora = oracle.infer_types(dialect, data, C)
+    assert got == [t for t, _ in ora], (got, ora)
+    assert masks == [sum(1 << oracle.CLASSES.index(x) for x in cls) for _, cls in ora]
