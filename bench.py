@@ -114,7 +114,9 @@ def gen_range(config, rank, world, pin=True, records=0):
     import datagen
     w = datagen.WORKLOADS[config]
     rb = records or RECORDS_PER_RANK[config]
-    cap = BYTES_CAP[config] + (1 << 20) if not records else records * 4096
+    # (--records: scaled from the config's bytes per record, with headroom; never more than needed)
+    cap = BYTES_CAP[config] + (1 << 20) if not records else \
+        int(BYTES_CAP[config] * records / RECORDS_PER_RANK[config] * 1.25) + (16 << 20)
     cut = lambda g: 0 if g == 0 else 37 + 11 * g              # mid-record cut points
     host = torch.empty(cap + (1 << 20), dtype=torch.uint8, pin_memory=pin)
     g0 = datagen.fill(w, host.data_ptr(), cap, first_record=rank * rb, max_records=rb)
