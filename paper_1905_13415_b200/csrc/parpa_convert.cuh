@@ -199,19 +199,20 @@ __device__ __forceinline__ int conv_window(uint32_t x0, uint32_t x1, uint32_t x2
 // conv_window, in one 32- / 64-bit word: the sign becomes a leading '0', the '.' is squeezed out (the bytes
 // after it move down one place), the n remaining characters are checked to be digits in one carry-free
 // test, shifted up so that 4 - n / 8 - n zero digits lead, and folded pairwise (1+1, 2+2, 4+4 digits).
-// Split in two so that the kernels can parse with one lane per field and finish in the column-major
-// writes: parse -> packed (m | frac << 27 | neg << 30), m < 10^8 < 2^27, frac <= 7 digits after the '.'.
-// Returns 1 (parsed) or 2 ("not handled here": the byte-wise converters decide validity exactly).
-constexpr uint32_t PK_FRAC_SHIFT = 27, PK_NEG = 1u << 30, PK_SLOW = 1u << 31;
-__device__ __forceinline__ int parse_window4(uint32_t x, uint32_t L, bool isf, uint32_t &pk) {
+// Returns 1 (converted) or 2 ("not handled here": the byte-wise converters decide validity exactly).
+// parse_window4/8 yield the significand m < 10^8, the digits after the '.' (frac <= 7) and the sign;
+// finish_window turns them into int64 or float64 bits (m / 10^frac, one correctly rounded division).
+__device__ __forceinline__ int parse_window4(uint32_t x, uint32_t L, bool isf, uint32_t &m, uint32_t &frac, bool &neg) {
   const uint32_t c0 = x & 0xFFu;
+  neg = c0 == '-';
   const uint32_t sgn = (c0 == '-' || c0 == '+') ? 1u : 0u;
   const uint32_t vm = 0xFFFFFFFFu >> (32u - 8u * L);
   uint32_t d = (x ^ 0x30303030u) & vm;
   if (sgn) d &= 0xFFFFFF00u;                                     // sign -> leading zero digit
   const uint32_t t = d ^ 0x1E1E1E1Eu;                            // '.' (0x2E ^ 0x30) -> 0
   const uint32_t dotm = ~(((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & 0x80808080u & vm;
-  uint32_t n = L, frac = 0;
+  uint32_t n = L;
+  frac = 0;
   if (dotm) {
     const uint32_t q = (uint32_t)(__ffs(dotm) - 1) >> 3;        // byte of the first '.'
     const uint32_t lo = (1u << (8u * q)) - 1u;
@@ -224,12 +225,13 @@ __device__ __forceinline__ int parse_window4(uint32_t x, uint32_t L, bool isf, u
   if ((((d & 0x7F7F7F7Fu) + 0x76767676u) | d) & 0x80808080u & nm) return 2;   // stray byte / 2nd '.'
   d <<= 8u * (4u - n);                                           // right-align: 4 - n leading zeros
   d = (d * 10u + (d >> 8)) & 0x00FF00FFu;
-  const uint32_t m = (d & 0xFFFFu) * 100u + (d >> 16);
-  pk = m | (frac << PK_FRAC_SHIFT) | (c0 == '-' ? PK_NEG : 0u);
+  m = (d & 0xFFFFu) * 100u + (d >> 16);
   return 1;
 }
-__device__ __forceinline__ int parse_window8(unsigned long long x, uint32_t L, bool isf, uint32_t &pk) {
+__device__ __forceinline__ int parse_window8(unsigned long long x, uint32_t L, bool isf, uint32_t &m, uint32_t &frac,
+                                             bool &neg) {
   const uint32_t c0 = (uint32_t)x & 0xFFu;
+  neg = c0 == '-';
   const uint32_t sgn = (c0 == '-' || c0 == '+') ? 1u : 0u;
   const unsigned long long H = 0x8080808080808080ull, M7 = 0x7F7F7F7F7F7F7F7Full;
   const unsigned long long vm = L >= 8u ? ~0ull : (1ull << (8u * L)) - 1ull;
@@ -237,7 +239,8 @@ __device__ __forceinline__ int parse_window8(unsigned long long x, uint32_t L, b
   if (sgn) d &= ~0xFFull;
   const unsigned long long t = d ^ 0x1E1E1E1E1E1E1E1Eull;
   const unsigned long long dotm = ~(((t & M7) + M7) | t) & H & vm;
-  uint32_t n = L, frac = 0;
+  uint32_t n = L;
+  frac = 0;
   if (dotm) {
     const uint32_t q = (uint32_t)(__ffsll((long long)dotm) - 1) >> 3;
     const unsigned long long lo = (1ull << (8u * q)) - 1ull;
@@ -251,14 +254,10 @@ __device__ __forceinline__ int parse_window8(unsigned long long x, uint32_t L, b
   d <<= 8u * (8u - n);
   d = (d * 10u + (d >> 8)) & 0x00FF00FF00FF00FFull;
   d = (d * 100u + (d >> 16)) & 0x0000FFFF0000FFFFull;
-  const uint32_t m = (uint32_t)((d * 10000u + (d >> 32)) & 0xFFFFFFFFull);
-  pk = m | (frac << PK_FRAC_SHIFT) | (c0 == '-' ? PK_NEG : 0u);
+  m = (uint32_t)((d * 10000u + (d >> 32)) & 0xFFFFFFFFull);
   return 1;
 }
-// packed -> int64 / float64 bits: the float is m / 10^frac, one correctly rounded division (div_pow10)
-__device__ __forceinline__ long long finish_window(uint32_t pk, bool isf) {
-  const uint32_t m = pk & ((1u << PK_FRAC_SHIFT) - 1u), frac = (pk >> PK_FRAC_SHIFT) & 7u;
-  const bool neg = (pk & PK_NEG) != 0;
+__device__ __forceinline__ long long finish_window(uint32_t m, uint32_t frac, bool neg, bool isf) {
   if (!isf) return neg ? -(long long)m : (long long)m;
   double v = (double)m;
   if (frac) v = div_pow10(v, frac);
@@ -266,15 +265,17 @@ __device__ __forceinline__ long long finish_window(uint32_t pk, bool isf) {
   return __double_as_longlong(v);
 }
 __device__ __forceinline__ int conv_window4(uint32_t x, uint32_t L, bool isf, long long &out) {
-  uint32_t pk;
-  if (parse_window4(x, L, isf, pk) != 1) return 2;
-  out = finish_window(pk, isf);
+  uint32_t m, frac;
+  bool neg;
+  if (parse_window4(x, L, isf, m, frac, neg) != 1) return 2;
+  out = finish_window(m, frac, neg, isf);
   return 1;
 }
 __device__ __forceinline__ int conv_window8(unsigned long long x, uint32_t L, bool isf, long long &out) {
-  uint32_t pk;
-  if (parse_window8(x, L, isf, pk) != 1) return 2;
-  out = finish_window(pk, isf);
+  uint32_t m, frac;
+  bool neg;
+  if (parse_window8(x, L, isf, m, frac, neg) != 1) return 2;
+  out = finish_window(m, frac, neg, isf);
   return 1;
 }
 
