@@ -209,18 +209,20 @@ __device__ __forceinline__ int parse_window4(uint32_t x, uint32_t L, bool isf, u
   const uint32_t vm = 0xFFFFFFFFu >> (32u - 8u * L);
   uint32_t d = (x ^ 0x30303030u) & vm;
   if (sgn) d &= 0xFFFFFF00u;                                     // sign -> leading zero digit
-  const uint32_t t = d ^ 0x1E1E1E1Eu;                            // '.' (0x2E ^ 0x30) -> 0
-  const uint32_t dotm = ~(((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & 0x80808080u & vm;
   uint32_t n = L;
   frac = 0;
-  if (dotm) {
-    const uint32_t q = (uint32_t)(__ffs(dotm) - 1) >> 3;        // byte of the first '.'
-    const uint32_t lo = (1u << (8u * q)) - 1u;
-    d = (d & lo) | ((d >> 8) & ~lo);                             // squeeze it out
-    n = L - 1u;
-    frac = n - q;
+  if (isf) {                                                     // (an int64 '.' fails the digit test)
+    const uint32_t t = d ^ 0x1E1E1E1Eu;                          // '.' (0x2E ^ 0x30) -> 0
+    const uint32_t dotm = ~(((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & 0x80808080u & vm;
+    if (dotm) {
+      const uint32_t q = (uint32_t)(__ffs(dotm) - 1) >> 3;      // byte of the first '.'
+      const uint32_t lo = (1u << (8u * q)) - 1u;
+      d = (d & lo) | ((d >> 8) & ~lo);                           // squeeze it out
+      n = L - 1u;
+      frac = n - q;
+    }
   }
-  if (n <= sgn || (dotm && !isf)) return 2;                      // no digit, or '.' in an int64
+  if (n <= sgn) return 2;                                        // no digit
   const uint32_t nm = 0xFFFFFFFFu >> (32u - 8u * n);
   if ((((d & 0x7F7F7F7Fu) + 0x76767676u) | d) & 0x80808080u & nm) return 2;   // stray byte / 2nd '.'
   d <<= 8u * (4u - n);                                           // right-align: 4 - n leading zeros
@@ -237,18 +239,20 @@ __device__ __forceinline__ int parse_window8(unsigned long long x, uint32_t L, b
   const unsigned long long vm = L >= 8u ? ~0ull : (1ull << (8u * L)) - 1ull;
   unsigned long long d = (x ^ 0x3030303030303030ull) & vm;
   if (sgn) d &= ~0xFFull;
-  const unsigned long long t = d ^ 0x1E1E1E1E1E1E1E1Eull;
-  const unsigned long long dotm = ~(((t & M7) + M7) | t) & H & vm;
   uint32_t n = L;
   frac = 0;
-  if (dotm) {
-    const uint32_t q = (uint32_t)(__ffsll((long long)dotm) - 1) >> 3;
-    const unsigned long long lo = (1ull << (8u * q)) - 1ull;
-    d = (d & lo) | ((d >> 8) & ~lo);
-    n = L - 1u;
-    frac = n - q;
+  if (isf) {
+    const unsigned long long t = d ^ 0x1E1E1E1E1E1E1E1Eull;
+    const unsigned long long dotm = ~(((t & M7) + M7) | t) & H & vm;
+    if (dotm) {
+      const uint32_t q = (uint32_t)(__ffsll((long long)dotm) - 1) >> 3;
+      const unsigned long long lo = (1ull << (8u * q)) - 1ull;
+      d = (d & lo) | ((d >> 8) & ~lo);
+      n = L - 1u;
+      frac = n - q;
+    }
   }
-  if (n <= sgn || (dotm && !isf)) return 2;
+  if (n <= sgn) return 2;
   const unsigned long long nm = n >= 8u ? ~0ull : (1ull << (8u * n)) - 1ull;
   if ((((d & M7) + 0x7676767676767676ull) | d) & H & nm) return 2;
   d <<= 8u * (8u - n);
