@@ -964,6 +964,14 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
             continue;
           }
           const uint32_t e = ws->fields[k];
+          if (k) {                                             // only field 0 can carry a special entry
+            const uint32_t o = e & 0x7FFu, len = (e >> 11) & 0xFFFu;
+            const unsigned long long off = tbase_g + o;
+            st_col(cd->off + row, off);
+            st_col(cd->len + row, len);
+            if (type != T_SPAN) write_value_tile<TS>(a, cd, type, c, row, o, len, (e >> 31) != 0, false, off, tb, tbase_g);
+            continue;
+          }
           if (e == FIELD_WRITTEN) continue;
           uint32_t len, o;
           unsigned long long off;
