@@ -66,6 +66,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void stage_chunk(const KArgs &a, uint4 *buf, uint32_t t, int lane) {
   const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
+  if ((unsigned long long)(t + 1) * WT <= a.len) {                  // whole tile in range (all but the last):
+#pragma unroll                                                         // no per-unit clamps (the pass kernels
+    for (int u = 0; u < 4; u++) cp_async16(buf + pswz(lane, u), a.in + cstart + 16 * u, 16u);   // are ALU-bound)
+    return;
+  }
   const int nv = chunk_valid(a, cstart);
 #pragma unroll
   for (int u = 0; u < 4; u++) {
