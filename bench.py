@@ -1,22 +1,32 @@
 #!/usr/bin/env python
-"""Benchmark of the ParPaRaw hot path on B200.
+"""Benchmark of the ParPaRaw hot path on B200 (see DESIGN.md §7 Measurement).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config taxi|yelp|clf|cfg1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config yelp|taxi|clf|cfg1] [--impl ours|reference]
 
-A step = one full parse (all of S1-S8) of one GPU's input: the configuration BASELINE.json's metric
-is quoted on at N=1 is configs[1] (taxi-shaped CSV, 4.8 GB, 18 columns).  For N > 1 (torchrun, one
-rank per GPU, NCCL) every rank owns one contiguous, deliberately not record-aligned 4.8 GB byte
-range of one logical taxi file (weak scaling) and the step includes the two summary allgathers.
+A step = one full parse (all of S1-S8) of one GPU's input, resident in HBM.  With no --config the
+main line is the north-star configuration (yelp-shaped quoted CSV, 4.823 GB: "bit-exact parse of
+>= 4.8 GB quoted CSV on one B200", BASELINE.json) and the other single-GPU configs of BASELINE.json
+(taxi 4.8 GB = configs[1], CLF ~8 GB = configs[3], the 1 MB cfg1 = configs[0]) follow as same-run
+sub-records under "configs", each with its own roofline, step fraction, clocks and parity.
 
-`value` = input GB/s of the whole job (all ranks' bytes / max-over-ranks device time), inputs
-resident in HBM, outputs written column-major into pre-sized device columns (capacity from an
-untimed plan pass; DESIGN.md explains why this is not skipped work).  One JSON line on rank 0.
+For N > 1 (one rank per GPU, NCCL; `--gpus N` without torchrun re-launches itself under
+torch.distributed.run) every rank owns one contiguous, deliberately not record-aligned byte range
+of one logical file of the config's shape (weak scaling) and the step includes the two summary
+allgathers.
+
+`value` = input GB/s of the whole job (all ranks' bytes / max-over-ranks device time), outputs
+written column-major into pre-sized device columns (capacity from an untimed plan pass).  Parity:
+after the timed steps every output row of every column is compared with the oracle (the sequential
+CPU parser, oracle/), run over generator record ranges on the host's cores.  One JSON line on rank 0.
 """
 from __future__ import annotations
 
 import argparse
+import concurrent.futures as cf
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -28,13 +38,15 @@ sys.path.insert(0, ROOT)
 
 METRIC = "on-device parse GB/s of input (1/2/4/8 B200) and fraction of HBM roofline"
 CONFIG_LABEL = {
-    "taxi": "NYC-taxi-shaped CSV, 4.8 GB, 18 numeric/datetime columns, unquoted, 1 B200 per rank",
-    "yelp": "Yelp-reviews-shaped CSV, ~4.8 GB, all fields quoted, long multi-line text",
-    "clf": "Common-Log-Format-shaped logs, ~8 GB, 9-state DFA",
-    "cfg1": "1 MB RFC-4180 CSV, 8 columns, ~10% quoted fields",
+    "yelp": "Yelp-reviews-shaped CSV, 4.823 GB, all fields quoted, long multi-line text with escaped quotes "
+            "(BASELINE configs[2] at the paper's size; the north-star >= 4.8 GB quoted-CSV target)",
+    "taxi": "NYC-taxi-shaped CSV, 4.8 GB, 18 numeric/datetime columns, unquoted (BASELINE configs[1])",
+    "clf": "Common-Log-Format-shaped logs, ~7.5 GB, 9-state DFA, '#' directive lines (BASELINE configs[3])",
+    "cfg1": "1 MB RFC-4180 CSV, 8 columns, ~10% quoted fields (BASELINE configs[0])",
 }
 RECORDS_PER_RANK = {"taxi": 48_900_000, "yelp": 6_670_000, "clf": 78_000_000, "cfg1": 10_000}
 BYTES_CAP = {"taxi": 4_800_000_000, "yelp": 4_823_000_000, "clf": 8_000_000_000, "cfg1": 1_000_000}
+SUB_CONFIGS = ["taxi", "clf", "cfg1"]
 
 
 def load_peaks():
@@ -59,7 +71,19 @@ def load_traffic(config, nbytes, timestamps=False):
         return None
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 class Clocks:
+    """nvidia-smi sampled every 25 ms during the timed region (clocks + throttle reasons)."""
+
     def __init__(self):
         self.proc = None
         self.path = None
@@ -75,6 +99,7 @@ class Clocks:
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "25"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.2)
         except Exception:
             self.proc = None
 
@@ -103,6 +128,11 @@ class Clocks:
                         reasons.add(n)
         except Exception:
             return None
+        finally:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
@@ -158,12 +188,12 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import numpy as np
     import datagen
     import oracle
-    w = workload(args.config, args.timestamps)
+    config = args.config or "yelp"
+    w = workload(config, args.timestamps)
     sample = args.ref_sample_bytes
-    data, g = datagen.generate(args.config, sample)
+    data, g = datagen.generate(config, sample)
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -177,10 +207,11 @@ def run_reference(args):
     line = {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.config, "description": CONFIG_LABEL[args.config], "timestamps": bool(args.timestamps),
+            "config": {"workload": config, "description": CONFIG_LABEL[config], "timestamps": bool(args.timestamps),
                        "sample_bytes": len(data), "records": g.records},
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                             "sample": f"first {len(data)} bytes ({g.records} records) of the {args.config} workload, "
+                             "cpu": cpu_model(),
+                             "sample": f"first {len(data)} bytes ({g.records} records) of the {config} workload, "
                                        f"single-threaded sequential parse incl. int64/float64 conversion"},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -188,8 +219,6 @@ def run_reference(args):
 
 def cpu_baseline(config, data_host, budget_s=10.0, timestamps=False):
     """The oracle as it stands, 1 host core, on a bounded prefix of this workload."""
-    import numpy as np
-    import datagen
     import oracle
     w = workload(config, timestamps)
     arr = data_host.numpy()
@@ -201,206 +230,73 @@ def cpu_baseline(config, data_host, budget_s=10.0, timestamps=False):
     t0 = time.perf_counter()
     r = oracle.parse(w.dialect, arr[:n], w.C, list(w.types))
     dt = time.perf_counter() - t0
-    return {"value": round(n / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+    return {"value": round(n / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
             "sample": f"first {n} bytes ({r.R} records) of this rank's input; single-threaded sequential "
-                      f"parse with int64/float64 conversion; {os.cpu_count()} host cores present"}
+                      f"parse with int64/float64 conversion; oracle uses 1 of {os.cpu_count()} host cores"}
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="taxi", choices=list(CONFIG_LABEL))
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--ref-sample-bytes", type=int, default=150_000_000)
-    ap.add_argument("--records", type=int, default=0, help="override records per rank (profiling runs)")
-    ap.add_argument("--timestamps", action="store_true", help="type the datetime columns as TIMESTAMP (SURVEY N2)")
-    ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays of the parse (default for cfg1)")
-    ap.add_argument("--no-graph", action="store_true", help="time eager launches even for cfg1")
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
+# ---- same-run parity: every output row against the oracle, over generator record ranges -----------------
+def _digest(a):
+    return hashlib.blake2b(memoryview(a).cast("B"), digest_size=16).hexdigest()
 
+
+def _oracle_chunk(config, w, r0, m):
+    """Worker: the generator's records [r0, r0 + m) parsed by the oracle; per-column digests with
+    offsets relative to the chunk's first byte (the chunk starts a record, so the state is the start)."""
     import numpy as np
-    import torch
     import datagen
-    import paper_1905_13415_b200 as parpa
-    from paper_1905_13415_b200 import distributed as pdist
+    import oracle
+    cap = int(BYTES_CAP[config] / RECORDS_PER_RANK[config] * m * 1.5) + (4 << 20)
+    while True:
+        data, g = datagen.generate(config, cap, first_record=r0, threads=1, max_records=m)
+        if g.records == m:
+            break
+        cap *= 2                                             # a chunk of long records: retry larger
+    r = oracle.parse(w.dialect, data, w.C, list(w.types))
+    cols = []
+    for c in range(w.C):
+        d = [_digest(r.offset[c]), _digest(r.length[c])]
+        if r.value[c] is not None:
+            d += [_digest(r.value[c]), _digest(r.valid[c])]
+        cols.append(d)
+    return len(data), r.R, r.status, r.n_missing, r.n_extra, cols
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    # test switch: every rank on cuda:0 with gloo collectives (validates the sharded path on one GPU;
-    # never used for a reported number)
-    shared = os.environ.get("PARPA_BENCH_SHARED_GPU") == "1"
-    gpu = 0 if shared else local
-    coll = "cpu" if shared else "cuda"
-    torch.cuda.set_device(gpu)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        if shared:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w = workload(args.config, args.timestamps)
-    dfa = parpa.Dfa.dialect(w.dialect)
-    schema = parpa.Schema(list(w.types))
 
-    t_gen = time.time()
-    data_host, left_host, block_len, cut0, g = gen_range(args.config, rank, world, records=args.records)
-    t_gen = time.time() - t_gen
-    n = data_host.numel()
-    d = torch.empty(n + 64, dtype=torch.uint8, device="cuda")[:n]
-    d.copy_(data_host, non_blocking=True)
-    left = left_host.cuda() if left_host is not None else None
-    base = 0
-    if world > 1:
-        lens = torch.tensor([block_len], dtype=torch.int64, device=coll)
-        all_lens = [torch.zeros_like(lens) for _ in range(world)]
-        dist.all_gather(all_lens, lens)
-        base = sum(int(x.item()) for x in all_lens[:rank]) + cut0
-    torch.cuda.synchronize()
-
-    # capacity from an untimed scan pass (records of this range)
-    stream = torch.cuda.current_stream()
-    if world == 1:
-        res_plan = parpa.parse(dfa, schema, d)
-        cap = res_plan.records
-        assert res_plan.status == 0 and cap == g.records, (res_plan.stats, g.records)
-        del res_plan
-    else:
-        cap = g.records + 2
-    cols = parpa.alloc_columns(schema, cap)
-    st = parpa.new_stats_tensor()
-    is_last = rank == world - 1
-
-    def step():
-        if world == 1:
-            return parpa.parse_into(dfa, schema, d, cols, cap, st)
-        pdist.parse_sharded(dfa, schema, d, base, cols, cap, st, left=left, is_last=is_last,
-                            exchange_device=coll)
-        return 7                                  # range_begin 2 + range_count 2 + range_emit 3
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    stats = parpa.stats_from_tensor(st)
-    assert stats["status"] == 0, stats
-    if world == 1:
-        assert stats["records"] == g.records, (stats, g.records)
-    else:                                                     # the ranks' records add up exactly
-        tr = torch.tensor([stats["records"], g.records], dtype=torch.float64, device=coll)
-        dist.all_reduce(tr, op=dist.ReduceOp.SUM)
-        assert int(tr[0].item()) == int(tr[1].item()), (stats, tr)
-
-    # launch-bound inputs (cfg1, 1 MB): each step is one replay of a CUDA graph of the parse
-    use_graph = world == 1 and (args.graph or (args.config == "cfg1" and not args.no_graph))
-    graph, per_step = None, 0
-    if use_graph:
-        gs = torch.cuda.Stream()
-        gs.wait_stream(stream)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(gs):
-            with torch.cuda.graph(graph, stream=gs):
-                per_step = parpa.parse_into(dfa, schema, d, cols, cap, st, stream=gs)
-        torch.cuda.synchronize()
-        for _ in range(args.warmup):
-            graph.replay()
-        torch.cuda.synchronize()
-        assert parpa.stats_from_tensor(st)["records"] == g.records
-
-    clocks = Clocks()
-    clocks.start(gpu)
-    parpa.set_profiling(not use_graph)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches = 0
-    e0.record(stream)
-    for _ in range(args.steps):
-        if use_graph:
-            graph.replay()
-            launches += per_step
-        else:
-            launches += step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    ms_total = e0.elapsed_time(e1)
-    if use_graph:                                             # per-kernel times from one eager step
-        parpa.set_profiling(True)
-        step()
-        torch.cuda.synchronize()
-    ktimes = parpa.last_kernel_times()
-    parpa.set_profiling(False)
-    clk = clocks.stop()
-    ms_step = ms_total / args.steps
-    if dist:
-        t = torch.tensor([ms_step], dtype=torch.float64, device=coll)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
-        tb = torch.tensor([n], dtype=torch.float64, device=coll)
-        dist.all_reduce(tb, op=dist.ReduceOp.SUM)
-        total_bytes = float(tb.item())
-    else:
-        total_bytes = float(n)
-    value = total_bytes / (ms_step * 1e-3) / 1e9
-
-    # roofline of the dominant kernel (algorithmic bytes)
-    T = sum(1 for t in w.types if t != datagen.SPAN)
-    R = stats["records"]
-    alg_bytes = n + R * w.C * 12 + R * T * 9
-    # dominant kernel of the step: k_emit (reads the input, writes every output column)
-    dom = "k_emit"
-    kt = [ms for name, ms in ktimes if name == dom]
-    per_kernel = {}
-    for name, ms in ktimes:
-        per_kernel.setdefault(name, []).append(ms)
-    peak, peak_src = load_peaks()
-    roof = None
-    if kt:
-        kms = statistics.mean(kt)
-        achieved = alg_bytes / (kms * 1e-3) / 1e9
-        tr = load_traffic(args.config, n, args.timestamps)
-        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": tr, "kernel": dom, "kernel_ms": round(kms, 4),
-                "algorithmic_bytes_per_launch": int(alg_bytes), "peak_source": peak_src,
-                "share_of_step": round(kms / ms_step, 4),
-                "step_achieved": round(alg_bytes * (total_bytes / n) / (ms_step * 1e-3) / 1e9, 1),
-                "step_frac": round(alg_bytes * (total_bytes / n) / (ms_step * 1e-3) / 1e9 / peak, 4)}
-
-    cpu = None
-    if rank == 0 and not args.no_cpu:
-        cpu = cpu_baseline(args.config, data_host, timestamps=args.timestamps)
-
-    e2e = None
-    if rank == 0 and world == 1 and not args.no_e2e:
-        e2e = run_e2e(parpa, dfa, schema, data_host, cap, w, args.e2e_steps)
-
-    if rank == 0:
-        line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-                "config": {"workload": args.config, "description": CONFIG_LABEL[args.config], "timestamps": bool(args.timestamps),
-                           "bytes_per_gpu": n, "records_per_gpu": R, "columns": w.C, "typed_columns": T,
-                           "dialect": w.dialect, "path": "parse_into (k_pass1, k_tau_scan, k_pass2, k_seg_scan, k_emit, k_finalize, k_deferred)" if world == 1 else
-                           "range_begin + allgather(tau) + range_count + allgather(counts) + range_emit",
-                           "l2": "input >> 126 MB L2 (no flush needed)" if n > (512 << 20) else
-                                 "input < L2: outputs and inputs stay L2-resident between steps (latency-bound size)",
-                           "launch": "CUDA graph replay per step (kernel_ms from one eager step)" if use_graph else "eager",
-                           "generate_s": round(t_gen, 1),
-                           "kernel_ms": {k: round(statistics.mean(v), 4) for k, v in per_kernel.items()}},
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk}
-        print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
+def full_parity(config, w, cols, stats, R, workers=None):
+    """Compare every row of every device column with the oracle, chunk by chunk in parallel threads (the
+    oracle and the generator release the GIL).  Returns a dict for the JSON line."""
+    import numpy as np
+    t0 = time.perf_counter()
+    workers = workers or max(1, (os.cpu_count() or 2) - 1)
+    m = max(1000, -(-R // (workers * 6)))
+    starts = list(range(0, R, m))
+    with cf.ThreadPoolExecutor(workers) as ex:
+        res = list(ex.map(lambda r0: _oracle_chunk(config, w, r0, min(m, R - r0)), starts))
+    base = np.cumsum([0] + [x[0] for x in res[:-1]]).astype(np.uint64)
+    bad = []
+    if sum(x[1] for x in res) != R:
+        bad.append(f"records oracle {sum(x[1] for x in res)} vs device {R}")
+    if any(x[2] != 0 for x in res) or sum(x[3] for x in res) != stats["missing_records"] \
+            or sum(x[4] for x in res) != stats["extra_fields"]:
+        bad.append("status / missing / extra counts")
+    for c in range(w.C):
+        off = cols[c].offset.cpu().numpy().view(np.uint64)[:R]
+        ln = cols[c].length.cpu().numpy().view(np.uint32)[:R]
+        val = cols[c].value.cpu().numpy().view(np.int64)[:R] if cols[c].value is not None else None
+        ok = cols[c].valid.cpu().numpy()[:R] if cols[c].valid is not None else None
+        for k, r0 in enumerate(starts):
+            r1 = min(R, r0 + m)
+            d = [_digest(off[r0:r1] - base[k]), _digest(np.ascontiguousarray(ln[r0:r1]))]
+            if val is not None:
+                d += [_digest(np.ascontiguousarray(val[r0:r1])), _digest(np.ascontiguousarray(ok[r0:r1]))]
+            if d != res[k][5][c]:
+                bad.append(f"column {c} rows [{r0}, {r1})")
+                break
+        del off, ln, val, ok
+    return {"checked": f"all {R} rows x {w.C} columns (offset, length; value + valid of typed columns) and "
+                       f"the record / missing / extra counts vs the oracle, {len(starts)} generator record "
+                       f"ranges on {workers} host threads", "mismatches": len(bad), "detail": bad[:5],
+            "ok": not bad, "seconds": round(time.perf_counter() - t0, 1)}
 
 
 def run_e2e(parpa, dfa, schema, data_host, cap, w, steps):
@@ -435,6 +331,248 @@ def run_e2e(parpa, dfa, schema, data_host, cap, w, steps):
     return {"value": round(data_host.numel() / t / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": int(data_host.numel()), "d2h_bytes_per_step": int(out_bytes + 56),
             "ms_per_step": round(t * 1e3, 2), "api": "parpa_parse_host (pinned host input and columns)"}
+
+
+def run_config(args, config, ctx, main=True):
+    """Generate, parse (untimed plan + warm-up), time `steps` parses, check parity; returns the record."""
+    import numpy as np
+    import torch
+    import datagen
+    import paper_1905_13415_b200 as parpa
+    from paper_1905_13415_b200 import distributed as pdist
+
+    world, rank, dist, coll, gpu = ctx["world"], ctx["rank"], ctx["dist"], ctx["coll"], ctx["gpu"]
+    w = workload(config, args.timestamps)
+    dfa = parpa.Dfa.dialect(w.dialect)
+    schema = parpa.Schema(list(w.types))
+
+    t_gen = time.time()
+    data_host, left_host, block_len, cut0, g = gen_range(config, rank, world, records=args.records)
+    t_gen = time.time() - t_gen
+    n = data_host.numel()
+    d = torch.empty(n + 64, dtype=torch.uint8, device="cuda")[:n]
+    d.copy_(data_host, non_blocking=True)
+    left = left_host.cuda() if left_host is not None else None
+    base = 0
+    if world > 1:
+        lens = torch.tensor([block_len], dtype=torch.int64, device=coll)
+        all_lens = [torch.zeros_like(lens) for _ in range(world)]
+        dist.all_gather(all_lens, lens)
+        base = sum(int(x.item()) for x in all_lens[:rank]) + cut0
+    torch.cuda.synchronize()
+
+    # capacity from an untimed scan pass (records of this range)
+    stream = torch.cuda.current_stream()
+    if world == 1:
+        res_plan = parpa.parse(dfa, schema, d)
+        cap = res_plan.records
+        assert res_plan.status == 0 and cap == g.records, (res_plan.stats, g.records)
+        del res_plan
+    else:
+        cap = g.records + 2
+    cols = parpa.alloc_columns(schema, cap)
+    st = parpa.new_stats_tensor()
+    is_last = rank == world - 1
+
+    def step():
+        if world == 1:
+            return parpa.parse_into(dfa, schema, d, cols, cap, st)
+        pdist.parse_sharded(dfa, schema, d, base, cols, cap, st, left=left, is_last=is_last,
+                            exchange_device=coll)
+        return 7                                  # range_begin 2 + range_count 2 + range_emit 3
+
+    parpa.set_profiling(False)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stats = parpa.stats_from_tensor(st)
+    assert stats["status"] == 0, stats
+    if world == 1:
+        assert stats["records"] == g.records, (stats, g.records)
+    else:                                                     # the ranks' records add up exactly
+        tr = torch.tensor([stats["records"], g.records], dtype=torch.float64, device=coll)
+        dist.all_reduce(tr, op=dist.ReduceOp.SUM)
+        assert int(tr[0].item()) == int(tr[1].item()), (stats, tr)
+
+    # launch-bound inputs (cfg1, 1 MB): each step is one replay of a CUDA graph of the parse
+    use_graph = world == 1 and (args.graph or (config == "cfg1" and not args.no_graph))
+    graph, per_step = None, 0
+    if use_graph:
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(gs):
+            with torch.cuda.graph(graph, stream=gs):
+                per_step = parpa.parse_into(dfa, schema, d, cols, cap, st, stream=gs)
+        torch.cuda.synchronize()
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+        assert parpa.stats_from_tensor(st)["records"] == g.records
+
+    # the timed region: production launch sequence, no profiling events between the kernels
+    steps = args.steps * (20 if use_graph else 1)
+    clocks = Clocks()
+    clocks.start(gpu)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    e0.record(stream)
+    for _ in range(steps):
+        if use_graph:
+            graph.replay()
+            launches += per_step
+        else:
+            launches += step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms_total = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    # per-kernel device times from separate profiled steps (CUDA events around every launch)
+    parpa.set_profiling(True)
+    for _ in range(2 if config != "cfg1" else 5):
+        step()
+    torch.cuda.synchronize()
+    ktimes = parpa.last_kernel_times()
+    parpa.set_profiling(False)
+    ms_step = ms_total / steps
+    if dist:
+        t = torch.tensor([ms_step], dtype=torch.float64, device=coll)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+        tb = torch.tensor([n], dtype=torch.float64, device=coll)
+        dist.all_reduce(tb, op=dist.ReduceOp.SUM)
+        total_bytes = float(tb.item())
+    else:
+        total_bytes = float(n)
+    value = total_bytes / (ms_step * 1e-3) / 1e9
+
+    # roofline of the dominant kernel (algorithmic bytes, SURVEY §8d)
+    stats = parpa.stats_from_tensor(st)
+    T = sum(1 for t in w.types if t != datagen.SPAN)
+    R = stats["records"]
+    alg_bytes = n + R * w.C * 12 + R * T * 9
+    dom = "k_emit"                     # reads the input, writes every output column (DESIGN.md §5)
+    per_kernel = {}
+    for name, ms in ktimes:
+        per_kernel.setdefault(name, []).append(ms)
+    kt = per_kernel.get(dom, [])
+    peak, peak_src = load_peaks()
+    roof = None
+    if kt:
+        kms = statistics.mean(kt)
+        achieved = alg_bytes / (kms * 1e-3) / 1e9
+        tr = load_traffic(config, n, args.timestamps)
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": tr, "kernel": dom, "kernel_ms": round(kms, 4),
+                "algorithmic_bytes_per_launch": int(alg_bytes), "peak_source": peak_src,
+                "share_of_step": round(kms / ms_step, 4),
+                "step_achieved": round(alg_bytes * (total_bytes / n) / (ms_step * 1e-3) / 1e9, 1),
+                "step_frac": round(alg_bytes * (total_bytes / n) / (ms_step * 1e-3) / 1e9 / peak, 4)}
+
+    parity = None
+    if world == 1 and args.parity == "full":
+        parity = full_parity(config, w, cols, stats, R)
+        if not parity["ok"]:
+            print(f"PARITY FAILURE {config}: {parity['detail']}", file=sys.stderr, flush=True)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu and main:
+        cpu = cpu_baseline(config, data_host, timestamps=args.timestamps)
+    e2e = None
+    if rank == 0 and world == 1 and not args.no_e2e and main:
+        e2e = run_e2e(parpa, dfa, schema, data_host, cap, w, args.e2e_steps)
+
+    rec = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": steps,
+           "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+           "config": {"workload": config, "description": CONFIG_LABEL[config], "timestamps": bool(args.timestamps),
+                      "bytes_per_gpu": n, "records_per_gpu": R, "columns": w.C, "typed_columns": T,
+                      "dialect": w.dialect,
+                      "path": ("parse_into (" + ", ".join(per_kernel) + ")") if world == 1 else
+                              "range_begin + allgather(tau) + range_count + allgather(counts) + range_emit",
+                      "l2": "input >> 126 MB L2 (no flush needed)" if n > (512 << 20) else
+                            "input < L2: outputs and inputs stay L2-resident between steps (latency-bound size)",
+                      "launch": "CUDA graph replay per step" if use_graph else "eager",
+                      "generate_s": round(t_gen, 1),
+                      "kernel_ms": {k: round(statistics.mean(v), 4) for k, v in per_kernel.items()},
+                      "kernel_ms_source": "separate profiled steps after the timed region"},
+           "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+           "parity": parity}
+    del cols, d, data_host, left, st
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return rec
+
+
+def relaunch(args):
+    """--gpus N > 1 without torchrun: one process per GPU under torch.distributed.run."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=None, choices=list(CONFIG_LABEL),
+                    help="one config only (default: yelp main line + taxi / clf / cfg1 sub-records at N=1)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-subs", action="store_true", help="main config only")
+    ap.add_argument("--parity", default="full", choices=["full", "none"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-sample-bytes", type=int, default=150_000_000)
+    ap.add_argument("--records", type=int, default=0, help="override records per rank (profiling runs)")
+    ap.add_argument("--timestamps", action="store_true", help="type the datetime columns as TIMESTAMP (SURVEY N2)")
+    ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays of the parse (default for cfg1)")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches even for cfg1")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    # test switch: every rank on cuda:0 with gloo collectives (validates the sharded path on one GPU;
+    # never used for a reported number)
+    shared = os.environ.get("PARPA_BENCH_SHARED_GPU") == "1"
+    gpu = 0 if shared else local
+    coll = "cpu" if shared else "cuda"
+    torch.cuda.set_device(gpu)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = {"world": world, "rank": rank, "dist": dist, "coll": coll, "gpu": gpu}
+    main_cfg = args.config or "yelp"
+    subs = [] if (args.config or world > 1 or args.no_subs or args.records) else SUB_CONFIGS
+    line = run_config(args, main_cfg, ctx, main=True)
+    if subs:
+        line["configs"] = [run_config(args, c, ctx, main=False) for c in subs]
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -471,6 +472,23 @@ struct parpa_result {
   parpa_stats stats;
 };
 
+// A plan may be counted / emitted more than once: each call first clears the control words and look-back
+// flags its kernels accumulate into (a repeated call used to run on stale tickets and flags).
+static int reset_scan_state(parpa_plan *p) {
+  Ctrl *c = p->w.ctrl;
+  CK(cudaMemsetAsync(&c->ticket2, 0, sizeof(c->ticket2), p->s));
+  CK(cudaMemsetAsync(&c->inv_neg, 0, sizeof(c->inv_neg), p->s));
+  if (p->w.nblk) CK(cudaMemsetAsync(p->w.bflag, 0, (size_t)p->w.nblk * 4, p->s));
+  return PARPA_OK;
+}
+static int reset_emit_state(parpa_plan *p, cudaStream_t s) {
+  Ctrl *c = p->w.ctrl;
+  CK(cudaMemsetAsync(&c->n_defer, 0, offsetof(Ctrl, inv_neg) - offsetof(Ctrl, n_defer), s));
+  CK(cudaMemsetAsync(&c->n_missing, 0, sizeof(Ctrl) - offsetof(Ctrl, n_missing), s));
+  return PARPA_OK;
+}
+
+
 extern "C" {
 
 const char *parpa_last_error(void) { return t_last_error; }
@@ -648,6 +666,7 @@ int parpa_plan_emit(parpa_plan *p, const parpa_schema *sch, const parpa_column *
   a.strict = sch->strict;
   a.cap = p->records;
   a.stats = d_stats ? (Stats *)d_stats : p->w.stats;
+  if ((rc = reset_emit_state(p, s))) return rc;
   rc = launch_emit(a, p->dfa->k, ck, s, nullptr);
   if (!rc) rc = launch_tail(a, p->dfa->k, ck, s, nullptr);
   prof_end();
@@ -1107,6 +1126,7 @@ int parpa_range_begin(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len
 
 int parpa_range_count(parpa_plan *p, uint32_t entry_state, parpa_counts *out) {
   if (!p || !out || entry_state >= p->dfa->S) return PARPA_EINVAL;
+  if (int rc0 = reset_scan_state(p)) return rc0;
   p->a.seed_dev = p->dfa->dmap[entry_state];
   int rc = launch_half2(p->a, p->dfa->k, p->s, nullptr);
   prof_end();
@@ -1138,6 +1158,7 @@ int parpa_range_emit(parpa_plan *p, const parpa_schema *sch, const parpa_context
   a.left = left;
   a.left_len = left_len;
   a.is_last = is_last;
+  if ((rc = reset_emit_state(p, s))) return rc;
   rc = launch_emit(a, p->dfa->k, ck, s, nullptr);
   if (!rc) rc = launch_tail(a, p->dfa->k, ck, s, nullptr);
   prof_end();

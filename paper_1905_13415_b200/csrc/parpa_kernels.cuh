@@ -428,6 +428,7 @@ __device__ __forceinline__ void push_defer(const KArgs &a, const ColDesc *cd, un
                                            unsigned long long ld, unsigned long long row, uint32_t c, uint32_t ic) {
   uint32_t idx = atomicAdd(&a.ctrl->n_defer, 1u);
   if (idx < a.dq_cap) {
+    cd->valid[row] = 0;              // k_deferred's overflow sweep must only see markers of this launch
     a.dq[idx] = DeferItem{fd, ld, row, c, ic};
   } else {
     cd->valid[row] = ic ? VALID_REDO_IC : VALID_REDO;
@@ -1269,8 +1270,8 @@ __global__ void k_deferred(const KArgs a, const DfaK dfa, const ColsK colsk) {
     __threadfence();
     // (modulo the grid: a plan emitted more than once keeps counting)
     if ((atomicAdd(&a.ctrl->deferred_done, 1u) + 1u) % gridDim.x == 0u && a.stats &&
-        *reinterpret_cast<volatile unsigned int *>(&a.ctrl->unsupported) && a.stats->status == ST_OK)
-      a.stats->status = ST_EUNSUPPORTED;
+        *reinterpret_cast<volatile unsigned int *>(&a.ctrl->unsupported) && a.stats->status != ST_EFORMAT)
+      a.stats->status = ST_EUNSUPPORTED;             // k_finalize's order: EFORMAT > EUNSUPPORTED > the rest
   }
 }
 

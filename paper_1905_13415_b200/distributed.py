@@ -80,11 +80,16 @@ def exchange(dfa, local_tau: list, count_fn, group=None, device=None):
 
 
 def parse_sharded(dfa, schema, data, base: int, columns, capacity: int, stats_tensor, left=None,
-                  is_last: bool = True, group=None, stream=None, exchange_device=None):
+                  is_last: bool | None = None, group=None, stream=None, exchange_device=None):
     """Parse this rank's range after the summary exchange.  data / left: CUDA uint8 tensors.
     Every pass runs once per rank: S1-S3 (range_begin) -> allgather τ -> S4-S5 from the entry
-    state (range_count) -> allgather counts -> S6-S7 with the ⊕-prefix (range_emit)."""
+    state (range_count) -> allgather counts -> S6-S7 with the ⊕-prefix (range_emit).  ``is_last``
+    (the range ends the input, so the end-of-input action applies) defaults to "this is the group's
+    last rank"."""
+    import torch.distributed as dist
     from . import RangePlan
+    if is_last is None:
+        is_last = dist.get_rank(group) == dist.get_world_size(group) - 1
     plan = RangePlan(dfa, data, base, stream)
     try:
         e, prefix, _ = exchange(dfa, plan.tau, plan.count, group,

@@ -160,3 +160,34 @@ def test_virtual_ranks_adversarial_clf():
         if t != oracle.SPAN:
             assert np.array_equal(ok, ora.valid[c]), c
             assert np.array_equal(val, ora.value[c]), c
+
+
+def test_range_plan_repeated_count_and_emit():
+    """A range plan counted and emitted more than once: every repeat must return the same
+    counts and columns as the first call and as the oracle (the control words and look-back flags are
+    cleared per call)."""
+    w = datagen.WORKLOADS["cfg1"]
+    data, g = datagen.generate("cfg1", 300_000)
+    ora = oracle.parse(w.dialect, data, w.C, list(w.types))
+    dfa = parpa.Dfa.dialect(w.dialect)
+    schema = parpa.Schema(list(w.types))
+    plan = parpa.RangePlan(dfa, dev(data), 0)
+    try:
+        c1 = bytes(plan.count(dfa.start))
+        c2 = bytes(plan.count(dfa.start))
+        assert c1 == c2
+        prefix = pdist.prefix_counts([], 0)
+        for _ in range(3):
+            cols = parpa.alloc_columns(schema, ora.R)
+            st = parpa.new_stats_tensor()
+            plan.emit(schema, prefix, cols, ora.R, st, is_last=True)
+            s = parpa.stats_from_tensor(st)
+            assert s["status"] == 0 and s["records"] == ora.R and s["missing_records"] == ora.n_missing, s
+            for c, t in enumerate(w.types):
+                assert np.array_equal(to_np(cols[c].offset).view(np.uint64)[:ora.R], ora.offset[c])
+                assert np.array_equal(to_np(cols[c].length).view(np.uint32)[:ora.R], ora.length[c])
+                if t != datagen.SPAN:
+                    assert np.array_equal(to_np(cols[c].value).view(np.int64)[:ora.R], ora.value[c])
+                    assert np.array_equal(to_np(cols[c].valid).view(np.uint8)[:ora.R], ora.valid[c])
+    finally:
+        plan.close()
