@@ -49,7 +49,7 @@ int cuda_status(cudaError_t e) {
 struct DevCfg {
   bool init = false;
   int sms = 0;
-  int occ_pass1 = 0, occ_pass2 = 0, occ_emit = 0, occ_fused = 0;
+  int occ_pass1 = 0, occ_pass2 = 0, occ_emit = 0;
 };
 std::mutex g_mu;
 DevCfg g_dev[64];
@@ -69,9 +69,6 @@ int dev_cfg(DevCfg **out) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass1, k_pass1, PASS_WARPS * 32, PASS_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass2, k_pass2, PASS_WARPS * 32, PASS_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit<false>, EMIT_WARPS * 32, EMIT_SMEM));
-    CK(cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F_SMEM));
-    CK(cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)F_SMEM));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_fused, k_fused<false>, F_WARPS * 32, F_SMEM));
     if (getenv("PARPA_DEBUG")) {
       auto show = [](const char *n, const void *f) {
         cudaFuncAttributes fa;
@@ -85,7 +82,6 @@ int dev_cfg(DevCfg **out) {
       show("k_seg_scan", (const void *)k_seg_scan);
       show("k_emit", (const void *)k_emit<false>);
       show("k_emit<ts>", (const void *)k_emit<true>);
-      show("k_fused", (const void *)k_fused<false>);
       fprintf(stderr, "[parpa] occ pass1=%d pass2=%d emit=%d sms=%d\n", c.occ_pass1, c.occ_pass2, c.occ_emit, c.sms);
     }
     cudaMemPool_t pool;
@@ -145,8 +141,6 @@ struct Work {
   unsigned long long *tau_desc = nullptr;
   uint32_t *bflag = nullptr;
   Ctrl *ctrl = nullptr;
-  unsigned long long *gdesc = nullptr;
-  uint64_t gstride = 0;
   uint32_t *lex = nullptr, *wtau = nullptr, *tot_tau = nullptr;
   uint32_t *wpre = nullptr;
   uint4 *wseg = nullptr;
@@ -168,14 +162,11 @@ int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cu
   w.ntiles = (uint32_t)nt64;
   w.nblk = (uint32_t)((nt64 + SCAN_TILE - 1) / SCAN_TILE);
   size_t nt = std::max<size_t>(w.ntiles, 1), nb = std::max<size_t>(w.nblk, 1);
-  // the look-back descriptors serve k_seg_scan (scan blocks) or k_fused (group tiles), never both
-  const size_t ngt = (nt + FG_CW - 1) / FG_CW;
   w.dq_cap = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(4096, len / 512), 1u << 24);
   size_t o = 0;
   size_t o_tau = o; o = align_up(o + nb * 8);
   size_t o_flag = o; o = align_up(o + nb * 4);
   size_t o_ctrl = o; o = align_up(o + sizeof(Ctrl));
-  size_t o_gd = o; o = align_up(o + 7 * ngt * 8);
   size_t zero = o;
   size_t o_lex = o; o = align_up(o + nt * 32 * 4);
   size_t o_wtau = o; o = align_up(o + nt * 4);
@@ -195,8 +186,6 @@ int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cu
   w.tau_desc = (unsigned long long *)(b + o_tau);
   w.bflag = (uint32_t *)(b + o_flag);
   w.ctrl = (Ctrl *)(b + o_ctrl);
-  w.gdesc = (unsigned long long *)(b + o_gd);
-  w.gstride = ngt;
   w.lex = (uint32_t *)(b + o_lex);
   w.wtau = (uint32_t *)(b + o_wtau);
   w.wpre = (uint32_t *)(b + o_went);
@@ -251,8 +240,6 @@ void make_args(KArgs &a, const Work &w, const uint8_t *in, uint64_t len) {
   a.chunk_state = w.chunk_state;
   a.masks = w.masks;
   a.ctrl = w.ctrl;
-  a.gdesc = w.gdesc;
-  a.gstride = w.gstride;
   a.dq = w.dq;
   a.dq_cap = w.dq_cap;
   a.is_last = 1;
@@ -381,46 +368,6 @@ int launch_emit(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, 
       CK(launch_k(k_emit<false>, grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s, true, a, ck));
   }
   CK(cudaGetLastError());
-  if (launches) (*launches)++;
-  return PARPA_OK;
-}
-
-// S4-S7 in one kernel (k_fused): re-simulation, record/column look-back scan, partition + conversion
-int launch_fused(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, uint32_t *launches) {
-  if (a.ntiles == 0) return PARPA_OK;
-  DevCfg *dc;
-  int rc = dev_cfg(&dc);
-  if (rc) return rc;
-  const uint32_t ngt = (a.ntiles + FG_CW - 1) / FG_CW;
-  const unsigned grid = (unsigned)std::max(1, std::min(std::max(dc->occ_fused, 1) * dc->sms,
-                                                       (int)((ngt + FG_GROUPS - 1) / FG_GROUPS)));
-  static const bool fprof = getenv("PARPA_FPROF") && getenv("PARPA_FPROF")[0] == '1';
-  KArgs ap = a;
-  unsigned long long *prof = nullptr;
-  if (fprof) {
-    CK(cudaMallocAsync(&prof, grid * 16 * 8, s));
-    CK(cudaMemsetAsync(prof, 0, grid * 16 * 8, s));
-    ap.prof = prof;
-  }
-  {
-    Launch L(s, "k_fused");
-    if (has_timestamps(a, ck)) CK(launch_k(k_fused<true>, grid, F_WARPS * 32, F_SMEM, s, true, ap, k, ck));
-    else CK(launch_k(k_fused<false>, grid, F_WARPS * 32, F_SMEM, s, true, ap, k, ck));
-  }
-  CK(cudaGetLastError());
-  if (fprof) {
-    std::vector<unsigned long long> h(grid * 16);
-    CK(cudaMemcpyAsync(h.data(), prof, grid * 16 * 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    unsigned long long t[16] = {0};
-    for (unsigned b = 0; b < grid; b++)
-      for (int i = 0; i < 16; i++) t[i] += h[b * 16 + i];
-    const double it = t[0] ? (double)t[0] : 1.0;
-    fprintf(stderr, "[parpa fprof] iters=%llu per-iter cycles: pass2=%.0f bar1=%.0f e1=%.0f lookback(w0)=%.0f "
-            "bar2=%.0f e2=%.0f | rounds/iter=%.2f spins/iter=%.2f scanwait=%.0f\n", t[0], t[1] / it, t[2] / it, t[3] / it,
-            t[4] / it, t[5] / it, t[6] / it, t[7] / it, t[8] / it, t[9] / it);
-    cudaFreeAsync(prof, s);
-  }
   if (launches) (*launches)++;
   return PARPA_OK;
 }
@@ -749,12 +696,6 @@ void parpa_result_free(parpa_result *r) {
 }
 
 // ---- single-pass capacity path ------------------------------------------------------------------
-// parse_into / parse_range run S4-S7 as the staged kernels (k_pass2 + k_seg_scan + k_emit);
-// PARPA_FUSED=1 selects the fused kernel k_fused (measured slower, kept for A/B).
-static bool use_fused() {
-  static const bool on = getenv("PARPA_FUSED") && getenv("PARPA_FUSED")[0] == '1';
-  return on;
-}
 static int parse_into_impl(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_bytes, uint64_t len,
                            const parpa_column *cols, uint64_t cap, parpa_stats *d_stats, cudaStream_t s,
                            uint32_t seed_dev, const Seg &seed, uint64_t base, const uint8_t *left,
@@ -784,13 +725,8 @@ static int parse_into_impl(const parpa_dfa *dfa, const parpa_schema *sch, const 
     a.left_len = left_len;
     a.is_last = is_last;
     uint32_t n = 0;
-    if (use_fused()) {
-      rc = launch_passes(MODE_TAU, a, dfa->k, s, &n);
-      if (!rc) rc = launch_fused(a, dfa->k, ck, s, &n);
-    } else {
-      rc = launch_passes(MODE_COUNT, a, dfa->k, s, &n);
-      if (!rc) rc = launch_emit(a, dfa->k, ck, s, &n);
-    }
+    rc = launch_passes(MODE_COUNT, a, dfa->k, s, &n);
+    if (!rc) rc = launch_emit(a, dfa->k, ck, s, &n);
     if (!rc) rc = launch_tail(a, dfa->k, ck, s, &n);
     if (launches) *launches = n;
   }

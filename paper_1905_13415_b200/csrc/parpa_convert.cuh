@@ -369,6 +369,30 @@ __device__ __noinline__ int conv_timestamp(Src &s, long long &out) {
 }
 
 // ---- exact slow path ------------------------------------------------------------------------
+// The multi-precision decimal below (dec_* : digit shifts, round-half-even, float bits) follows the
+// structure of the Go standard library's strconv "decimal" conversion (decimal.go / atof.go), written
+// anew in C++ for this device tier.  That code's notice, reproduced as its license requires:
+//
+//   Copyright (c) 2009 The Go Authors. All rights reserved.
+//
+//   Redistribution and use in source and binary forms, with or without modification, are permitted
+//   provided that the following conditions are met:
+//     * Redistributions of source code must retain the above copyright notice, this list of
+//       conditions and the following disclaimer.
+//     * Redistributions in binary form must reproduce the above copyright notice, this list of
+//       conditions and the following disclaimer in the documentation and/or other materials provided
+//       with the distribution.
+//     * Neither the name of Google Inc. nor the names of its contributors may be used to endorse or
+//       promote products derived from this software without specific prior written permission.
+//
+//   THIS SOFTWARE IS PROVIDED BY THE COPYRIGHT HOLDERS AND CONTRIBUTORS "AS IS" AND ANY EXPRESS OR
+//   IMPLIED WARRANTIES, INCLUDING, BUT NOT LIMITED TO, THE IMPLIED WARRANTIES OF MERCHANTABILITY AND
+//   FITNESS FOR A PARTICULAR PURPOSE ARE DISCLAIMED. IN NO EVENT SHALL THE COPYRIGHT OWNER OR
+//   CONTRIBUTORS BE LIABLE FOR ANY DIRECT, INDIRECT, INCIDENTAL, SPECIAL, EXEMPLARY, OR CONSEQUENTIAL
+//   DAMAGES (INCLUDING, BUT NOT LIMITED TO, PROCUREMENT OF SUBSTITUTE GOODS OR SERVICES; LOSS OF USE,
+//   DATA, OR PROFITS; OR BUSINESS INTERRUPTION) HOWEVER CAUSED AND ON ANY THEORY OF LIABILITY, WHETHER
+//   IN CONTRACT, STRICT LIABILITY, OR TORT (INCLUDING NEGLIGENCE OR OTHERWISE) ARISING IN ANY WAY OUT
+//   OF THE USE OF THIS SOFTWARE, EVEN IF ADVISED OF THE POSSIBILITY OF SUCH DAMAGE.
 constexpr int DEC_MAX = 800;
 struct Decimal {
   uint8_t d[DEC_MAX];            // digit values 0..9, most significant first; value = 0.d × 10^dp

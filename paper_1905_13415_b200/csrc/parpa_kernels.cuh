@@ -84,7 +84,7 @@ struct Ctrl {
   unsigned int deferred_done;        // k_deferred blocks finished (the last one settles the status)
   unsigned int emit_ticket;          // k_emit: next warp tile to take (reset by the last warp out)
   unsigned int emit_done;            // k_emit: warps finished
-  unsigned int gticket;              // k_fused: next group tile
+  unsigned int pad0;
 };
 
 struct TileInfo {
@@ -116,8 +116,6 @@ struct KArgs {
   unsigned long long *tau_desc;      // [nblk] decoupled look-back descriptors (flag << 32) | nibble τ
   uint32_t *bflag;                   // [nblk] Seg look-back flags
   Seg *bagg, *bincl;                 // [nblk] block aggregate / inclusive prefix (valid once flagged)
-  unsigned long long *gdesc;         // k_fused look-back descriptors [7][gstride] (zeroed per call)
-  unsigned long long gstride;
   uint32_t *tot_tau;                 // τ of the whole range (nibble form, seed not applied)
   Seg *tot_seg;                      // Seg of the whole range (unseeded; the seed is applied on use)
   TileInfo *tinfo;                   // [ntiles]
@@ -567,10 +565,6 @@ struct alignas(16) WarpScratch {
   uint16_t dlist[FCAP];                     // delimiter positions (tile-local) | record bit << 15
   uint32_t dmask[WT / 32], kmask[WT / 32];  // DATA / CTRL bits of the tile, 32 per word
   uint16_t kpre[WT / 32];                   // CTRL bits before each word
-  // E1 results read by E2 (written by lane 0): field counts, CTRL total, field 0's tile-local part
-  uint32_t dense, nf, nrec, ktot, n_before, extra_after;
-  int32_t fd0, ld0;
-  uint32_t fl0;
 };
 #ifndef PARPA_E2_ROWS_MIN
 #define PARPA_E2_ROWS_MIN 16
@@ -698,11 +692,11 @@ __device__ __forceinline__ void write_value_tile(const KArgs &a, const ColDesc *
 __device__ __forceinline__ uint32_t kcount(const WarpScratch *ws, uint32_t x) {   // CTRL bytes before x
   return ws->kpre[x >> 5] + __popc(ws->kmask[x >> 5] & ((1u << (x & 31u)) - 1u));
 }
-// E1 (tile-local, independent of the prefix): delimiter list, record ends, DATA / CTRL words, the
-// per-field entries k >= 1, field 0's local part, and the extra-field counts that do not depend on
-// the entry column.  Results that E2 needs are left in the warp's scratch.
-__device__ void emit_tile_local(const KArgs &a, WarpScratch *ws, unsigned long long Dm, unsigned long long Fm,
-                                unsigned long long Rm, unsigned long long Vm) {
+template <bool TS>
+__device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, const Seg &prefix,
+                          unsigned long long Dm, unsigned long long Fm, unsigned long long Rm,
+                          unsigned long long Vm, unsigned long long tbase_g, unsigned long long cbase,
+                          EmitCounters &cnt) {
   const int lane = threadIdx.x & 31;
   const unsigned long long Km = Vm & ~Dm & ~Fm;
   // per-lane (delimiters << 16 | records) and CTRL counts -> exclusive offsets, tile totals
@@ -716,9 +710,10 @@ __device__ void emit_tile_local(const KArgs &a, WarpScratch *ws, unsigned long l
   }
   const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
   const uint32_t nf = tot >> 16, nrec = tot & 0xFFFFu;
-  if (nf > (uint32_t)FCAP || nrec >= (uint32_t)RCAP) {       // warp-uniform: dense tile, direct path in E2
-    if (lane == 0) ws->dense = 1u;
-    __syncwarp();
+  if (nf > (uint32_t)FCAP || nrec >= (uint32_t)RCAP) {       // warp-uniform: dense tile, direct path
+    SegT sagg;
+    const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
+    emit_chunk<TS>(a, cols, seg_op(prefix, segt_to_seg(sex, tbase_g)), Dm, Fm, Rm, Vm, cbase, cnt);
     return;
   }
   // ---- E1a ----
@@ -780,121 +775,25 @@ __device__ void emit_tile_local(const KArgs &a, WarpScratch *ws, unsigned long l
   }
   __syncwarp();
   const uint32_t ktot = __shfl_sync(0xffffffffu, kinc, 31);    // CTRL bytes in the tile (warp-uniform)
-  // fields terminated up to and including the first record delimiter take columns c0, c0 + 1, ...;
-  // the others are counted as extra here when their column (position in their record) is >= C
-  const uint32_t n_before = nrec ? (ws->rows[0] & 0xFFFFu) : nf;
-  uint32_t extra = 0;
-  if (ktot == 0u) {
+  const bool plain = ktot == 0u;
+  if (plain) {
     // E1b' (no CTRL byte in the tile): field k is the byte range between delimiters k-1 and k, all DATA,
-    // so E2 reads it straight from the delimiter list; only field 0 needs its local part.
+    // so E2 reads it straight from the delimiter list.  Only field 0 (which may continue a field of an
+    // earlier tile) needs an entry; extra fields (column >= C) are counted per row.
+    const uint32_t c0 = prefix.col;
+    uint32_t extra = 0;
     const uint32_t last_end = nrec ? (ws->rows[nrec - 1] & 0xFFFFu) : 0u;
     const uint32_t nrows = nrec + (nf > last_end ? 1u : 0u);
-    for (uint32_t j = 1 + lane; j < nrows; j += 32) {
-      const uint32_t start = ws->rows[j - 1] & 0xFFFFu, end = j < nrec ? (ws->rows[j] & 0xFFFFu) : nf;
-      if (end - start > a.C) extra += end - start - a.C;
+    for (uint32_t j = lane; j < nrows; j += 32) {
+      const uint32_t start = j ? (ws->rows[j - 1] & 0xFFFFu) : 0u, end = j < nrec ? (ws->rows[j] & 0xFFFFu) : nf;
+      const uint32_t cs = j ? 0u : c0, hi = cs + (end - start), lo = max(a.C, cs);
+      if (hi > lo) extra += hi - lo;
     }
-    extra = __reduce_add_sync(0xffffffffu, extra);
     if (lane == 0 && nf) {
       const uint32_t p = ws->dlist[0] & 0x7FFu;
-      ws->fd0 = p ? 0 : -1;
-      ws->ld0 = (int)p - 1;
-      ws->fl0 = 0u;
-    }
-  } else {
-  // ---- E1b ----
-    uint32_t jcarry = 0;
-    int lastrec = -1;
-    const unsigned lt = (1u << lane) - 1u;
-    for (uint32_t kb = 0; kb < nf; kb += 32) {
-      const uint32_t k = kb + (uint32_t)lane;
-      const bool act = k < nf;
-      const uint32_t dl = act ? ws->dlist[k] : 0u;
-      const uint32_t p = dl & 0x7FFu;
-      const bool isrec = act && (dl >> 15);
-      const unsigned recm = __ballot_sync(0xffffffffu, isrec);
-      const unsigned before = recm & lt;
-      const int lr = before ? (int)(kb + 31u - __clz(before)) : lastrec;
-      extra += (uint32_t)__popc(__ballot_sync(0xffffffffu, act && lr >= 0 && k - (uint32_t)lr - 1u >= a.C));
-      if (act) {
-        const uint32_t x = k ? (ws->dlist[k - 1] & 0x7FFu) + 1u : 0u;   // field bytes [x, p)
-        int fd = -1, ld = -1;
-        uint32_t ic = 0;
-        if (x < p) {
-          uint32_t w = x >> 5;
-          uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu << (x & 31u));
-          const uint32_t wp = p >> 5;
-          while (!bits && w < wp) bits = ws->dmask[++w];
-          if (bits) {
-            const uint32_t f = (w << 5) + (uint32_t)__ffs(bits) - 1u;
-            if (f < p) fd = (int)f;
-          }
-        }
-        if (fd >= 0) {
-          const uint32_t y = p - 1u;
-          uint32_t w = y >> 5;
-          uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu >> (31u - (y & 31u)));
-          while (!bits) bits = ws->dmask[--w];
-          ld = (int)((w << 5) + 31u - (uint32_t)__clz(bits));
-          if (ld > fd && kcount(ws, (uint32_t)ld) > kcount(ws, (uint32_t)fd + 1u)) ic = 0x80000000u;
-        }
-        if (k == 0) {                                         // may continue a field of an earlier tile
-          uint32_t fl = ic ? F_IC : 0u;
-          if (fd >= 0) {
-            if (kcount(ws, (uint32_t)fd) > 0u) fl |= F_PRE;
-            if (kcount(ws, p) > kcount(ws, (uint32_t)ld + 1u)) fl |= F_PC;
-          } else if (kcount(ws, p) > 0u) {
-            fl |= F_PRE;
-          }
-          ws->fd0 = fd;
-          ws->ld0 = ld;
-          ws->fl0 = fl;
-        } else {
-          ws->fields[k] = fd < 0 ? p : ((uint32_t)fd | ((uint32_t)(ld + 1 - fd) << 11) | ic);  // empty: (delim, 0)
-        }
-      }
-      jcarry += (uint32_t)__popc(recm);
-      if (recm) lastrec = (int)(kb + 31u - __clz(recm));
-    }
-  }
-  if (lane == 0) {
-    ws->dense = 0u;
-    ws->nf = nf;
-    ws->nrec = nrec;
-    ws->ktot = ktot;
-    ws->n_before = n_before;
-    ws->extra_after = extra;
-  }
-  __syncwarp();
-}
-
-// E1 part that needs the prefix (field 0 continues the open field of the prefix; the entry column
-// decides which of the first record's fields are extra), then E2.
-template <bool TS>
-__device__ void emit_tile_global(const KArgs &a, const ColDesc *cols, WarpScratch *ws, const Seg &prefix,
-                                 unsigned long long Dm, unsigned long long Fm, unsigned long long Rm,
-                                 unsigned long long Vm, unsigned long long tbase_g, unsigned long long cbase,
-                                 EmitCounters &cnt) {
-  const int lane = threadIdx.x & 31;
-  if (ws->dense) {                                          // dense tile: per-chunk direct path
-    SegT sagg;
-    const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
-    emit_chunk<TS>(a, cols, seg_op(prefix, segt_to_seg(sex, tbase_g)), Dm, Fm, Rm, Vm, cbase, cnt);
-    __syncwarp();
-    return;
-  }
-  const uint32_t nf = ws->nf, nrec = ws->nrec;
-  const bool plain = ws->ktot == 0u;
-  if (lane == 0) {
-    const uint32_t c0 = prefix.col, nb = ws->n_before;
-    const uint32_t room = c0 >= a.C ? 0u : a.C - c0;
-    cnt.extra += ws->extra_after + (nb > room ? nb - room : 0u);
-    if (nf) {
-      const uint32_t p = ws->dlist[0] & 0x7FFu;
-      const int fd = ws->fd0, ld = ws->ld0;
       unsigned long long cfd = prefix.fd, cld = prefix.ld;
       uint32_t cfl = prefix.flags & (F_IC | F_PC | F_PRE);
-      open_combine(cfd, cld, cfl, fd >= 0 ? tbase_g + (unsigned)fd : NONE, fd >= 0 ? tbase_g + (unsigned)ld : NONE,
-                   ws->fl0);
+      open_combine(cfd, cld, cfl, p ? tbase_g : NONE, p ? tbase_g + p - 1u : NONE, 0u);
       uint32_t e;
       if (cfd == NONE) {
         e = p;
@@ -915,11 +814,96 @@ __device__ void emit_tile_global(const KArgs &a, const ColDesc *cols, WarpScratc
       }
       ws->fields[0] = e;
     }
+    cnt.extra += extra;
+  } else {
+  // ---- E1b ----
+  {
+    const uint32_t c0 = prefix.col;
+    uint32_t jcarry = 0, extra = 0;
+    int lastrec = -1;
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint32_t kb = 0; kb < nf; kb += 32) {
+      const uint32_t k = kb + (uint32_t)lane;
+      const bool act = k < nf;
+      const uint32_t dl = act ? ws->dlist[k] : 0u;
+      const uint32_t p = dl & 0x7FFu;
+      const bool isrec = act && (dl >> 15);
+      const unsigned recm = __ballot_sync(0xffffffffu, isrec);
+      const uint32_t jr = jcarry + __popc(recm & lt);
+      const unsigned before = recm & lt;
+      const int lr = before ? (int)(kb + 31u - __clz(before)) : lastrec;
+      const uint32_t c = lr >= 0 ? k - (uint32_t)lr - 1u : c0 + k;
+      extra += (uint32_t)__popc(__ballot_sync(0xffffffffu, act && c >= a.C));
+      if (act) {
+        const uint32_t x = k ? (ws->dlist[k - 1] & 0x7FFu) + 1u : 0u;   // field bytes [x, p)
+        int fd = -1, ld = -1;
+        uint32_t ic = 0;
+        if (ktot == 0u) {                                     // no CTRL byte: [x, p) is all DATA
+          if (x < p) { fd = (int)x; ld = (int)p - 1; }
+        } else {
+          if (x < p) {
+            uint32_t w = x >> 5;
+            uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu << (x & 31u));
+            const uint32_t wp = p >> 5;
+            while (!bits && w < wp) bits = ws->dmask[++w];
+            if (bits) {
+              const uint32_t f = (w << 5) + (uint32_t)__ffs(bits) - 1u;
+              if (f < p) fd = (int)f;
+            }
+          }
+          if (fd >= 0) {
+            const uint32_t y = p - 1u;
+            uint32_t w = y >> 5;
+            uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu >> (31u - (y & 31u)));
+            while (!bits) bits = ws->dmask[--w];
+            ld = (int)((w << 5) + 31u - (uint32_t)__clz(bits));
+            if (ld > fd && kcount(ws, (uint32_t)ld) > kcount(ws, (uint32_t)fd + 1u)) ic = 0x80000000u;
+          }
+        }
+        uint32_t e = fd < 0 ? p : ((uint32_t)fd | ((uint32_t)(ld + 1 - fd) << 11) | ic);  // empty: (delim, 0)
+        if (k == 0) {                                         // may continue a field of an earlier tile
+          uint32_t fl = ic ? F_IC : 0u;
+          if (ktot) {
+            if (fd >= 0) {
+              if (kcount(ws, (uint32_t)fd) > 0u) fl |= F_PRE;
+              if (kcount(ws, p) > kcount(ws, (uint32_t)ld + 1u)) fl |= F_PC;
+            } else if (kcount(ws, p) > 0u) {
+              fl |= F_PRE;
+            }
+          }
+          unsigned long long cfd = prefix.fd, cld = prefix.ld;
+          uint32_t cfl = prefix.flags & (F_IC | F_PC | F_PRE);
+          open_combine(cfd, cld, cfl, fd >= 0 ? tbase_g + (unsigned)fd : NONE, fd >= 0 ? tbase_g + (unsigned)ld : NONE,
+                       fl);
+          if (cfd == NONE) {
+            e = p;
+          } else {
+            const unsigned long long L = cld + 1 - cfd;
+            const long long rel = (long long)cfd - (long long)tbase_g;
+            const uint32_t icf = (cfl & F_IC) ? 0x80000000u : 0u;
+            if (rel >= 0 && L <= (unsigned long long)WT) {
+              e = (uint32_t)rel | ((uint32_t)L << 11) | icf;
+            } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
+              emit_field<TS>(a, cols, prefix.recs + jr, c, cfd, cld, cfl, tbase_g + p, cnt);
+              e = FIELD_WRITTEN;
+              if (c >= a.C) cnt.extra--;                      // emit_field counted it already
+            } else {
+              ws->f0 = make_uint2((uint32_t)(int32_t)rel, (uint32_t)L | icf);
+              e = FIELD_FAR;
+            }
+          }
+        }
+        ws->fields[k] = e;
+      }
+      jcarry += (uint32_t)__popc(recm);
+      if (recm) lastrec = (int)(kb + 31u - __clz(recm));
+    }
+    if (lane == 0) cnt.extra += extra;
+  }
   }
   __syncwarp();
   // ---- E2 ----
   const uint8_t *tb = reinterpret_cast<const uint8_t *>(ws->bytes);
-  (void)Dm; (void)Fm; (void)Rm; (void)Vm; (void)cbase;
   const uint32_t last_end = nrec ? (ws->rows[nrec - 1] & 0xFFFFu) : 0u;
   const uint32_t nrows = nrec + (nf > last_end ? 1u : 0u);
   if (nrows == 0) {                                         // no delimiter: the open field continues
@@ -1068,19 +1052,8 @@ __device__ void emit_tile_global(const KArgs &a, const ColDesc *cols, WarpScratc
   __syncwarp();
 }
 
-// Per-warp emission of one tile (S6+S7): E1 then E2.  prefix = everything before the tile (seed included).
-template <bool TS>
-__device__ __forceinline__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, const Seg &prefix,
-                                          unsigned long long Dm, unsigned long long Fm, unsigned long long Rm,
-                                          unsigned long long Vm, unsigned long long tbase_g, unsigned long long cbase,
-                                          EmitCounters &cnt) {
-  emit_tile_local(a, ws, Dm, Fm, Rm, Vm);
-  emit_tile_global<TS>(a, cols, ws, prefix, Dm, Fm, Rm, Vm, tbase_g, cbase, cnt);
-}
-
 }  // namespace parpa
 #include "parpa_passes.cuh"
-#include "parpa_fused.cuh"
 namespace parpa {
 
 // ---- two-phase emit kernel (per warp tile, from the stored prefixes; no look-back) ------------------

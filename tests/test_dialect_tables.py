@@ -55,7 +55,7 @@ def test_invalid_state_absorbing_and_catch_all_idempotent(name):
     for g in range(t.G):
         assert t.transition[g][t.invalid] == t.invalid
     ca = t.transition[t.G - 1]
-    assert [ca[s] for s in ca] == ca          # r∘r = r (used by DESIGN.md's event kernels)
+    assert [ca[s] for s in ca] == ca          # r∘r = r: the catch-all row is idempotent
 
 
 def random_dfa(rng):

@@ -226,3 +226,18 @@ def test_strict_columns():
     assert r.status == oracle.ECOLUMNS and r.n_missing == 1
     r = oracle.parse("csv", b"1,2,3\n", 2)
     assert r.status == oracle.OK and r.n_extra == 1
+
+
+@pytest.mark.parametrize("dialect", ["csv_comment", "clf"])
+def test_dialect_fixtures_hand_derived(dialect):
+    """Transitions of the two invented dialects not covered by the SURVEY Appendix A fixtures, each
+    expected value derived by hand from the printed tables (A.2 / A.3), not from the oracle."""
+    for fx in FIX[dialect + "_extra"]:
+        data = fx["input"].encode()
+        r = oracle.parse(dialect, data, fx["C"], types=[oracle.SPAN] * fx["C"], trace=True)
+        if fx.get("status") == "EFORMAT":
+            assert r.status == oracle.EFORMAT and r.first_invalid == fx["first_invalid"], fx["cite"]
+            continue
+        assert r.status == oracle.OK and r.R == fx["R"], fx["cite"]
+        got = [data_bytes(data, r, r.trace_kind, c)[row] for row in range(r.R) for c in range(fx["C"])]
+        assert got == [x.encode() for x in fx["data"]], fx["cite"]
