@@ -504,9 +504,8 @@ int parpa_create_dfa(uint32_t S, uint32_t start, uint32_t inv, uint32_t G, const
         kind = d->emit[g][s];
       }
       sel |= nd << (4 * j);
-      uint32_t fl = (kind != PARPA_DATA ? NOT_DATA : 0) |
-                    ((kind != PARPA_FIELD && kind != PARPA_RECORD) ? NOT_DELIM : 0) |
-                    (kind != PARPA_RECORD ? NOT_REC : 0);
+      const uint32_t fl = (kind == PARPA_DATA ? KC_DATA : kind == PARPA_FIELD ? KC_FIELD
+                           : kind == PARPA_RECORD ? KC_RECORD : KC_CTRL) << 4;
       step[j] = (uint8_t)(0x80u | nd | fl);
     }
     d->k.lut[b][0] = sel & 0xFFFFu;

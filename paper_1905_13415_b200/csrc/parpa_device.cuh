@@ -34,8 +34,11 @@ constexpr uint32_t INV_DEV = 0xFu;
 constexpr unsigned long long NONE = 0xFFFFFFFFFFFFFFFFull;
 constexpr uint32_t NONE16 = 0xFFFFu;
 
-// emission flags in a pass-2 step byte (inverted so that 0xFF, produced for INV, reads as CTRL)
-constexpr uint32_t NOT_DATA = 0x10, NOT_DELIM = 0x20, NOT_REC = 0x40;
+// emission kind in bits 4-5 of a pass-2 step byte, coded so that 0xFF (produced for INV by PRMT's sign
+// replication) reads as CTRL: DATA 00, FIELD 01, RECORD 10, CTRL 11.  Two gathered bits per byte give the
+// masks: DATA = ~(b4 | b5), DELIM = b4 ^ b5, RECORD = b5 & ~b4.
+constexpr uint32_t KC_DATA = 0u, KC_FIELD = 1u, KC_RECORD = 2u, KC_CTRL = 3u, KC_MASK = 0x30u;
+__device__ __host__ __forceinline__ uint32_t step_kind_code(uint32_t x) { return (x >> 4) & 3u; }
 
 // SegT / Seg flag bits
 constexpr uint32_t F_ABS = 1, F_HD = 2, F_IC = 4, F_PC = 8, F_PRE = 16;

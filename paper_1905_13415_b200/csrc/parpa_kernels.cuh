@@ -181,7 +181,7 @@ __device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_
                                                 unsigned long long &Dm, unsigned long long &Fm,
                                                 unsigned long long &Rm) {
   uint32_t x = 0x80u | entry;
-  uint32_t d[2] = {0, 0}, f[2] = {0, 0}, r[2] = {0, 0};
+  uint32_t g4[2] = {0, 0}, g5[2] = {0, 0};                // kind-code bits 4 / 5 of every byte
 #pragma unroll
   for (int w = 0; w < 16; w++) {
     uint32_t xs[4];
@@ -197,15 +197,15 @@ __device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_
       }
     }
     uint32_t pk = prmt(prmt(xs[0], xs[1], 0x0040u), prmt(xs[2], xs[3], 0x0040u), 0x5410u);
-    uint32_t npk = ~pk;
     int h = w >> 3, sh = 4 * (w & 7);
-    d[h] |= gather4(npk, 0x10101010u, 0x10204080u) << sh;
-    f[h] |= gather4(npk, 0x20202020u, 0x08102040u) << sh;
-    r[h] |= gather4(npk, 0x40404040u, 0x04081020u) << sh;
+    g4[h] |= gather4(pk, 0x10101010u, 0x10204080u) << sh;
+    g5[h] |= gather4(pk, 0x20202020u, 0x08102040u) << sh;
   }
-  Dm = (unsigned long long)d[0] | ((unsigned long long)d[1] << 32);
-  Fm = (unsigned long long)f[0] | ((unsigned long long)f[1] << 32);
-  Rm = (unsigned long long)r[0] | ((unsigned long long)r[1] << 32);
+  const unsigned long long b4 = (unsigned long long)g4[0] | ((unsigned long long)g4[1] << 32);
+  const unsigned long long b5 = (unsigned long long)g5[0] | ((unsigned long long)g5[1] << 32);
+  Dm = ~(b4 | b5);
+  Fm = b4 ^ b5;
+  Rm = b5 & ~b4;
   return x & 0xFu;
 }
 
@@ -1176,7 +1176,7 @@ struct DfaDataSrc {                   // DATA bytes of [fd, ld], re-simulated fr
       uint32_t step_lo = d->lut[b][2], step_hi = d->lut[b][3];
       uint32_t prev = x;
       x = prmt(step_lo, step_hi, prev);
-      if ((x & NOT_DATA) == 0) { c = b; return true; }
+      if ((x & KC_MASK) == 0u) { c = b; return true; }
     }
     return false;
   }
@@ -1263,8 +1263,8 @@ __global__ void k_debug_trace(const KArgs a, const DfaK dfa, uint8_t *chunk_stat
       uint8_t b = a.in[p];
       if (states) states[p] = dfa.hmap[x & 0xFu];
       x = prmt(dfa.lut[b][2], dfa.lut[b][3], x);
-      uint32_t f = x & 0x70u;
-      uint8_t kind = !(f & NOT_REC) ? 3 : !(f & NOT_DELIM) ? 2 : !(f & NOT_DATA) ? 0 : 1;
+      const uint32_t kc = step_kind_code(x);
+      uint8_t kind = kc == KC_RECORD ? 3 : kc == KC_FIELD ? 2 : kc == KC_DATA ? 0 : 1;   // parpa_emit codes
       if (kinds) kinds[p] = kind;
     }
   }

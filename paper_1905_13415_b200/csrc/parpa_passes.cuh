@@ -182,51 +182,40 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_tau_scan(const KArgs a) {
 // the last delimiter (first / last DATA byte, control bytes before / inside / after).
 __device__ __forceinline__ SegT warp_tile_segt(unsigned long long Dm, unsigned long long Fm, unsigned long long Rm,
                                                unsigned long long Vm) {
+  // Branch-free form: every per-lane quantity is a select on the lane's position relative to the lane of
+  // the last record / last delimiter / first and last open DATA byte (no divergent single-lane paths).
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu;
   const uint32_t nrec = __reduce_add_sync(FULL, (uint32_t)__popcll(Rm));
   const uint32_t nd = __reduce_add_sync(FULL, (uint32_t)__popcll(Fm));
-  uint32_t fl = 0, col;
-  const unsigned rb = __ballot_sync(FULL, Rm != 0ull);
-  if (rb) {
-    const int L = 31 - __clz(rb);
-    const uint32_t mine = lane > L ? (uint32_t)__popcll(Fm)
-                          : lane == L ? (uint32_t)__popcll(Fm & above(msb64(Rm))) : 0u;
-    col = __reduce_add_sync(FULL, mine);
-    fl |= F_ABS;
-  } else {
-    col = nd;
-  }
-  unsigned long long open = Vm;
-  const unsigned fb = __ballot_sync(FULL, Fm != 0ull);
-  if (fb) {
-    fl |= F_HD;
-    const int Lf = 31 - __clz(fb);
-    open = lane > Lf ? Vm : lane == Lf ? (Vm & above(msb64(Fm))) : 0ull;
-  }
+  // bits strictly after the last record / delimiter of this lane (all bits if it has none)
+  const unsigned long long aftR = Rm ? (~0ull << (63 - __clzll(Rm))) << 1 : ~0ull;
+  const unsigned long long aftF = Fm ? (~0ull << (63 - __clzll(Fm))) << 1 : ~0ull;
+  const unsigned rb = __ballot_sync(FULL, Rm != 0ull), fb = __ballot_sync(FULL, Fm != 0ull);
+  const int L = rb ? 31 - __clz(rb) : -1, Lf = fb ? 31 - __clz(fb) : -1;
+  const uint32_t col = __reduce_add_sync(FULL, lane >= L ? (uint32_t)__popcll(Fm & aftR) : 0u);
+  uint32_t fl = (rb ? F_ABS : 0u) | (fb ? F_HD : 0u);
+  const unsigned long long open = lane >= Lf ? (Vm & aftF) : 0ull;     // the field left open at the end
   const unsigned long long Km = Vm & ~Dm & ~Fm;
   const unsigned long long Do = Dm & open, Ko = Km & open;
   const unsigned db = __ballot_sync(FULL, Do != 0ull);
-  uint32_t pos;
+  uint32_t pos = 0xFFFFFFFFu, pf;
   if (db) {
-    const int fl_lane = __ffs(db) - 1, ll_lane = 31 - __clz(db);
-    const int fdl = Do ? lsb64(Do) : 0, ldl = Do ? msb64(Do) : 0;
-    const int fdloc = __shfl_sync(FULL, fdl, fl_lane), ldloc = __shfl_sync(FULL, ldl, ll_lane);
-    const bool pre = (lane < fl_lane && Ko) || (lane == fl_lane && (Ko & below(fdloc)));
-    const bool pc = (lane > ll_lane && Ko) || (lane == ll_lane && (Ko & above(ldloc)));
-    unsigned long long in = 0ull;
-    if (lane > fl_lane && lane < ll_lane) in = Ko;
-    else if (lane == fl_lane && lane == ll_lane) in = Ko & above(fdloc) & below(ldloc);
-    else if (lane == fl_lane) in = Ko & above(fdloc);
-    else if (lane == ll_lane) in = Ko & below(ldloc);
-    if (__any_sync(FULL, pre)) fl |= F_PRE;
-    if (__any_sync(FULL, pc)) fl |= F_PC;
-    if (__any_sync(FULL, in != 0ull)) fl |= F_IC;
-    pos = (uint32_t)(fl_lane * CHUNK + fdloc) | ((uint32_t)(ll_lane * CHUNK + ldloc) << 16);
+    const int f0 = __ffs(db) - 1, f1 = 31 - __clz(db);
+    const int fdloc = __shfl_sync(FULL, Do ? __ffsll((long long)Do) - 1 : 0, f0);
+    const int ldloc = __shfl_sync(FULL, Do ? 63 - __clzll(Do) : 0, f1);
+    const unsigned long long belowF = (1ull << fdloc) - 1ull, aboveF = (~0ull << fdloc) << 1;
+    const unsigned long long belowL = (1ull << ldloc) - 1ull, aboveL = (~0ull << ldloc) << 1;
+    const unsigned long long pre_m = lane < f0 ? ~0ull : lane == f0 ? belowF : 0ull;
+    const unsigned long long pc_m = lane > f1 ? ~0ull : lane == f1 ? aboveL : 0ull;
+    const unsigned long long in_m = (lane > f0 ? ~0ull : lane == f0 ? aboveF : 0ull) &
+                                    (lane < f1 ? ~0ull : lane == f1 ? belowL : 0ull);
+    pf = ((Ko & pre_m) ? F_PRE : 0u) | ((Ko & pc_m) ? F_PC : 0u) | ((Ko & in_m) ? F_IC : 0u);
+    pos = (uint32_t)(f0 * CHUNK + fdloc) | ((uint32_t)(f1 * CHUNK + ldloc) << 16);
   } else {
-    pos = 0xFFFFFFFFu;
-    if (__any_sync(FULL, Ko != 0ull)) fl |= F_PRE;
+    pf = Ko ? F_PRE : 0u;
   }
+  fl |= __reduce_or_sync(FULL, pf);
   return SegT{nrec | (nd << 16), col | (fl << 16), pos};
 }
 

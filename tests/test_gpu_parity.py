@@ -78,13 +78,14 @@ def test_ragged_sizes(n):
 
 def test_golden_fixtures_on_gpu():
     fx = json.load(open(os.path.join(GOLD, "fixtures.json")))
-    for dialect, cases in fx.items():
-        if dialect == "source":
+    for key, cases in fx.items():
+        if key == "source":
             continue
+        dialect = key.replace("_extra", "")              # the hand-derived extra fixtures of a dialect
         for case in cases:
             C = case["C"]
             types = [oracle.SPAN] * C
-            if dialect == "clf":
+            if dialect == "clf" and C == 7:
                 types[5] = types[6] = oracle.INT64
             run_all_paths(dialect, case["input"].encode(), types, label=case["cite"][:30])
 
