@@ -49,7 +49,7 @@ int cuda_status(cudaError_t e) {
 struct DevCfg {
   bool init = false;
   int sms = 0;
-  int occ_pass1 = 0, occ_pass2 = 0, occ_emit = 0;
+  int occ_pass1 = 0, occ_pass2 = 0, occ_emit = 0, occ_small = 0;
 };
 std::mutex g_mu;
 DevCfg g_dev[64];
@@ -69,6 +69,9 @@ int dev_cfg(DevCfg **out) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass1, k_pass1, PASS_WARPS * 32, PASS_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass2, k_pass2, PASS_WARPS * 32, PASS_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit<false>, EMIT_WARPS * 32, EMIT_SMEM));
+    CK(cudaFuncSetAttribute(k_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMALL_SMEM));
+    CK(cudaFuncSetAttribute(k_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMALL_SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_small, k_small<false>, SMALL_WARPS * 32, SMALL_SMEM));
     if (getenv("PARPA_DEBUG")) {
       auto show = [](const char *n, const void *f) {
         cudaFuncAttributes fa;
@@ -368,6 +371,56 @@ int launch_emit(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, 
       CK(launch_k(k_emit<false>, grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s, true, a, ck));
   }
   CK(cudaGetLastError());
+  if (launches) (*launches)++;
+  return PARPA_OK;
+}
+
+// Small inputs (<= SMALL_MAX_TILES warp tiles): the whole parse as one cooperative launch (k_small).
+// PARPA_SMALL=0 in the environment forces the multi-kernel path (A/B, tests).
+static bool small_enabled() {
+  static const bool on = !(getenv("PARPA_SMALL") && getenv("PARPA_SMALL")[0] == '0');
+  return on;
+}
+bool use_small(const KArgs &a) {
+  if (!small_enabled() || a.ntiles == 0 || a.ntiles > SMALL_MAX_TILES) return false;
+  DevCfg *dc;
+  if (dev_cfg(&dc)) return false;
+  return dc->occ_small >= 1;
+}
+int launch_small(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, uint32_t *launches) {
+  DevCfg *dc;
+  int rc0 = dev_cfg(&dc);
+  if (rc0) return rc0;
+  // one warp per tile in the passes, SMALL_NP warps per tile in the emission phase
+  const unsigned grid = (unsigned)std::min<long long>((long long)dc->occ_small * dc->sms,
+                                                       ((long long)a.ntiles * SMALL_NP + SMALL_WARPS - 1) / SMALL_WARPS);
+  void *args[] = {(void *)&a, (void *)&k, (void *)&ck};
+  static const bool sprof = getenv("PARPA_SPROF") && getenv("PARPA_SPROF")[0] == '1';
+  KArgs ap = a;
+  if (sprof) {
+    CK(cudaMallocAsync(&ap.prof, 16 * 8, s));
+    CK(cudaMemsetAsync(ap.prof, 0, 16 * 8, s));
+    args[0] = (void *)&ap;
+  }
+  {
+    Launch L(s, "k_small");
+    if (has_timestamps(a, ck))
+      CK(cudaLaunchCooperativeKernel((const void *)k_small<true>, dim3(grid), dim3(SMALL_WARPS * 32), args, SMALL_SMEM, s));
+    else
+      CK(cudaLaunchCooperativeKernel((const void *)k_small<false>, dim3(grid), dim3(SMALL_WARPS * 32), args, SMALL_SMEM, s));
+  }
+  CK(cudaGetLastError());
+  if (sprof) {
+    unsigned long long h[16];
+    CK(cudaMemcpyAsync(h, ap.prof, 16 * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    fprintf(stderr, "[parpa sprof] us: lut %.1f pass1 %.1f sync %.1f tauscan %.1f pass2 %.1f sync %.1f segscan %.1f emit %.1f "
+            "sync %.1f fin %.1f sync %.1f deferred+sync %.1f total %.1f\n", (h[1] - h[0]) / 1e3, (h[2] - h[1]) / 1e3,
+            (h[3] - h[2]) / 1e3, (h[4] - h[3]) / 1e3, (h[5] - h[4]) / 1e3, (h[6] - h[5]) / 1e3, (h[7] - h[6]) / 1e3,
+            (h[8] - h[7]) / 1e3, (h[9] - h[8]) / 1e3, (h[10] - h[9]) / 1e3, (h[11] - h[10]) / 1e3, (h[12] - h[11]) / 1e3,
+            (h[12] - h[0]) / 1e3);
+    cudaFreeAsync(ap.prof, s);
+  }
   if (launches) (*launches)++;
   return PARPA_OK;
 }
@@ -724,9 +777,13 @@ static int parse_into_impl(const parpa_dfa *dfa, const parpa_schema *sch, const 
     a.left_len = left_len;
     a.is_last = is_last;
     uint32_t n = 0;
-    rc = launch_passes(MODE_COUNT, a, dfa->k, s, &n);
-    if (!rc) rc = launch_emit(a, dfa->k, ck, s, &n);
-    if (!rc) rc = launch_tail(a, dfa->k, ck, s, &n);
+    if (use_small(a)) {
+      rc = launch_small(a, dfa->k, ck, s, &n);
+    } else {
+      rc = launch_passes(MODE_COUNT, a, dfa->k, s, &n);
+      if (!rc) rc = launch_emit(a, dfa->k, ck, s, &n);
+      if (!rc) rc = launch_tail(a, dfa->k, ck, s, &n);
+    }
     if (launches) *launches = n;
   }
   work_free(w, s);

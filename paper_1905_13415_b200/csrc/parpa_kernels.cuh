@@ -565,6 +565,7 @@ struct alignas(16) WarpScratch {
   uint16_t dlist[FCAP];                     // delimiter positions (tile-local) | record bit << 15
   uint32_t dmask[WT / 32], kmask[WT / 32];  // DATA / CTRL bits of the tile, 32 per word
   uint16_t kpre[WT / 32];                   // CTRL bits before each word
+  uint32_t e1_nf, e1_nrec, e1_plain;        // E1 -> E2 when several warps share a tile (k_small)
 };
 #ifndef PARPA_E2_ROWS_MIN
 #define PARPA_E2_ROWS_MIN 16
@@ -692,12 +693,18 @@ __device__ __forceinline__ void write_value_tile(const KArgs &a, const ColDesc *
 __device__ __forceinline__ uint32_t kcount(const WarpScratch *ws, uint32_t x) {   // CTRL bytes before x
   return ws->kpre[x >> 5] + __popc(ws->kmask[x >> 5] & ((1u << (x & 31u)) - 1u));
 }
-template <bool TS>
+// NP > 1 (k_small): NP warps share one tile — part 0 runs E0/E1 into its scratch `ws`, a named barrier
+// (bar, NP warps) publishes it, and every part writes the columns c = part, part + NP, ... in E2 (the
+// column-uniform path) or every NP-th item (the flattened path).  NP == 1 is the one-warp-per-tile path.
+template <bool TS, int NP = 1>
 __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, const Seg &prefix,
                           unsigned long long Dm, unsigned long long Fm, unsigned long long Rm,
                           unsigned long long Vm, unsigned long long tbase_g, unsigned long long cbase,
-                          EmitCounters &cnt) {
+                          EmitCounters &cnt, uint32_t part = 0, int bar = 0) {
   const int lane = threadIdx.x & 31;
+  uint32_t nf = 0, nrec = 0;
+  bool plain = false;
+  if (NP == 1 || part == 0) {
   const unsigned long long Km = Vm & ~Dm & ~Fm;
   // per-lane (delimiters << 16 | records) and CTRL counts -> exclusive offsets, tile totals
   const uint32_t mine = (uint32_t)__popcll(Rm) | ((uint32_t)__popcll(Fm) << 16);
@@ -709,13 +716,16 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     if (lane >= d) { inc += o; kinc += ko; }
   }
   const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
-  const uint32_t nf = tot >> 16, nrec = tot & 0xFFFFu;
+  nf = tot >> 16;
+  nrec = tot & 0xFFFFu;
   if (nf > (uint32_t)FCAP || nrec >= (uint32_t)RCAP) {       // warp-uniform: dense tile, direct path
     SegT sagg;
     const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
     emit_chunk<TS>(a, cols, seg_op(prefix, segt_to_seg(sex, tbase_g)), Dm, Fm, Rm, Vm, cbase, cnt);
-    return;
-  }
+    if (NP == 1) return;
+    nf = 0u;                                                  // the other parts have nothing to write
+    nrec = 0u;
+  } else {
   // ---- E1a ----
   if (nf <= E1A_SELECT_MAX) {
     // few delimiters (long fields, e.g. yelp text): lane k selects the k-th delimiter of the tile — the
@@ -775,7 +785,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   }
   __syncwarp();
   const uint32_t ktot = __shfl_sync(0xffffffffu, kinc, 31);    // CTRL bytes in the tile (warp-uniform)
-  const bool plain = ktot == 0u;
+  plain = ktot == 0u;
   if (plain) {
     // E1b' (no CTRL byte in the tile): field k is the byte range between delimiters k-1 and k, all DATA,
     // so E2 reads it straight from the delimiter list.  Only field 0 (which may continue a field of an
@@ -836,6 +846,9 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
       extra += (uint32_t)__popc(__ballot_sync(0xffffffffu, act && c >= a.C));
       if (act) {
         const uint32_t x = k ? (ws->dlist[k - 1] & 0x7FFu) + 1u : 0u;   // field bytes [x, p)
+        // inner / surrounding control bytes only matter for converted columns (a span is [first, last DATA])
+        const uint32_t ty = c < a.C ? cols[c].type : (uint32_t)T_SKIP;
+        const bool typed = ty != T_SPAN && ty != T_SKIP;
         int fd = -1, ld = -1;
         uint32_t ic = 0;
         if (ktot == 0u) {                                     // no CTRL byte: [x, p) is all DATA
@@ -857,13 +870,13 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
             uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu >> (31u - (y & 31u)));
             while (!bits) bits = ws->dmask[--w];
             ld = (int)((w << 5) + 31u - (uint32_t)__clz(bits));
-            if (ld > fd && kcount(ws, (uint32_t)ld) > kcount(ws, (uint32_t)fd + 1u)) ic = 0x80000000u;
+            if (typed && ld > fd && kcount(ws, (uint32_t)ld) > kcount(ws, (uint32_t)fd + 1u)) ic = 0x80000000u;
           }
         }
         uint32_t e = fd < 0 ? p : ((uint32_t)fd | ((uint32_t)(ld + 1 - fd) << 11) | ic);  // empty: (delim, 0)
         if (k == 0) {                                         // may continue a field of an earlier tile
           uint32_t fl = ic ? F_IC : 0u;
-          if (ktot) {
+          if (ktot && typed) {
             if (fd >= 0) {
               if (kcount(ws, (uint32_t)fd) > 0u) fl |= F_PRE;
               if (kcount(ws, p) > kcount(ws, (uint32_t)ld + 1u)) fl |= F_PC;
@@ -901,13 +914,23 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     if (lane == 0) cnt.extra += extra;
   }
   }
+  }                                                         // (not dense)
+  }                                                         // (E0 / E1: the whole tile or part 0)
   __syncwarp();
+  if (NP > 1) {                                             // part 0's E1 -> every part
+    if (part == 0 && lane == 0) { ws->e1_nf = nf; ws->e1_nrec = nrec; ws->e1_plain = plain ? 1u : 0u; }
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(NP * 32) : "memory");
+    nf = ws->e1_nf;
+    nrec = ws->e1_nrec;
+    plain = ws->e1_plain != 0u;
+  }
   // ---- E2 ----
   const uint8_t *tb = reinterpret_cast<const uint8_t *>(ws->bytes);
   const uint32_t last_end = nrec ? (ws->rows[nrec - 1] & 0xFFFFu) : 0u;
   const uint32_t nrows = nrec + (nf > last_end ? 1u : 0u);
   if (nrows == 0) {                                         // no delimiter: the open field continues
     __syncwarp();
+    if (NP > 1) asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(NP * 32) : "memory");
     return;
   }
   const uint32_t c0 = prefix.col;
@@ -932,8 +955,8 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
         row = r0 + ji - a.row_base;
         live = row < a.cap;
       }
-      if (live && closed && end - start + cs < a.C) cnt.missing++;   // record closed with fewer fields
-      for (uint32_t c = 0; c < a.C; c++) {                     // warp-uniform
+      if ((NP == 1 || part == 0) && live && closed && end - start + cs < a.C) cnt.missing++;   // short record
+      for (uint32_t c = (NP == 1 ? 0u : part); c < a.C; c += NP) {   // warp-uniform
         const ColDesc *cd = cols + c;
         const uint32_t type = cd->type;
         if (type == T_SKIP) continue;
@@ -988,15 +1011,17 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
       }
     }
     __syncwarp();
+    if (NP > 1) asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(NP * 32) : "memory");
     return;
   }
   // Column-major writes: (column, tile row) items flattened over the lanes, rows fastest, so a warp
   // step stores consecutive rows of one or two columns (coalesced) with every lane busy; numeric
   // columns share one converter, so mixed int / float steps do not diverge.
   const uint32_t total = a.C * nrows;
-  uint32_t c = (uint32_t)lane / nrows, jr = (uint32_t)lane - c * nrows;   // nrows >= 1 here
-  const uint32_t dc = 32u / nrows, djr = 32u - dc * nrows;
-  for (uint32_t it = lane; it < total; it += 32) {
+  const uint32_t it0 = (uint32_t)lane + 32u * (NP == 1 ? 0u : part), step = 32u * NP;
+  uint32_t c = it0 / nrows, jr = it0 - c * nrows;            // nrows >= 1 here
+  const uint32_t dc = step / nrows, djr = step - dc * nrows;
+  for (uint32_t it = it0; it < total; it += step) {
     const uint32_t ci = c, ji = jr;
     jr += djr;
     c += dc;
@@ -1050,6 +1075,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     }
   }
   __syncwarp();
+  if (NP > 1) asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(NP * 32) : "memory");   // scratch reusable
 }
 
 }  // namespace parpa
@@ -1120,10 +1146,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const
 }
 
 // ---- finalize ---------------------------------------------------------------------------------------
-__global__ void k_finalize(const KArgs a, const DfaK dfa, const ColsK colsk) {
-  PdlTrigger pdl_trigger;
-  pdl_wait();
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void finalize_one(const KArgs &a, const DfaK &dfa, const ColsK &colsk) {   // one thread
   Seg tot = a.ntiles ? seg_op(a.seed, *a.tot_seg) : a.seed;
   uint32_t tau = a.ntiles ? *a.tot_tau : NIB_IDENT;
   uint32_t fin = nib_at(tau, a.seed_dev);
@@ -1160,6 +1183,13 @@ __global__ void k_finalize(const KArgs a, const DfaK dfa, const ColsK colsk) {
     a.stats->status = status;
     a.stats->final_state = dfa.hmap[fin];
   }
+}
+__global__ void k_finalize(const __grid_constant__ KArgs a, const __grid_constant__ DfaK dfa,
+                           const __grid_constant__ ColsK colsk) {
+  PdlTrigger pdl_trigger;
+  pdl_wait();
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  finalize_one(a, dfa, colsk);
 }
 
 // ---- device-tier conversion of deferred fields ------------------------------------------------------
@@ -1212,12 +1242,10 @@ __device__ void convert_deferred(const KArgs &a, const DfaK &dfa, const ColDesc 
   cd->valid[row] = (uint8_t)ok;
 }
 
+// every thread of the grid (tid of nth): the queued fields, then (after an overflow) the marked rows
 template <bool TS>
-__global__ void k_deferred(const KArgs a, const DfaK dfa, const ColsK colsk) {
-  PdlTrigger pdl_trigger;
-  pdl_wait();
-  const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
-  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+__device__ __forceinline__ void deferred_all(const KArgs &a, const DfaK &dfa, const ColsK &colsk, unsigned long long tid,
+                             unsigned long long nth) {
   unsigned int n = min(a.ctrl->n_defer, a.dq_cap);
   for (unsigned long long i = tid; i < n; i += nth) {
     const DeferItem it = a.dq[i];
@@ -1237,6 +1265,15 @@ __global__ void k_deferred(const KArgs a, const DfaK dfa, const ColsK colsk) {
       }
     }
   }
+}
+template <bool TS>
+__global__ void k_deferred(const __grid_constant__ KArgs a, const __grid_constant__ DfaK dfa,
+                           const __grid_constant__ ColsK colsk) {
+  PdlTrigger pdl_trigger;
+  pdl_wait();
+  const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  deferred_all<TS>(a, dfa, colsk, tid, nth);
   // the last block to finish settles the status (every block's conversions are done by then)
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1271,3 +1308,4 @@ __global__ void k_debug_trace(const KArgs a, const DfaK dfa, uint8_t *chunk_stat
 }
 
 }  // namespace parpa
+#include "parpa_small.cuh"
