@@ -377,8 +377,8 @@ def run_config(args, config, ctx, main=True):
     def step():
         if world == 1:
             return parpa.parse_into(dfa, schema, d, cols, cap, st)
-        pdist.parse_sharded(dfa, schema, d, base, cols, cap, st, left=left, is_last=is_last,
-                            exchange_device=coll)
+        pdist.parse_sharded(dfa, schema, d, base, cols, cap, st, left=None, is_last=is_last,
+                            exchange_device=coll)          # the halo is exchanged between the ranks
         return 7                                  # range_begin 2 + range_count 2 + range_emit 3
 
     parpa.set_profiling(False)

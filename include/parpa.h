@@ -277,6 +277,26 @@ int parpa_range_emit(parpa_plan *plan, const parpa_schema *schema, const parpa_c
                      const parpa_column *columns, uint64_t capacity, parpa_stats *d_stats,
                      void *stream);
 
+/* ---- the cross-rank halo (the multi-GPU analogue of the paper's partition carry-over) --- *
+ * A field whose DATA begins on an earlier rank (its first DATA byte = the composed prefix's open_first
+ * < base) needs those bytes to be converted; if control bytes lie inside it, also the DFA state at
+ * some earlier position (the device tier re-simulates to drop them).
+ * parpa_range_state_at   *state = the DFA state before the byte at global offset `pos` of this range,
+ *                        for pos - base a multiple of parpa_chunk_bytes() (after parpa_range_count;
+ *                        synchronous).  The rank holding the start of a straddling field sends the bytes
+ *                        from that chunk boundary on, with this state, to the ranks that need them.
+ * parpa_range_emit_halo  parpa_range_emit with `left_state` = the DFA state before left_context[0]
+ *                        (PARPA_STATE_UNKNOWN: as parpa_range_emit, where a straddling typed field with
+ *                        inner control bytes is PARPA_EUNSUPPORTED).
+ * Errors: PARPA_EINVAL (pos not chunk-aligned / outside the range / before the count; a known
+ * left_state without left bytes or >= num_states). */
+#define PARPA_STATE_UNKNOWN 0xFFFFFFFFu
+int parpa_range_state_at(const parpa_plan *plan, uint64_t pos, uint32_t *state);
+int parpa_range_emit_halo(parpa_plan *plan, const parpa_schema *schema, const parpa_context *ctx,
+                          const uint8_t *left_context, uint64_t left_len, uint32_t left_state, int is_last,
+                          const parpa_column *columns, uint64_t capacity, parpa_stats *d_stats,
+                          void *stream);
+
 int parpa_parse_range(const parpa_dfa *dfa, const parpa_schema *schema, const uint8_t *d_bytes,
                       uint64_t len, const parpa_context *ctx, const uint8_t *left_context,
                       uint64_t left_len, int is_last, const parpa_column *columns,

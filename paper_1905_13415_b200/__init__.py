@@ -437,6 +437,9 @@ def strings(dfa: Dfa, data, column, rows: int, stream=None):
     return offs, buf[:int(total.value)]
 
 
+STATE_UNKNOWN = 0xFFFFFFFF
+
+
 class RangePlan:
     """Staged parse of one byte range (the multi-GPU exchange with every pass run once):
     ``begin`` -> the range's transition vector, ``count(entry_state)`` -> its counts,
@@ -460,16 +463,28 @@ class RangePlan:
         self.entry_state = int(entry_state)
         return c
 
-    def emit(self, schema: Schema, prefix, columns, capacity: int, stats_tensor, left=None, is_last=True):
+    def state_at(self, pos: int) -> int:
+        """DFA state before the byte at global offset ``pos`` (chunk-aligned, within the range; after
+        ``count``) — the state a halo sender attaches to bytes sent from ``pos`` on."""
+        st = ctypes.c_uint32(0)
+        _check(_lib.load().parpa_range_state_at(self.handle, int(pos), ctypes.byref(st)), "parpa_range_state_at")
+        return st.value
+
+    def emit(self, schema: Schema, prefix, columns, capacity: int, stats_tensor, left=None, is_last=True,
+             left_state=None):
+        """left: device bytes just before the range (the halo); left_state: the DFA state before left[0]
+        (None: unknown — straddling typed fields with inner control bytes are then unsupported)."""
         L = _lib.load()
         ctx = _lib.Context_t(self.entry_state, 0, self.base, prefix)
         sch = schema.struct()
         arr = _col_array(columns)
         lptr = ctypes.c_void_p(left.data_ptr()) if left is not None and left.numel() else None
         llen = left.numel() if left is not None else 0
-        _check(L.parpa_range_emit(self.handle, ctypes.byref(sch), ctypes.byref(ctx), lptr, llen, int(bool(is_last)),
-                                  arr, int(capacity), ctypes.c_void_p(stats_tensor.data_ptr()),
-                                  _stream_handle(self._stream)), "parpa_range_emit")
+        ls = STATE_UNKNOWN if left_state is None or not llen else int(left_state)
+        _check(L.parpa_range_emit_halo(self.handle, ctypes.byref(sch), ctypes.byref(ctx), lptr, llen, ls,
+                                       int(bool(is_last)), arr, int(capacity),
+                                       ctypes.c_void_p(stats_tensor.data_ptr()), _stream_handle(self._stream)),
+               "parpa_range_emit_halo")
 
     def close(self):
         if getattr(self, "handle", None) and self.handle.value:

@@ -247,6 +247,7 @@ void make_args(KArgs &a, const Work &w, const uint8_t *in, uint64_t len) {
   a.dq_cap = w.dq_cap;
   a.is_last = 1;
   a.cap = 0;
+  a.left_state = 0xFFu;                                     // no halo state known
 }
 
 int prepare_input(Work &w, const uint8_t *&in, uint64_t len, cudaStream_t s) {
@@ -1134,7 +1135,25 @@ int parpa_range_count(parpa_plan *p, uint32_t entry_state, parpa_counts *out) {
 int parpa_range_emit(parpa_plan *p, const parpa_schema *sch, const parpa_context *ctx, const uint8_t *left,
                      uint64_t left_len, int is_last, const parpa_column *cols, uint64_t cap, parpa_stats *d_stats,
                      void *stream) {
+  return parpa_range_emit_halo(p, sch, ctx, left, left_len, PARPA_STATE_UNKNOWN, is_last, cols, cap, d_stats, stream);
+}
+
+int parpa_range_state_at(const parpa_plan *p, uint64_t pos, uint32_t *state) {
+  if (!p || !state || pos < p->a.base || pos >= p->a.base + p->len || ((pos - p->a.base) % CHUNK) != 0 ||
+      p->a.seed_dev > INV_DEV)
+    return PARPA_EINVAL;
+  uint8_t d = 0;
+  CK(cudaMemcpyAsync(&d, p->w.chunk_state + (pos - p->a.base) / CHUNK, 1, cudaMemcpyDeviceToHost, p->s));
+  CK(cudaStreamSynchronize(p->s));
+  *state = p->dfa->k.hmap[d & 0xF];
+  return PARPA_OK;
+}
+
+int parpa_range_emit_halo(parpa_plan *p, const parpa_schema *sch, const parpa_context *ctx, const uint8_t *left,
+                          uint64_t left_len, uint32_t left_state, int is_last, const parpa_column *cols, uint64_t cap,
+                          parpa_stats *d_stats, void *stream) {
   if (!p || !sch || !ctx || !d_stats || (sch->num_columns && !cols)) return PARPA_EINVAL;
+  if (left_state != PARPA_STATE_UNKNOWN && (left_state >= p->dfa->S || !left || !left_len)) return PARPA_EINVAL;
   if (ctx->entry_state >= p->dfa->S || p->dfa->dmap[ctx->entry_state] != p->a.seed_dev) return PARPA_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   ColsK ck;
@@ -1149,6 +1168,7 @@ int parpa_range_emit(parpa_plan *p, const parpa_schema *sch, const parpa_context
   a.row_base = a.seed.recs;
   a.left = left;
   a.left_len = left_len;
+  a.left_state = left_state == PARPA_STATE_UNKNOWN ? 0xFFu : p->dfa->dmap[left_state];
   a.is_last = is_last;
   if ((rc = reset_emit_state(p, s))) return rc;
   rc = launch_emit(a, p->dfa->k, ck, s, nullptr);

@@ -104,6 +104,8 @@ struct KArgs {
   unsigned long long len, base;      // bytes of this range, global offset of in[0]
   const uint8_t *left;               // bytes preceding the range (multi-GPU halo), may be null
   unsigned long long left_len;
+  uint32_t left_state;               // device state before left[0] (the halo's entry state), 0xFF unknown
+  uint32_t pad_ls;
   uint32_t ntiles, seed_dev, is_last, C;
   Seg seed;                          // composed prefix of everything before the range
   unsigned long long row_base;       // global record index of local row 0
@@ -1201,7 +1203,7 @@ struct DfaDataSrc {                   // DATA bytes of [fd, ld], re-simulated fr
   bool ok;
   __device__ bool next(uint8_t &c) {
     while (pos <= end) {
-      uint8_t b = a->in[pos - a->base];
+      const uint8_t b = fetch_byte(*a, pos, ok);       // the left context (halo) before the range
       pos++;
       uint32_t step_lo = d->lut[b][2], step_hi = d->lut[b][3];
       uint32_t prev = x;
@@ -1219,18 +1221,31 @@ __device__ void convert_deferred(const KArgs &a, const DfaK &dfa, const ColDesc 
   long long v = 0;
   int ok = 0;
   if (ic) {
-    if (fd < a.base) {
-      atomicOr(&a.ctrl->unsupported, 1u);            // a span crossing into a previous range with inner
-    } else {                                          // control bytes (multi-GPU) is not handled
-      unsigned long long local = fd - a.base;
-      unsigned long long k = local / CHUNK;
-      uint32_t x = 0x80u | a.chunk_state[k];
-      for (unsigned long long p = k * CHUNK; p < local; p++) {
-        uint8_t b = a.in[p];
+    unsigned long long from;                         // a position whose state is known, and the state
+    uint32_t x;
+    bool known = true;
+    if (fd >= a.base) {
+      const unsigned long long k = (fd - a.base) / CHUNK;
+      from = a.base + k * CHUNK;
+      x = 0x80u | a.chunk_state[k];
+    } else if (a.left && a.left_state != 0xFFu && fd >= a.base - a.left_len) {
+      from = a.base - a.left_len;                    // the halo's first byte, whose state the sender gave
+      x = 0x80u | a.left_state;
+    } else {
+      known = false;                                 // a span crossing into a previous range with inner
+      from = fd;                                     // control bytes and no left context: unsupported
+      x = 0u;
+      atomicOr(&a.ctrl->unsupported, 1u);
+    }
+    if (known) {
+      bool okb = true;
+      for (unsigned long long p = from; p < fd; p++) {
+        const uint8_t b = fetch_byte(a, p, okb);
         x = prmt(dfa.lut[b][2], dfa.lut[b][3], x);
       }
       DfaDataSrc src{&a, &dfa, fd, ld, x, true};
       ok = conv_typed_exact<TS>(src, cd->type, v);
+      if (!src.ok || !okb) { ok = 0; atomicOr(&a.ctrl->unsupported, 1u); }
     }
   } else {
     RawSrc src{&a, fd, ld, true};

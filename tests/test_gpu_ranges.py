@@ -26,7 +26,7 @@ def dev(a):
     return t[:len(a)]
 
 
-def sharded_parse(dialect, data, types, cuts, left_bytes=4096, staged=False):
+def sharded_parse(dialect, data, types, cuts, left_bytes=4096, staged=False, halo=False):
     """Parse every range as its own "rank" and assemble the global columns.  Columns stay sharded
     (SURVEY §8e): the record straddling cut g has its columns < col(g) on rank g-1 (local row
     R_local) and the rest on rank g (local row 0).  staged=True uses the range plan
@@ -48,6 +48,12 @@ def sharded_parse(dialect, data, types, cuts, left_bytes=4096, staged=False):
         counts.append(c)
     C = len(types)
     out = [[[] for _ in range(4)] for _ in range(C)]
+    hplan = {}
+    if halo:                     # the exact halo of distributed.halo_plan, state from the owner's plan
+        assert staged
+        bases, lens = cuts[:-1], [cuts[g + 1] - cuts[g] for g in range(G)]
+        open_first = [pdist.prefix_counts(counts, g).open_first for g in range(G)]
+        hplan = pdist.halo_plan(bases, lens, open_first)
     for g in range(G):
         e = pdist.entry_state(dfa, taus, g)
         prefix = pdist.prefix_counts(counts, g)
@@ -58,8 +64,14 @@ def sharded_parse(dialect, data, types, cuts, left_bytes=4096, staged=False):
         st = parpa.new_stats_tensor()
         left = dev(data[max(0, lo - left_bytes):lo]) if lo else None
         last = g == G - 1
+        left_state = None
+        if halo:
+            left = None
+            if g in hplan:
+                h, r0, _ = hplan[g]
+                left, left_state = dev(data[h:lo]), plans[r0].state_at(h)
         if staged:
-            plans[g].emit(schema, prefix, cols, cap, st, left=left, is_last=last)
+            plans[g].emit(schema, prefix, cols, cap, st, left=left, is_last=last, left_state=left_state)
         else:
             parpa.parse_range(dfa, schema, dev(data[lo:hi]), e, lo, prefix, cols, cap, st, left=left, is_last=last)
         s = parpa.stats_from_tensor(st)
@@ -191,3 +203,41 @@ def test_range_plan_repeated_count_and_emit():
                     assert np.array_equal(to_np(cols[c].valid).view(np.uint8)[:ora.R], ora.valid[c])
     finally:
         plan.close()
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_virtual_ranks_exact_halo_long_and_inner_control_fields(seed):
+    """The cross-rank halo (distributed.halo_plan): each range receives exactly the bytes of the field
+    straddling its start, from the owner's chunk boundary, with the DFA state there.  Fields of 4-9 KB
+    straddle the cuts: quoted numbers with "" inside (inner control bytes: the device tier re-simulates
+    the halo from its state — before this, PARPA_EUNSUPPORTED), long floats and long quoted text."""
+    rng = random.Random(seed)
+    rows = []
+    for i in range(3000):
+        a = rng.randint(-999, 999)
+        b = f"{rng.randint(0, 99999)}.{rng.randint(0, 999)}"
+        t = '"' + "".join(rng.choice("abc ,\n") for _ in range(rng.randint(0, 60))) + '"'
+        rows.append(f"{a},{b},{t}\n")
+    giants = ['"1' + "2" * 4500 + '""' + "3" * 3000 + '"',       # typed, inner control byte: invalid
+              "1" * 6000 + "." + "5" * 2000,                     # a 8 KB float: valid, device tier
+              '"' + "7" * 5000 + '"']                            # a quoted 5 KB integer: invalid (overflow)
+    pos = sorted(rng.sample(range(100, 2900), 6))
+    for k, p in enumerate(pos):
+        g = giants[k % 3]
+        rows[p] = (f"{g},1.5,x\n" if k % 3 != 1 else f"3,{g},\"t\"\n")
+    data = "".join(rows).encode()
+    types = [oracle.INT64, oracle.FLOAT64, oracle.SPAN]
+    ora = oracle.parse("csv", data, 3, types)
+    assert ora.status == 0
+    # cut inside the giant fields (and elsewhere)
+    starts = [data.index(g.encode()) for g in giants if g.encode() in data]
+    inner = sorted(set([s0 + 2500 for s0 in starts] + rng.sample(range(1, len(data) - 1), 2)))
+    cuts = [0] + inner + [len(data)]
+    cols = sharded_parse("csv", data, types, cuts, staged=True, halo=True)
+    for c, t in enumerate(types):
+        off, ln, val, ok = cols[c]
+        assert np.array_equal(off, ora.offset[c]), c
+        assert np.array_equal(ln, ora.length[c]), c
+        if t != oracle.SPAN:
+            assert np.array_equal(ok, ora.valid[c]), c
+            assert np.array_equal(val, ora.value[c]), c
