@@ -64,7 +64,11 @@ typedef struct parpa_result parpa_result;
  * parpa_create_dfa — compile a parsing DFA ("uses a DFA while parsing"; P:727:
  * "collapse all the transition table's symbols that have identical state transitions into
  * symbol groups"; tab:ttable row-per-group layout).
- *   num_states      |S|, 2..16 (this build runs |S|-1 <= 8 non-invalid states, else EUNSUPPORTED)
+ *   num_states      |S|, 2..16.  The device works on classes of non-invalid states with identical
+ *                   transition and emission rows (states that differ only in their eoi action, such as
+ *                   CSV's EOR / EOF, share a class; the exact state is recovered wherever it is reported
+ *                   or decides the end-of-input action).  This build runs up to 8 classes (else
+ *                   PARPA_EUNSUPPORTED); with at most 4 — CSV — pass 1 composes with one PRMT per byte.
  *   start_state     the sequential parser's starting state (reading R1)
  *   invalid_state   the INV state; must be absorbing: transition[g][inv] == inv for all g,
  *                   and emit[g][inv] == PARPA_CTRL
@@ -281,7 +285,8 @@ int parpa_range_emit(parpa_plan *plan, const parpa_schema *schema, const parpa_c
  * A field whose DATA begins on an earlier rank (its first DATA byte = the composed prefix's open_first
  * < base) needs those bytes to be converted; if control bytes lie inside it, also the DFA state at
  * some earlier position (the device tier re-simulates to drop them).
- * parpa_range_state_at   *state = the DFA state before the byte at global offset `pos` of this range,
+ * parpa_range_state_at   *state = the DFA state before the byte at global offset `pos` of this range (a
+ *                        member of its class, which parses identically),
  *                        for pos - base a multiple of parpa_chunk_bytes() (after parpa_range_count;
  *                        synchronous).  The rank holding the start of a straddling field sends the bytes
  *                        from that chunk boundary on, with this state, to the ranks that need them.

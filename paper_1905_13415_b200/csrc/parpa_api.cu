@@ -454,6 +454,52 @@ void host_tau_dfa(const parpa_dfa *d, uint32_t nib, parpa_tau *out) {
   }
 }
 
+// ---- exact states where device classes merged DFA states (see DfaK) ----------------------------------
+uint32_t host_class_step(const parpa_dfa *d, uint32_t c, uint8_t b) {
+  return c == INV_DEV ? INV_DEV : d->dmap[d->trans[d->gob[b]][d->k.hmap[c]]];
+}
+uint32_t host_exact_after(const parpa_dfa *d, uint32_t cls_before_last, uint8_t last) {
+  return cls_before_last == INV_DEV ? d->inv : d->trans[d->gob[last]][d->k.hmap[cls_before_last]];
+}
+// The range's transition vector in DFA numbering with exact entries: the class vector over all but the
+// last byte (tile prefix ∘ lane prefix, then the last chunk's bytes on the host), then the last byte's
+// exact row.  Needs lex / wpre of a completed pass 1 + τ scan.
+int host_tau_exact(const parpa_dfa *d, const Work &w, const uint8_t *in, uint64_t len, uint32_t tot_nib,
+                   cudaStream_t s, parpa_tau *out) {
+  if (!d->k.merged || len == 0) { host_tau_dfa(d, tot_nib, out); return PARPA_OK; }
+  const uint64_t kc = (len - 1) / CHUNK, t = kc / 32;
+  uint32_t lex = 0, wpre = 0;
+  uint8_t bytes[CHUNK];
+  const uint64_t nb = len - kc * CHUNK;
+  CK(cudaMemcpyAsync(&lex, w.lex + kc, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&wpre, w.wpre + t, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(bytes, in + kc * CHUNK, nb, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (int i = 0; i < 16; i++) out->tau[i] = 0xFF;
+  for (uint32_t st = 0; st < d->S; st++) {
+    uint32_t c = nib_at(lex, nib_at(wpre, d->dmap[st]));
+    for (uint64_t q = 0; q + 1 < nb; q++) c = host_class_step(d, c, bytes[q]);
+    out->tau[st] = (uint8_t)host_exact_after(d, c, bytes[nb - 1]);
+  }
+  return PARPA_OK;
+}
+// The exact DFA state after a scanned range (for its end-of-input action on the host): the class
+// before the last byte from the last chunk's entry state, then the last byte's exact row.
+int host_final_exact(const parpa_dfa *d, const Work &w, const uint8_t *in, uint64_t len, uint32_t fin_class,
+                     uint32_t seed_exact, cudaStream_t s, uint32_t &exact) {
+  if (len == 0) { exact = seed_exact; return PARPA_OK; }
+  if (!d->k.merged) { exact = d->k.hmap[fin_class]; return PARPA_OK; }
+  const uint64_t kc = (len - 1) / CHUNK, nb = len - kc * CHUNK;
+  uint8_t st = 0, bytes[CHUNK];
+  CK(cudaMemcpyAsync(&st, w.chunk_state + kc, 1, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(bytes, in + kc * CHUNK, nb, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  uint32_t c = st & 0xFu;
+  for (uint64_t q = 0; q + 1 < nb; q++) c = host_class_step(d, c, bytes[q]);
+  exact = host_exact_after(d, c, bytes[nb - 1]);
+  return PARPA_OK;
+}
+
 }  // namespace
 
 struct parpa_plan {
@@ -525,7 +571,6 @@ int parpa_create_dfa(uint32_t S, uint32_t start, uint32_t inv, uint32_t G, const
     if (trans[g * S + inv] != inv || emit[g * S + inv] != PARPA_CTRL) return PARPA_EINVAL;
   for (uint32_t s = 0; s < S; s++)
     if (eoi[s] > PARPA_EOI_ERROR) return PARPA_EINVAL;
-  if (S - 1 > 8) return PARPA_EUNSUPPORTED;
   parpa_dfa *d = new (std::nothrow) parpa_dfa;
   if (!d) return PARPA_ENOMEM;
   memset(d, 0, sizeof(*d));
@@ -537,15 +582,32 @@ int parpa_create_dfa(uint32_t S, uint32_t start, uint32_t inv, uint32_t G, const
       d->emit[g][s] = emit[g * S + s];
     }
   memcpy(d->eoi, eoi, S);
-  // device numbering: live states 0..k-1 in order, INV -> 0xF
-  uint32_t live[8], k = 0;
+  // device states = classes of live states with identical transition and emission rows (in order of
+  // their first member); INV -> 0xF
+  uint32_t rep[16], k = 0;
   for (uint32_t s = 0; s < S; s++) {
     if (s == inv) { d->dmap[s] = INV_DEV; continue; }
-    d->dmap[s] = (uint8_t)k;
-    live[k++] = s;
+    uint32_t j = 0;
+    for (; j < k; j++) {
+      bool same = true;
+      for (uint32_t g = 0; g < G && same; g++)
+        same = d->trans[g][s] == d->trans[g][rep[j]] && d->emit[g][s] == d->emit[g][rep[j]];
+      if (same) break;
+    }
+    if (j == k) rep[k++] = s;
+    d->dmap[s] = (uint8_t)j;
   }
+  if (k > 8) { delete d; return PARPA_EUNSUPPORTED; }
+  d->k.nlive = k;
+  d->k.merged = k < S - 1 ? 1u : 0u;
+  d->k.inv_state = inv;
+  memcpy(d->k.gob, gob, 256);
+  for (uint32_t s = 0; s < S; s++) d->k.eoi_state[s] = eoi[s];
   for (int j = 0; j < 16; j++) { d->k.hmap[j] = (uint8_t)inv; d->k.eoi[j] = eoi[inv]; }
-  for (uint32_t j = 0; j < k; j++) { d->k.hmap[j] = (uint8_t)live[j]; d->k.eoi[j] = eoi[live[j]]; }
+  for (uint32_t j = 0; j < k; j++) { d->k.hmap[j] = (uint8_t)rep[j]; d->k.eoi[j] = eoi[rep[j]]; }
+  for (uint32_t j = 0; j < 16; j++)
+    for (uint32_t g = 0; g < 16; g++)
+      d->k.next_exact[j][g] = (uint8_t)(j < k && g < G ? d->trans[g][rep[j]] : inv);
   for (int b = 0; b < 256; b++) {
     uint32_t g = gob[b];
     uint32_t sel = 0;
@@ -553,7 +615,7 @@ int parpa_create_dfa(uint32_t S, uint32_t start, uint32_t inv, uint32_t G, const
     for (uint32_t j = 0; j < 8; j++) {
       uint32_t nd = INV_DEV, kind = PARPA_CTRL;
       if (j < k) {
-        uint32_t s = live[j];
+        uint32_t s = rep[j];
         nd = d->dmap[d->trans[g][s]];
         kind = d->emit[g][s];
       }
@@ -593,7 +655,7 @@ int parpa_last_kernel_times(const char **names, float *ms, int cap) {
 }
 
 // ---- plan: scan pass -------------------------------------------------------------------------
-static int plan_scan(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint32_t seed_dev,
+static int plan_scan(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint32_t seed_state,
                      const Seg &seed, uint64_t base, uint32_t C, cudaStream_t s, parpa_plan *p) {
   p->dfa = dfa;
   p->len = len;
@@ -604,7 +666,8 @@ static int plan_scan(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len,
   if ((rc = prepare_input(p->w, in, len, s))) return rc;
   p->in = in;
   make_args(p->a, p->w, in, len);
-  p->a.seed_dev = seed_dev;
+  p->a.seed_dev = dfa->dmap[seed_state];
+  p->a.seed_exact = seed_state;
   p->a.seed = seed;
   p->a.base = base;
   p->a.row_base = seed.recs;
@@ -636,14 +699,17 @@ int parpa_plan_create(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len
   parpa_plan *p = new (std::nothrow) parpa_plan;
   if (!p) return PARPA_ENOMEM;
   prof_begin();
-  int rc = plan_scan(dfa, d_bytes, len, dfa->dmap[dfa->start], seg_identity(), 0, 1024, s, p);
+  int rc = plan_scan(dfa, d_bytes, len, dfa->start, seg_identity(), 0, 1024, s, p);
   if (rc) { work_free(p->w, s); delete p; return rc; }
   Seg tot;
   uint32_t tau;
   uint64_t fi;
   if ((rc = plan_totals(p, tot, tau, fi))) { work_free(p->w, s); delete p; return rc; }
-  uint32_t fin = nib_at(tau, p->a.seed_dev);
-  p->records = tot.recs + (dfa->k.eoi[fin] == EOI_RECORD ? 1 : 0);
+  uint32_t fin = 0;
+  if ((rc = host_final_exact(dfa, p->w, p->in, len, nib_at(tau, p->a.seed_dev), p->a.seed_exact, s, fin))) {
+    work_free(p->w, s); delete p; return rc;
+  }
+  p->records = tot.recs + (dfa->eoi[fin] == EOI_RECORD ? 1 : 0);
   *out = p;
   return PARPA_OK;
 }
@@ -751,7 +817,7 @@ void parpa_result_free(parpa_result *r) {
 // ---- single-pass capacity path ------------------------------------------------------------------
 static int parse_into_impl(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_bytes, uint64_t len,
                            const parpa_column *cols, uint64_t cap, parpa_stats *d_stats, cudaStream_t s,
-                           uint32_t seed_dev, const Seg &seed, uint64_t base, const uint8_t *left,
+                           uint32_t seed_state, const Seg &seed, uint64_t base, const uint8_t *left,
                            uint64_t left_len, int is_last, uint32_t *launches) {
   if (!dfa || !sch || !d_stats || (len && !d_bytes) || (sch->num_columns && !cols)) return PARPA_EINVAL;
   ColsK ck;
@@ -770,7 +836,8 @@ static int parse_into_impl(const parpa_dfa *dfa, const parpa_schema *sch, const 
     a.strict = sch->strict;
     a.cap = cap;
     a.stats = (Stats *)d_stats;
-    a.seed_dev = seed_dev;
+    a.seed_dev = dfa->dmap[seed_state];
+    a.seed_exact = seed_state;
     a.seed = seed;
     a.base = base;
     a.row_base = seed.recs;
@@ -797,7 +864,7 @@ int parpa_parse_into(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_
                      uint32_t *gpu_launches) {
   if (!dfa) return PARPA_EINVAL;
   return parse_into_impl(dfa, sch, d_bytes, len, cols, cap, d_stats, (cudaStream_t)stream,
-                         dfa->dmap[dfa->start], seg_identity(), 0, nullptr, 0, 1, gpu_launches);
+                         dfa->start, seg_identity(), 0, nullptr, 0, 1, gpu_launches);
 }
 
 int parpa_parse_range(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_bytes, uint64_t len,
@@ -805,7 +872,7 @@ int parpa_parse_range(const parpa_dfa *dfa, const parpa_schema *sch, const uint8
                       const parpa_column *cols, uint64_t cap, parpa_stats *d_stats, void *stream) {
   if (!dfa || !ctx || ctx->entry_state >= dfa->S) return PARPA_EINVAL;
   return parse_into_impl(dfa, sch, d_bytes, len, cols, cap, d_stats, (cudaStream_t)stream,
-                         dfa->dmap[ctx->entry_state], counts_to_seg(ctx->prefix), ctx->base, left, left_len,
+                         ctx->entry_state, counts_to_seg(ctx->prefix), ctx->base, left, left_len,
                          is_last, nullptr);
 }
 
@@ -1043,9 +1110,9 @@ int parpa_summarize(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, 
   if (!rc && w.ntiles) {
     if (cudaMemcpyAsync(&desc, w.tot_tau, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = PARPA_ECUDA;
   }
-  work_free(w, s);
   if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
-  if (!rc) host_tau_dfa(dfa, (uint32_t)desc, out);
+  if (!rc) rc = host_tau_exact(dfa, w, in, len, (uint32_t)desc, s, out);
+  work_free(w, s);
   return rc;
 }
 
@@ -1054,16 +1121,16 @@ int parpa_count(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint
   if (!dfa || !out || entry >= dfa->S || (len && !d_bytes)) return PARPA_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   parpa_plan p;
-  int rc = plan_scan(dfa, d_bytes, len, dfa->dmap[entry], seg_identity(), base, 1, s, &p);
+  int rc = plan_scan(dfa, d_bytes, len, entry, seg_identity(), base, 1, s, &p);
   Seg tot;
   uint32_t tau = NIB_IDENT;
   uint64_t fi = NONE;
   if (!rc) rc = plan_totals(&p, tot, tau, fi);
-  work_free(p.w, s);
   if (!rc) {
     *out = seg_to_counts(tot, fi);
-    if (tau_out) host_tau_dfa(dfa, tau, tau_out);
+    if (tau_out) rc = host_tau_exact(dfa, p.w, p.in, len, tau, s, tau_out);
   }
+  work_free(p.w, s);
   return rc;
 }
 
@@ -1111,8 +1178,8 @@ int parpa_range_begin(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len
     rc = PARPA_ECUDA;
   if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
   prof_end();
+  if (!rc) rc = host_tau_exact(dfa, p->w, p->in, len, tau, s, tau_out);
   if (rc) { work_free(p->w, s); delete p; return rc; }
-  host_tau_dfa(dfa, tau, tau_out);
   *out = p;
   return PARPA_OK;
 }
@@ -1121,6 +1188,7 @@ int parpa_range_count(parpa_plan *p, uint32_t entry_state, parpa_counts *out) {
   if (!p || !out || entry_state >= p->dfa->S) return PARPA_EINVAL;
   if (int rc0 = reset_scan_state(p)) return rc0;
   p->a.seed_dev = p->dfa->dmap[entry_state];
+  p->a.seed_exact = entry_state;
   int rc = launch_half2(p->a, p->dfa->k, p->s, nullptr);
   prof_end();
   if (rc) return rc;
@@ -1183,7 +1251,7 @@ int parpa_infer_columns(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t l
   if (!dfa || !min_fields || !max_fields || !records || (len && !d_bytes)) return PARPA_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   parpa_plan p;
-  int rc = plan_scan(dfa, d_bytes, len, dfa->dmap[dfa->start], seg_identity(), 0, 1, s, &p);
+  int rc = plan_scan(dfa, d_bytes, len, dfa->start, seg_identity(), 0, 1, s, &p);
   unsigned int *d_mm = nullptr;
   unsigned int mm[2] = {0xFFFFFFFFu, 0u};
   if (!rc && cudaMallocAsync(&d_mm, 8, s) != cudaSuccess) rc = PARPA_ENOMEM;
@@ -1200,12 +1268,13 @@ int parpa_infer_columns(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t l
   uint32_t tau;
   uint64_t fi;
   if (!rc) rc = plan_totals(&p, tot, tau, fi);               // synchronises
+  uint32_t fin = 0;
+  if (!rc) rc = host_final_exact(dfa, p.w, p.in, len, nib_at(tau, p.a.seed_dev), p.a.seed_exact, s, fin);
   if (d_mm) cudaFreeAsync(d_mm, s);
   work_free(p.w, s);
   if (rc) return rc;
   uint64_t R = tot.recs;
-  const uint32_t fin = nib_at(tau, p.a.seed_dev);
-  if (dfa->k.eoi[fin] == EOI_RECORD) {                         // the implicit last record
+  if (dfa->eoi[fin] == EOI_RECORD) {                         // the implicit last record
     const uint32_t n = tot.col + 1;
     mm[0] = std::min(mm[0], n);
     mm[1] = std::max(mm[1], n);
@@ -1286,6 +1355,7 @@ static int strings_impl(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t l
   KArgs a;
   make_args(a, w, in, len);
   a.seed_dev = dfa->dmap[dfa->start];
+  a.seed_exact = dfa->start;
   if (!rc) rc = launch_passes(MODE_COUNT, a, dfa->k, s, nullptr);       // the chunk masks
   DevCfg *dc = nullptr;
   if (!rc) rc = dev_cfg(&dc);
@@ -1344,7 +1414,7 @@ int parpa_debug_trace(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len
   if (!dfa || (len && !d_bytes)) return PARPA_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   parpa_plan p;
-  int rc = plan_scan(dfa, d_bytes, len, dfa->dmap[dfa->start], seg_identity(), 0, 1, s, &p);
+  int rc = plan_scan(dfa, d_bytes, len, dfa->start, seg_identity(), 0, 1, s, &p);
   if (!rc && len) {
     k_debug_trace<<<1024, 128, 0, s>>>(p.a, dfa->k, d_chunk_states, d_kinds, d_states);
     if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;

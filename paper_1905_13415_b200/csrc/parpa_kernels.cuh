@@ -47,10 +47,19 @@ __device__ __forceinline__ int conv_typed_exact(Src &s, uint32_t type, long long
 enum { EOI_NONE = 0, EOI_RECORD = 1, EOI_ERROR = 2 };
 enum { ST_OK = 0, ST_EFORMAT = -4, ST_ECOLUMNS = -5, ST_EUNSUPPORTED = -6, ST_ENEEDMORE = -7 };
 
+// Device states are CLASSES of live DFA states with identical transition and emission rows (they may
+// differ only in their end-of-input action, e.g. CSV's EOR and EOF): CSV's five live states become
+// four, so pass 1 composes τ with one PRMT per byte instead of two.  Where the exact member matters
+// (the end-of-input action, reported states) it is recovered from the byte before: members of a class
+// share their rows, so the state after a byte is exact (next_exact) whatever member the class stood for.
 struct DfaK {                       // compiled DFA, passed by value (kernel parameter space)
   uint32_t lut[256][4];             // per byte: {sel_lo, sel_hi, step_lo, step_hi}
-  uint8_t hmap[16];                 // device state -> DFA state (index 15 = INV)
-  uint8_t eoi[16];                  // EOI action by device state
+  uint8_t hmap[16];                 // device state -> DFA state (its first member; index 15 = INV)
+  uint8_t eoi[16];                  // EOI action by device state (of its first member)
+  uint8_t gob[256];                 // byte -> symbol group
+  uint8_t next_exact[16][16];       // [device state][group] -> exact DFA state after the byte
+  uint8_t eoi_state[16];            // EOI action by DFA state
+  uint32_t nlive, merged, inv_state, pad;   // device states in use; 1 if some class has > 1 member
 };
 
 struct ColDesc {
@@ -107,6 +116,7 @@ struct KArgs {
   uint32_t left_state;               // device state before left[0] (the halo's entry state), 0xFF unknown
   uint32_t pad_ls;
   uint32_t ntiles, seed_dev, is_last, C;
+  uint32_t seed_exact, pad_se;       // the DFA state seed_dev stands for (exact; for an empty range's EOI)
   Seg seed;                          // composed prefix of everything before the range
   unsigned long long row_base;       // global record index of local row 0
   unsigned long long cap;            // rows per column
@@ -145,7 +155,10 @@ __device__ __forceinline__ uint2 lds_u2(uint32_t addr) {
 __device__ __forceinline__ void build_lut(uint8_t *lut, const DfaK &d) {
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
     int b = i >> 5, half = (i >> 4) & 1, slot = i & 15;
-    uint2 v = half ? make_uint2(d.lut[b][2], d.lut[b][3]) : make_uint2(d.lut[b][0], d.lut[b][1]);
+    // (at most four device states: the τ half holds sel_lo in 32 four-byte slots, one per lane, so the
+    // 32-bit loads of chunk_tau4<NS4> never share a bank between lanes l and l + 16)
+    uint2 v = half ? make_uint2(d.lut[b][2], d.lut[b][3])
+                   : make_uint2(d.lut[b][0], d.nlive <= 4 ? d.lut[b][0] : d.lut[b][1]);
     *reinterpret_cast<uint2 *>(lut + b * 256 + half * 128 + slot * 8) = v;
   }
 }
@@ -213,7 +226,15 @@ __device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_
 
 // ---- 4-way ILP τ: the chunk is cut into four 16-byte quarters with independent PRMT chains, composed
 // at the end.  qt[q] = nibble τ of quarter q (q = 0..2).
-template <bool FULL>
+__device__ __forceinline__ uint32_t lds_u1(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+// NS4: at most four device states (+ INV): τ in byte form fits one register, and one PRMT per byte
+// composes it (selector nibbles 0-3 pick bytes 0-3; an INV nibble 0xF replicates the sign of byte 7,
+// which is byte 3 of the same register — set, so INV stays INV).
+template <bool FULL, bool NS4 = false>
 __device__ __forceinline__ void chunk_tau4(uint32_t laneaddr, const uint32_t (&v)[16], int nvalid,
                                            uint32_t &t0, uint32_t &t1, uint32_t (&qt)[3]) {
   uint32_t a0[4], a1[4];
@@ -225,11 +246,16 @@ __device__ __forceinline__ void chunk_tau4(uint32_t laneaddr, const uint32_t (&v
     for (int q = 0; q < 4; q++) {
       const int b = 16 * q + i;
       if (!FULL && b >= nvalid) continue;
-      const uint2 e = lds_u2<0>(prmt(v[b >> 2], laneaddr, 0x5604u | ((uint32_t)(b & 3) << 4)));
-      uint32_t n0 = prmt(a0[q], a1[q], e.x);
-      uint32_t n1 = prmt(a0[q], a1[q], e.y);
-      a0[q] = n0;
-      a1[q] = n1;
+      const uint32_t ad = prmt(v[b >> 2], laneaddr, 0x5604u | ((uint32_t)(b & 3) << 4));
+      if (NS4) {
+        a0[q] = prmt(a0[q], a0[q], lds_u1(ad));
+      } else {
+        const uint2 e = lds_u2<0>(ad);
+        uint32_t n0 = prmt(a0[q], a1[q], e.x);
+        uint32_t n1 = prmt(a0[q], a1[q], e.y);
+        a0[q] = n0;
+        a1[q] = n1;
+      }
     }
   }
   uint32_t n[4];
@@ -1151,12 +1177,26 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const
 __device__ void finalize_one(const KArgs &a, const DfaK &dfa, const ColsK &colsk) {   // one thread
   Seg tot = a.ntiles ? seg_op(a.seed, *a.tot_seg) : a.seed;
   uint32_t tau = a.ntiles ? *a.tot_tau : NIB_IDENT;
-  uint32_t fin = nib_at(tau, a.seed_dev);
+  const uint32_t fin = nib_at(tau, a.seed_dev);
+  // the exact final DFA state: the class's member if it has one member, else from the last byte
+  uint32_t fin_exact = dfa.hmap[fin];
+  if (a.len == 0) {
+    fin_exact = a.seed_exact;
+  } else if (dfa.merged) {
+    const unsigned long long kc = (a.len - 1) / CHUNK;
+    uint32_t x = 0x80u | a.chunk_state[kc];
+    for (unsigned long long p = kc * CHUNK; p + 1 < a.len; p++) {
+      const uint8_t b = a.in[p];
+      x = prmt(dfa.lut[b][2], dfa.lut[b][3], x);
+    }
+    const uint32_t cb = x & 0xFu;
+    fin_exact = cb == INV_DEV ? dfa.inv_state : dfa.next_exact[cb][dfa.gob[a.in[a.len - 1]]];
+  }
   EmitCounters cnt{0ull, 0ull, 0u};
   unsigned long long R = tot.recs, nf = tot.nflds;
   unsigned long long first_inv = a.ctrl->inv_neg ? ~a.ctrl->inv_neg : NONE;
   if (a.is_last) {
-    uint32_t act = dfa.eoi[fin];
+    uint32_t act = dfa.eoi_state[fin_exact];
     unsigned long long end = a.base + a.len;
     if (act == EOI_RECORD) {                               // implicit record delimiter at EOI
       emit_field<true>(a, colsk.c, R, tot.col, tot.fd, tot.ld, tot.flags & (F_IC | F_PC | F_PRE), end, cnt);
@@ -1183,7 +1223,7 @@ __device__ void finalize_one(const KArgs &a, const DfaK &dfa, const ColsK &colsk
     a.stats->extra_fields = extra;
     a.stats->deferred_fields = n_defer;
     a.stats->status = status;
-    a.stats->final_state = dfa.hmap[fin];
+    a.stats->final_state = fin_exact;
   }
 }
 __global__ void k_finalize(const __grid_constant__ KArgs a, const __grid_constant__ DfaK dfa,
@@ -1301,19 +1341,37 @@ __global__ void k_deferred(const __grid_constant__ KArgs a, const __grid_constan
 }
 
 // ---- debug trace (tests): per-byte state-before and emission kind ---------------------------------
-__global__ void k_debug_trace(const KArgs a, const DfaK dfa, uint8_t *chunk_states_out, uint8_t *kinds,
-                              uint8_t *states) {
+__global__ void k_debug_trace(const __grid_constant__ KArgs a, const __grid_constant__ DfaK dfa,
+                              uint8_t *chunk_states_out, uint8_t *kinds, uint8_t *states) {
+  // exact DFA states: the state before byte p is next_exact[class before byte p-1][group of byte p-1]
+  // (the class before the first byte of a chunk comes from re-simulating the chunk before it)
   unsigned long long nchunks = (a.len + CHUNK - 1) / CHUNK;
   for (unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; k < nchunks;
        k += (unsigned long long)gridDim.x * blockDim.x) {
-    uint32_t st = a.chunk_state[k];
-    if (chunk_states_out) chunk_states_out[k] = dfa.hmap[st];
+    uint32_t prev_cls = 0xFFu, prev_b = 0u;                  // class before / value of the byte before chunk k
+    if (k > 0) {
+      uint32_t y = 0x80u | a.chunk_state[k - 1];
+      for (unsigned long long p = (k - 1) * CHUNK; p + 1 < k * CHUNK; p++) {
+        const uint8_t b = a.in[p];
+        y = prmt(dfa.lut[b][2], dfa.lut[b][3], y);
+      }
+      prev_cls = y & 0xFu;
+      prev_b = a.in[k * CHUNK - 1];
+    }
+    auto exact = [&](uint32_t cls_before_prev, uint32_t bprev) -> uint32_t {
+      return cls_before_prev == INV_DEV ? dfa.inv_state : dfa.next_exact[cls_before_prev][dfa.gob[bprev]];
+    };
+    const uint32_t st = a.chunk_state[k];
+    const uint32_t e0 = k == 0 ? a.seed_exact : exact(prev_cls, prev_b);
+    if (chunk_states_out) chunk_states_out[k] = (uint8_t)e0;
     if (!kinds && !states) continue;
     uint32_t x = 0x80u | st;
     unsigned long long end = min(a.len, (k + 1) * CHUNK);
     for (unsigned long long p = k * CHUNK; p < end; p++) {
       uint8_t b = a.in[p];
-      if (states) states[p] = dfa.hmap[x & 0xFu];
+      if (states) states[p] = (uint8_t)(p == k * CHUNK ? e0 : exact(prev_cls, prev_b));
+      prev_cls = x & 0xFu;
+      prev_b = b;
       x = prmt(dfa.lut[b][2], dfa.lut[b][3], x);
       const uint32_t kc = step_kind_code(x);
       uint8_t kind = kc == KC_RECORD ? 3 : kc == KC_FIELD ? 2 : kc == KC_DATA ? 0 : 1;   // parpa_emit codes

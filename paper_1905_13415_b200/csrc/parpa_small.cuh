@@ -88,8 +88,14 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 1) k_small(const __grid_cons
     const int nv = chunk_valid(a, cstart);
     uint32_t v[16], t0, t1, qt[3];
     load_chunk(a.in + cstart, nv, v);
-    if (nv == CHUNK) chunk_tau4<true>(laneaddr, v, nv, t0, t1, qt);
-    else chunk_tau4<false>(laneaddr, v, nv, t0, t1, qt);
+    if (dfa.nlive <= 4) {
+      const uint32_t la4 = (laneaddr & ~0xFFu) | ((uint32_t)lane * 4u);   // one 4-byte slot per lane
+      if (nv == CHUNK) chunk_tau4<true, true>(la4, v, nv, t0, t1, qt);
+      else chunk_tau4<false, true>(la4, v, nv, t0, t1, qt);
+    } else {
+      if (nv == CHUNK) chunk_tau4<true>(laneaddr, v, nv, t0, t1, qt);
+      else chunk_tau4<false>(laneaddr, v, nv, t0, t1, qt);
+    }
     uint32_t agg;
     const uint32_t ex = warp_scan_tau(t0, t1, agg);
     a.lex[(unsigned long long)t * 32 + lane] = ex;

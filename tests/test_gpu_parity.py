@@ -540,3 +540,17 @@ def test_strings_and_types_adversarial(kind):
     ora = oracle.infer_types(dialect, data, C)
     assert got == [t for t, _ in ora], (got, ora)
     assert masks == [sum(1 << oracle.CLASSES.index(x) for x in cls) for _, cls in ora]
+
+
+def test_merged_states_exact_at_the_end():
+    """Device states are classes of DFA states with identical rows (CSV: EOR and EOF differ only in their
+    end-of-input action).  Inputs ending in each of them must still take the right EOI action, report
+    the exact final state, and summarise to the exact transition vector (the oracle's final state)."""
+    for data in [b"a,b\nc,", b",", b"x,\n", b"1,2\n3,4\n" * 40 + b"5,", b"q\n" * 70, b'"a",', b'a,"b"\n,']:
+        types = [oracle.INT64, oracle.SPAN]
+        ora = run_all_paths("csv", data, types, label=repr(data[-8:]))
+        ro = oracle.parse("csv", data, 2, types, trace=True)
+        tau = parpa.summarize(dfa("csv"), dev(data))
+        assert tau[0] == ro.final_state, (data[-8:], tau, ro.final_state)
+        res = parpa.parse(dfa("csv"), parpa.Schema(types), dev(data))
+        assert res.stats["final_state"] == ro.final_state, (data[-8:], res.stats)
