@@ -152,13 +152,19 @@ __device__ __forceinline__ uint2 lds_u2(uint32_t addr) {
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2+%3];" : "=r"(v.x), "=r"(v.y) : "r"(addr), "n"(OFF));
   return v;
 }
+__device__ __forceinline__ uint32_t lds_u1(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ void build_lut(uint8_t *lut, const DfaK &d) {
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
     int b = i >> 5, half = (i >> 4) & 1, slot = i & 15;
     // (at most four device states: the τ half holds sel_lo in 32 four-byte slots, one per lane, so the
     // 32-bit loads of chunk_tau4<NS4> never share a bank between lanes l and l + 16)
-    uint2 v = half ? make_uint2(d.lut[b][2], d.lut[b][3])
-                   : make_uint2(d.lut[b][0], d.nlive <= 4 ? d.lut[b][0] : d.lut[b][1]);
+    const bool ns4 = d.nlive <= 4;
+    uint2 v = half ? make_uint2(d.lut[b][2], ns4 ? d.lut[b][2] : d.lut[b][3])
+                   : make_uint2(d.lut[b][0], ns4 ? d.lut[b][0] : d.lut[b][1]);
     *reinterpret_cast<uint2 *>(lut + b * 256 + half * 128 + slot * 8) = v;
   }
 }
@@ -191,7 +197,9 @@ __device__ __forceinline__ uint32_t gather4(uint32_t x, uint32_t bitmask, uint32
   return __umulhi(x & bitmask, mul) & 0xFu;
 }
 
-template <bool FULL>
+// NS4 (at most four device states): the step row fits one word (per-lane 4-byte slots, see build_lut)
+// and the step is PRMT(row, row, x) — an INV selector replicates the sign of byte 3.
+template <bool FULL, bool NS4 = false>
 __device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_t (&v)[16], int nvalid, uint32_t entry,
                                                 unsigned long long &Dm, unsigned long long &Fm,
                                                 unsigned long long &Rm) {
@@ -204,8 +212,14 @@ __device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_
     for (int k = 0; k < 4; k++) {
       int i = 4 * w + k;
       if (FULL || i < nvalid) {
-        const uint2 st = lds_u2<128>(prmt(v[w], laneaddr, 0x5604u | ((uint32_t)k << 4)));
-        x = prmt(st.x, st.y, x);
+        const uint32_t ad = prmt(v[w], laneaddr, 0x5604u | ((uint32_t)k << 4));
+        if (NS4) {
+          const uint32_t st = lds_u1(ad + 128u);
+          x = prmt(st, st, x);
+        } else {
+          const uint2 st = lds_u2<128>(ad);
+          x = prmt(st.x, st.y, x);
+        }
         xs[k] = x;
       } else {
         xs[k] = 0xFFu;                                    // outside the chunk: not data / delimiter
@@ -226,11 +240,6 @@ __device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_
 
 // ---- 4-way ILP τ: the chunk is cut into four 16-byte quarters with independent PRMT chains, composed
 // at the end.  qt[q] = nibble τ of quarter q (q = 0..2).
-__device__ __forceinline__ uint32_t lds_u1(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-  return v;
-}
 // NS4: at most four device states (+ INV): τ in byte form fits one register, and one PRMT per byte
 // composes it (selector nibbles 0-3 pick bytes 0-3; an INV nibble 0xF replicates the sign of byte 7,
 // which is byte 3 of the same register — set, so INV stays INV).

@@ -152,8 +152,14 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 1) k_small(const __grid_cons
     a.chunk_state[(unsigned long long)t * 32 + lane] = (uint8_t)entry;
     unsigned long long Dm, Fm, Rm;
     uint32_t fin;
-    if (nv == CHUNK) fin = chunk_masks<true>(laneaddr, v, nv, entry, Dm, Fm, Rm);
-    else fin = chunk_masks<false>(laneaddr, v, nv, entry, Dm, Fm, Rm);
+    if (dfa.nlive <= 4) {
+      const uint32_t la4 = (laneaddr & ~0xFFu) | ((uint32_t)lane * 4u);   // one 4-byte slot per lane
+      if (nv == CHUNK) fin = chunk_masks<true, true>(la4, v, nv, entry, Dm, Fm, Rm);
+      else fin = chunk_masks<false, true>(la4, v, nv, entry, Dm, Fm, Rm);
+    } else {
+      if (nv == CHUNK) fin = chunk_masks<true>(laneaddr, v, nv, entry, Dm, Fm, Rm);
+      else fin = chunk_masks<false>(laneaddr, v, nv, entry, Dm, Fm, Rm);
+    }
     if (fin == INV_DEV && entry != INV_DEV && nv > 0) {
       const int p = first_inv_in_chunk(lut, a.in + cstart, nv, laneoff, entry);
       if (p >= 0) atomicMax(&a.ctrl->inv_neg, ~(a.base + cstart + (unsigned)p));
