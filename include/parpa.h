@@ -314,6 +314,12 @@ int parpa_parse_range(const parpa_dfa *dfa, const parpa_schema *schema, const ui
  * the GPU from those entry states.  Synchronous. */
 int parpa_debug_trace(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len,
                       uint8_t *d_chunk_states, uint8_t *d_kinds, uint8_t *d_states, void *stream);
+/* parpa_debug_masks — the emission masks exactly as pass 2 (k_pass2, the production kernel) stores them
+ * for the emission kernel: d_masks (device, ceil(len / parpa_tile_bytes()) * 96 uint64) in the layout
+ * [warp tile][DATA, DELIM, RECORD][lane], bit i of lane l's word = byte i of chunk (tile * 32 + l).
+ * Synchronous.  Errors: PARPA_EINVAL on null pointers. */
+int parpa_debug_masks(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint64_t *d_masks,
+                      void *stream);
 uint32_t parpa_chunk_bytes(void);
 uint32_t parpa_tile_bytes(void);   /* bytes per warp tile (the unit of the scans and of emission) */
 

@@ -325,6 +325,24 @@ def debug_trace(dfa: Dfa, data, per_byte=True, stream=None):
 
 
 # ---- range summaries (windows / multi-GPU) -------------------------------------------------
+def debug_masks(dfa: Dfa, data, stream=None):
+    """The production pass-2 masks (parpa_debug_masks) as a host uint64 array [chunks, 3] (DATA, DELIM,
+    RECORD; bit i = byte i of the chunk)."""
+    import numpy as np
+    import torch
+    L = _lib.load()
+    _check_input(data)
+    n = data.numel()
+    tb = L.parpa_tile_bytes()
+    nt = (n + tb - 1) // tb
+    m = torch.empty(max(nt * 96, 1), dtype=torch.int64, device=data.device)
+    _check(L.parpa_debug_masks(dfa.handle, ctypes.c_void_p(data.data_ptr()), n, ctypes.c_void_p(m.data_ptr()),
+                               _stream_handle(stream)), "parpa_debug_masks")
+    a = m.cpu().numpy().view(np.uint64)[:nt * 96].reshape(nt, 3, 32)
+    nch = (n + L.parpa_chunk_bytes() - 1) // L.parpa_chunk_bytes()
+    return a.transpose(0, 2, 1).reshape(nt * 32, 3)[:nch]
+
+
 def summarize(dfa: Dfa, data, stream=None):
     L = _lib.load()
     _check_input(data)

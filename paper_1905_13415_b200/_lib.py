@@ -55,7 +55,7 @@ EXPORTS = [
     "parpa_compose_counts", "parpa_parse_range", "parpa_range_begin", "parpa_range_count", "parpa_range_emit",
     "parpa_range_state_at", "parpa_range_emit_halo",
     "parpa_strings_size", "parpa_strings_copy", "parpa_infer_columns", "parpa_infer_types",
-    "parpa_debug_trace", "parpa_chunk_bytes", "parpa_tile_bytes",
+    "parpa_debug_trace", "parpa_debug_masks", "parpa_chunk_bytes", "parpa_tile_bytes",
     "parpa_set_profiling", "parpa_last_kernel_times", "parpa_status_string", "parpa_version",
     "parpa_last_error",
 ]
@@ -116,6 +116,7 @@ def load(build_if_missing: bool = True):
         lib.parpa_parse_range.argtypes = [P, ctypes.POINTER(Schema_t), P, u64, ctypes.POINTER(Context_t), P, u64,
                                           ctypes.c_int, ctypes.POINTER(Column_t), u64, P, P]
         lib.parpa_debug_trace.argtypes = [P, P, u64, P, P, P, P]
+        lib.parpa_debug_masks.argtypes = [P, P, u64, P, P]
         lib.parpa_chunk_bytes.restype = u32
         lib.parpa_tile_bytes.restype = u32
         lib.parpa_set_profiling.argtypes = [ctypes.c_int]

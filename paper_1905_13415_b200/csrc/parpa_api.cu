@@ -1409,6 +1409,19 @@ int parpa_strings_copy(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t le
 }
 
 // ---- debug ----------------------------------------------------------------------------------------
+int parpa_debug_masks(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint64_t *d_masks, void *stream) {
+  if (!dfa || (len && (!d_bytes || !d_masks))) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  parpa_plan p;
+  int rc = plan_scan(dfa, d_bytes, len, dfa->start, seg_identity(), 0, 1, s, &p);
+  if (!rc && p.w.ntiles &&
+      cudaMemcpyAsync(d_masks, p.w.masks, (size_t)p.w.ntiles * 96 * 8, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    rc = PARPA_ECUDA;
+  work_free(p.w, s);
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
+  return rc;
+}
+
 int parpa_debug_trace(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, uint8_t *d_chunk_states,
                       uint8_t *d_kinds, uint8_t *d_states, void *stream) {
   if (!dfa || (len && !d_bytes)) return PARPA_EINVAL;

@@ -554,3 +554,30 @@ def test_merged_states_exact_at_the_end():
         assert tau[0] == ro.final_state, (data[-8:], tau, ro.final_state)
         res = parpa.parse(dfa("csv"), parpa.Schema(types), dev(data))
         assert res.stats["final_state"] == ro.final_state, (data[-8:], res.stats)
+
+
+@pytest.mark.parametrize("name", ["bruteforce", "cfg1", "yelp", "clf"])
+def test_production_masks_equal_oracle_kinds(name):
+    """The DATA / DELIM / RECORD masks pass 2 stores for the emission kernel (not a debug re-simulation),
+    bit for bit against the oracle's per-byte emission kinds (DELIM = field or record
+    delimiter, RECORD ⊂ DELIM; invalid tail bits of the last chunk are zero)."""
+    if name == "bruteforce":
+        data = b"".join(b"".join(t) + b"\n" for n in range(7) for t in itertools.product(ALPH, repeat=n))
+        dialect = "csv"
+    else:
+        w = datagen.WORKLOADS[name]
+        data, _ = datagen.generate(name, 2_000_000)
+        data, dialect = bytes(data), w.dialect
+    ora = oracle.parse(dialect, data, 1, trace=True)
+    m = parpa.debug_masks(dfa(dialect), dev(data))
+    k = ora.trace_kind
+    n = len(data)
+    pad = (-n) % 64
+    kk = np.concatenate([k, np.full(pad, 1, np.uint8)]).reshape(-1, 64)      # pad as CTRL (no bits)
+    w64 = (1 << np.arange(64, dtype=np.uint64)).astype(np.uint64)
+    exp_d = ((kk == oracle.DATA).astype(np.uint64) * w64).sum(axis=1, dtype=np.uint64)
+    exp_f = ((kk >= oracle.FIELD).astype(np.uint64) * w64).sum(axis=1, dtype=np.uint64)
+    exp_r = ((kk == oracle.RECORD).astype(np.uint64) * w64).sum(axis=1, dtype=np.uint64)
+    assert np.array_equal(m[:, 0], exp_d)
+    assert np.array_equal(m[:, 1], exp_f)
+    assert np.array_equal(m[:, 2], exp_r)
