@@ -43,9 +43,13 @@ CONFIG_LABEL = {
     "taxi": "NYC-taxi-shaped CSV, 4.8 GB, 18 numeric/datetime columns, unquoted (BASELINE configs[1])",
     "clf": "Common-Log-Format-shaped logs, ~7.5 GB, 9-state DFA, '#' directive lines (BASELINE configs[3])",
     "cfg1": "1 MB RFC-4180 CSV, 8 columns, ~10% quoted fields (BASELINE configs[0])",
+    "taxi64": "64 GB taxi-shaped CSV sharded across the GPUs (strong scaling), in-device windows with "
+              "summary carry, cross-GPU transition-vector / count allgather and halo (BASELINE configs[4])",
 }
 RECORDS_PER_RANK = {"taxi": 48_900_000, "yelp": 6_670_000, "clf": 78_000_000, "cfg1": 10_000}
 BYTES_CAP = {"taxi": 4_800_000_000, "yelp": 4_823_000_000, "clf": 8_000_000_000, "cfg1": 1_000_000}
+TAXI64_RECORDS = 652_000_000          # ~64e9 bytes of taxi-shaped records (98.1 B each), seed 5
+TAXI64_WINDOW = int(os.environ.get("PARPA_BENCH_WINDOW", 8_000_000_000))   # bytes per in-device window
 SUB_CONFIGS = ["taxi", "clf", "cfg1"]
 
 
@@ -509,6 +513,198 @@ def run_config(args, config, ctx, main=True):
     return rec
 
 
+def run_taxi64(args, ctx):
+    """configs[4]: 64 GB of taxi-shaped CSV, strong scaling.  Rank g of N holds records [g R/N, (g+1) R/N)
+    of one logical file, cut mid-record between ranks (the cut bytes belong to the rank after).  Each
+    rank's range is parsed in in-device windows of TAXI64_WINDOW bytes with the summary carry (range
+    plans: every window's pass 1 -> its transition vector; composed -> the rank's vector -> allgather
+    across ranks -> entry state; every window counted from its entry -> the rank's counts -> allgather ->
+    prefix; every window emitted into the same column buffers, the bytes before it on the GPU as its left
+    context, the cross-rank halo for the first).  One step = the whole 64 GB."""
+    import numpy as np
+    import torch
+    import datagen
+    import paper_1905_13415_b200 as parpa
+    from paper_1905_13415_b200 import distributed as pdist
+    world, rank, dist, coll, gpu = ctx["world"], ctx["rank"], ctx["dist"], ctx["coll"], ctx["gpu"]
+    w = datagen.WORKLOADS["taxi64"]
+    dfa = parpa.Dfa.dialect(w.dialect)
+    schema = parpa.Schema(list(w.types))
+    R_all = args.records or TAXI64_RECORDS
+    r0, r1 = rank * R_all // world, (rank + 1) * R_all // world
+    per_rec = 98.2
+    cap = int((r1 - r0) * per_rec * 1.08) + (64 << 20)
+    t_gen = time.time()
+    host = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
+    g = datagen.fill(w, host.data_ptr(), cap, first_record=r0, max_records=r1 - r0)
+    assert g.records == r1 - r0, (g.records, r1 - r0)
+    cut = lambda k: 0 if k == 0 else 37 + 11 * k
+    ext = b""
+    if rank + 1 < world:
+        ext = b"".join(datagen.record(w, r1 + i) for i in range(4))[:cut(rank + 1)]
+    if ext:
+        host[g.nbytes:g.nbytes + len(ext)] = torch.frombuffer(bytearray(ext), dtype=torch.uint8)
+    c0 = cut(rank) if world > 1 else 0
+    n = g.nbytes + len(ext) - c0
+    d = torch.empty(n + 64, dtype=torch.uint8, device="cuda")[:n]
+    d.copy_(host[c0:c0 + n], non_blocking=True)
+    torch.cuda.synchronize()
+    del host
+    t_gen = time.time() - t_gen
+    base = 0
+    if world > 1:
+        blk = torch.tensor([g.nbytes], dtype=torch.int64, device=coll)
+        all_blk = [torch.zeros_like(blk) for _ in range(world)]
+        dist.all_gather(all_blk, blk)
+        base = sum(int(x.item()) for x in all_blk[:rank]) + c0
+    wins = [(lo, min(n, lo + TAXI64_WINDOW)) for lo in range(0, n, TAXI64_WINDOW)] or [(0, 0)]
+    cap_w = int(min(TAXI64_WINDOW, n) / 80) + 1024         # rows per window (taxi records are >= 80 bytes)
+    HALO_W = 1 << 20                                      # left context of windows after the first
+    cols = parpa.alloc_columns(schema, cap_w)
+    sts = [parpa.new_stats_tensor() for _ in wins]
+    dev = coll
+
+    def step(check=None):
+        plans = [parpa.RangePlan(dfa, d[lo:hi], base + lo) for lo, hi in wins]
+        try:
+            tau = list(range(dfa.num_states))
+            for p in plans:
+                tau = parpa.compose_tau(dfa, tau, p.tau)
+            if world > 1:
+                taus = [pdist.tau_from_bytes(b, dfa.num_states)
+                        for b in pdist._allgather_bytes(pdist.tau_to_bytes(tau), None, dev)]
+                e = pdist.entry_state(dfa, taus, rank)
+            else:
+                e = dfa.start
+            counts, ew = [], e
+            for p in plans:
+                counts.append(p.count(ew))
+                ew = p.tau[ew]
+            mine = pdist.prefix_counts(counts, len(counts))
+            if world > 1:
+                allc = [parpa._lib.Counts_t.from_buffer_copy(b)
+                        for b in pdist._allgather_bytes(bytes(mine), None, dev)]
+                prefix = pdist.prefix_counts(allc, rank)
+                import struct
+                bl = [struct.unpack("<QQ", b) for b in pdist._allgather_bytes(struct.pack("<QQ", base, n), None, dev)]
+                bases, lens_ = [x[0] for x in bl], [x[1] for x in bl]
+                of = [pdist.prefix_counts(allc, k).open_first for k in range(world)]
+                halo, hstate = pdist.halo_exchange(_HaloSrc(plans, wins, base), d, rank, bases,
+                                                   pdist.halo_plan(bases, lens_, of), None, dev)
+            else:
+                prefix, halo, hstate = parpa.identity_counts(), None, None
+            pw = prefix
+            for k, (p, (lo, hi)) in enumerate(zip(plans, wins)):
+                if k == 0:
+                    left, ls = halo, hstate
+                else:                                      # the 1 MB before the window, with its state
+                    left, ls = d[lo - HALO_W:lo], plans[k - 1].state_at(base + lo - HALO_W)
+                p.emit(schema, pw, cols, cap_w, sts[k], left=left, left_state=ls,
+                       is_last=(rank == world - 1 and k == len(wins) - 1))
+                if check is not None:
+                    check(k, sts[k], pw, parpa.compose_counts(pw, counts[k]))
+                pw = parpa.compose_counts(pw, counts[k])
+        finally:
+            for p in plans:
+                p.close()
+        return 7 * len(wins)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # verification (untimed): records and the int64 columns' sums / null counts against the generator
+    # (G1), summed over all ranks and windows.
+    T_int = [c for c, t in enumerate(w.types) if t == datagen.INT64]
+    acc = torch.zeros(2 + 2 * len(T_int), dtype=torch.int64, device="cuda")       # records, status, sums, nulls
+    last_w = len(wins) - 1
+
+    def check(k, st_t, pw, after):
+        s_ = parpa.stats_from_tensor(st_t)
+        acc[1] += int(s_["status"] != 0)
+        R = s_["records"]
+        acc[0] += R
+        for i, c in enumerate(T_int):
+            # a record straddling a window (or rank) boundary: its columns < pw.column sit one row past the
+            # previous window's count, the rest in this window's row 0
+            lo_row = 1 if c < pw.column else 0
+            hi_row = R + (1 if (not (k == last_w and rank == world - 1) and c < after.column) else 0)
+            if hi_row <= lo_row:
+                continue
+            v = cols[c].value[lo_row:hi_row]
+            ok = cols[c].valid[lo_row:hi_row].bool()
+            acc[2 + i] += torch.where(ok, v, torch.zeros_like(v)).sum()
+            acc[2 + len(T_int) + i] += (~ok).sum()
+    step(check)
+    truth = torch.tensor([g.records, 0] + [((x + (1 << 63)) % (1 << 64)) - (1 << 63) for x in g.int_sums]
+                         + list(g.int_nulls), dtype=torch.int64, device="cuda")
+    if dist:
+        a2, t2 = acc.to(coll), truth.to(coll)
+        dist.all_reduce(a2)
+        dist.all_reduce(t2)
+        acc, truth = a2, t2
+    ok_all = bool(torch.equal(acc.cpu(), truth.cpu()))
+    if not ok_all:
+        print("taxi64 ground truth mismatch: got", acc.tolist(), "expected", truth.tolist(), file=sys.stderr)
+    gt = {"records": int(acc[0].item()), "exp_records": int(truth[0].item()), "windows_failed": int(acc[1].item()),
+          "int_sums_and_nulls_equal": bool(torch.equal(acc[2:].cpu(), truth[2:].cpu()))}
+    clocks = Clocks()
+    clocks.start(gpu)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    launches = 0
+    for _ in range(args.steps):
+        launches += step()
+    e1.record()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    tot = float(n)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=coll)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        tb = torch.tensor([tot], dtype=torch.float64, device=coll)
+        dist.all_reduce(tb, op=dist.ReduceOp.SUM)
+        tot = float(tb[0].item())
+    value = tot / (ms * 1e-3) / 1e9
+    R_total = R_all
+    alg = tot + R_total * w.C * 12 + R_total * sum(1 for t in w.types if t != datagen.SPAN) * 9
+    peak, peak_src = load_peaks()
+    return {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": "taxi64", "description": CONFIG_LABEL["taxi64"], "total_bytes": int(tot),
+                       "records": R_total, "windows_per_rank": len(wins), "window_bytes": TAXI64_WINDOW,
+                       "path": "range plans per window: range_begin, compose, (allgather tau), range_count, "
+                               "(allgather counts, halo all_to_all), range_emit", "generate_s": round(t_gen, 1),
+                       "l2": "input >> 126 MB L2 (no flush needed)"},
+            "roofline": {"bound": "hbm", "achieved": round(alg / (ms * 1e-3) / 1e9, 1), "peak": peak * world,
+                         "unit": "GB/s", "frac": round(alg / (ms * 1e-3) / 1e9 / (peak * world), 4),
+                         "traffic": None, "kernel": "whole step (all windows, all ranks)",
+                         "algorithmic_bytes_per_launch": int(alg), "peak_source": peak_src + " x n_gpus"},
+            "parity": {"checked": "generator ground truth (G1) over all 64 GB: record count, per-int64-column "
+                                  "wrapping sums and null counts, status of every window", "ok": ok_all,
+                       **gt},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": launches, "clocks": clk}
+
+
+class _HaloSrc:
+    """state_at over a rank's windows (the owner of a halo start may be any window's plan)."""
+    def __init__(self, plans, wins, base):
+        self.plans, self.wins, self.base = plans, wins, base
+
+    def state_at(self, pos):
+        for p, (lo, hi) in zip(self.plans, self.wins):
+            if self.base + lo <= pos < self.base + hi:
+                return p.state_at(pos)
+        raise ValueError(pos)
+
+
 def relaunch(args):
     """--gpus N > 1 without torchrun: one process per GPU under torch.distributed.run."""
     s = socket.socket()
@@ -566,7 +762,7 @@ def main():
     ctx = {"world": world, "rank": rank, "dist": dist, "coll": coll, "gpu": gpu}
     main_cfg = args.config or "yelp"
     subs = [] if (args.config or world > 1 or args.no_subs or args.records) else SUB_CONFIGS
-    line = run_config(args, main_cfg, ctx, main=True)
+    line = run_taxi64(args, ctx) if main_cfg == "taxi64" else run_config(args, main_cfg, ctx, main=True)
     if subs:
         line["configs"] = [run_config(args, c, ctx, main=False) for c in subs]
     if rank == 0:
