@@ -157,6 +157,26 @@ __device__ __forceinline__ uint32_t lds_u1(uint32_t addr) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
+// LUT layouts.  PRMT layout (pass 1, k_small): 256-byte rows, the τ row of byte b at b * 256 (16 eight-byte
+// slots, or 32 four-byte slots with at most four device states) and its step row at b * 256 + 128; the
+// LUT sits at a 64 KB-aligned shared address so one PRMT forms the LDS address (b << 8 | slot).
+// DP4A layout (pass 2): the step rows alone, 128 bytes per byte value (32 KB); the address is one IDP4A
+// on the FMA pipe, dp4a(v, 128 << 8k, base + slot) — pass 2 is bound by the ALU pipe, which then keeps
+// only the step and gather instructions (pass 1 with one compose PRMT per byte measured faster with the
+// PRMT address).
+template <bool DP>
+__device__ __forceinline__ uint32_t lut_addr(uint32_t v, uint32_t k, uint32_t lbase) {
+  if (DP) return __dp4a(v, 128u << (8u * k), lbase);
+  return prmt(v, lbase, 0x5604u | (k << 4));
+}
+constexpr uint32_t STEP_ROW_DP = 128;
+__device__ __forceinline__ void build_lut_step_dp(uint8_t *lut, const DfaK &d) {    // DP4A layout
+  const bool ns4 = d.nlive <= 4;
+  for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
+    const int b = i >> 4, slot = i & 15;
+    *reinterpret_cast<uint2 *>(lut + b * STEP_ROW_DP + slot * 8) = make_uint2(d.lut[b][2], ns4 ? d.lut[b][2] : d.lut[b][3]);
+  }
+}
 __device__ __forceinline__ void build_lut(uint8_t *lut, const DfaK &d) {
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
     int b = i >> 5, half = (i >> 4) & 1, slot = i & 15;
@@ -199,7 +219,7 @@ __device__ __forceinline__ uint32_t gather4(uint32_t x, uint32_t bitmask, uint32
 
 // NS4 (at most four device states): the step row fits one word (per-lane 4-byte slots, see build_lut)
 // and the step is PRMT(row, row, x) — an INV selector replicates the sign of byte 3.
-template <bool FULL, bool NS4 = false>
+template <bool FULL, bool NS4 = false, bool DP = false>
 __device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_t (&v)[16], int nvalid, uint32_t entry,
                                                 unsigned long long &Dm, unsigned long long &Fm,
                                                 unsigned long long &Rm) {
@@ -212,12 +232,12 @@ __device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_
     for (int k = 0; k < 4; k++) {
       int i = 4 * w + k;
       if (FULL || i < nvalid) {
-        const uint32_t ad = prmt(v[w], laneaddr, 0x5604u | ((uint32_t)k << 4));
+        const uint32_t ad = lut_addr<DP>(v[w], (uint32_t)k, laneaddr) + (DP ? 0u : 128u);
         if (NS4) {
-          const uint32_t st = lds_u1(ad + 128u);
+          const uint32_t st = lds_u1(ad);
           x = prmt(st, st, x);
         } else {
-          const uint2 st = lds_u2<128>(ad);
+          const uint2 st = lds_u2<0>(ad);
           x = prmt(st.x, st.y, x);
         }
         xs[k] = x;
@@ -255,7 +275,7 @@ __device__ __forceinline__ void chunk_tau4(uint32_t laneaddr, const uint32_t (&v
     for (int q = 0; q < 4; q++) {
       const int b = 16 * q + i;
       if (!FULL && b >= nvalid) continue;
-      const uint32_t ad = prmt(v[b >> 2], laneaddr, 0x5604u | ((uint32_t)(b & 3) << 4));
+      const uint32_t ad = lut_addr<false>(v[b >> 2], (uint32_t)(b & 3), laneaddr);
       if (NS4) {
         a0[q] = prmt(a0[q], a0[q], lds_u1(ad));
       } else {
@@ -280,12 +300,13 @@ __device__ __forceinline__ void chunk_tau4(uint32_t laneaddr, const uint32_t (&v
 }
 
 // scalar re-walk (rare): position of the first byte whose transition enters INV
+// (step rows at lut + b * row + laneoff: row = 256 with lut at the step half, or STEP_ROW_DP)
 __device__ int first_inv_in_chunk(const uint8_t *lut, const uint8_t *p, int nvalid, uint32_t laneoff,
-                                  uint32_t entry) {
+                                  uint32_t entry, uint32_t row = 256) {
   uint32_t x = 0x80u | entry;
   for (int i = 0; i < nvalid; i++) {
     uint32_t b = p[i];
-    uint2 st = *reinterpret_cast<const uint2 *>(lut + (b << 8) + laneoff + 128);
+    uint2 st = *reinterpret_cast<const uint2 *>(lut + b * row + laneoff);
     x = prmt(st.x, st.y, x);
     if ((x & 0xFu) == INV_DEV) return i;
   }

@@ -43,7 +43,7 @@ __device__ __forceinline__ PassSmem pass_smem(uint8_t *smem, int warp, int lane)
   p.lut = smem + lut_off;
   p.bufs = reinterpret_cast<uint4 *>(smem + boff);
   p.laneoff = (uint32_t)(lane & 15) * 8u;
-  p.laneaddr = p.laneoff | (((sb + lut_off) >> 16) << 16);
+  p.laneaddr = p.laneoff | (((sb + lut_off) >> 16) << 16);   // PRMT layout (pass 1)
   return p;
 }
 constexpr int SCAN_THREADS = 256, SCAN_ITEMS = 8;
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass1(const KArgs a, con
     uint32_t v[16], t0, t1, qt[3];
     read_chunk(bufs + i * (WT / 16), lane, v);
     if (dfa.nlive <= 4) {                                   // warp-uniform (kernel parameter)
-      const uint32_t la4 = (ps.laneaddr & ~0xFFu) | ((uint32_t)lane * 4u);   // one 4-byte slot per lane
+      const uint32_t la4 = ps.laneaddr - ps.laneoff + (uint32_t)lane * 4u;   // one 4-byte slot per lane
       if (nv == CHUNK) chunk_tau4<true, true>(la4, v, nv, t0, t1, qt);
       else chunk_tau4<false, true>(la4, v, nv, t0, t1, qt);
     } else {
@@ -231,7 +231,8 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, con
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const PassSmem ps = pass_smem(smem, warp, lane);
   PdlTrigger pdl_trigger;
-  build_lut(ps.lut, dfa);
+  build_lut_step_dp(ps.lut, dfa);                          // DP4A layout: step rows only
+  const uint32_t lbase = smem_u32(ps.lut) + ps.laneoff;
   __syncthreads();
   pdl_wait();
   uint4 *bufs = ps.bufs;
@@ -252,15 +253,15 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, con
     unsigned long long Dm, Fm, Rm;
     uint32_t fin;
     if (dfa.nlive <= 4) {
-      const uint32_t la4 = (ps.laneaddr & ~0xFFu) | ((uint32_t)lane * 4u);   // one 4-byte slot per lane
-      if (nv == CHUNK) fin = chunk_masks<true, true>(la4, v, nv, entry, Dm, Fm, Rm);
-      else fin = chunk_masks<false, true>(la4, v, nv, entry, Dm, Fm, Rm);
+      const uint32_t la4 = lbase - ps.laneoff + (uint32_t)lane * 4u;   // one 4-byte slot per lane
+      if (nv == CHUNK) fin = chunk_masks<true, true, true>(la4, v, nv, entry, Dm, Fm, Rm);
+      else fin = chunk_masks<false, true, true>(la4, v, nv, entry, Dm, Fm, Rm);
     } else {
-      if (nv == CHUNK) fin = chunk_masks<true>(ps.laneaddr, v, nv, entry, Dm, Fm, Rm);
-      else fin = chunk_masks<false>(ps.laneaddr, v, nv, entry, Dm, Fm, Rm);
+      if (nv == CHUNK) fin = chunk_masks<true, false, true>(lbase, v, nv, entry, Dm, Fm, Rm);
+      else fin = chunk_masks<false, false, true>(lbase, v, nv, entry, Dm, Fm, Rm);
     }
     if (fin == INV_DEV && entry != INV_DEV && nv > 0) {
-      int p = first_inv_in_chunk(ps.lut, a.in + cstart, nv, ps.laneoff, entry);
+      int p = first_inv_in_chunk(ps.lut, a.in + cstart, nv, ps.laneoff, entry, STEP_ROW_DP);
       if (p >= 0) atomicMax(&a.ctrl->inv_neg, ~(a.base + cstart + (unsigned)p));
     }
     unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;   // for k_emit

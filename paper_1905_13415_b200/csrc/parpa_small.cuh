@@ -42,7 +42,7 @@ __device__ __forceinline__ void small_smem(uint8_t *smem, int warp, int lane, ui
   ws = reinterpret_cast<WarpScratch *>(base + slot((uint32_t)warp));
   spare = base + slot(SMALL_WARPS);                     // one more slot: the scan arrays (<= 4 KB)
   laneoff = (uint32_t)(lane & 15) * 8u;
-  laneaddr = laneoff | (((sb + lut_off) >> 16) << 16);
+  laneaddr = laneoff | (((sb + lut_off) >> 16) << 16);       // PRMT layout
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 1) k_small(const __grid_cons
     uint32_t v[16], t0, t1, qt[3];
     load_chunk(a.in + cstart, nv, v);
     if (dfa.nlive <= 4) {
-      const uint32_t la4 = (laneaddr & ~0xFFu) | ((uint32_t)lane * 4u);   // one 4-byte slot per lane
+      const uint32_t la4 = laneaddr - laneoff + (uint32_t)lane * 4u;   // one 4-byte slot per lane
       if (nv == CHUNK) chunk_tau4<true, true>(la4, v, nv, t0, t1, qt);
       else chunk_tau4<false, true>(la4, v, nv, t0, t1, qt);
     } else {
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 1) k_small(const __grid_cons
     unsigned long long Dm, Fm, Rm;
     uint32_t fin;
     if (dfa.nlive <= 4) {
-      const uint32_t la4 = (laneaddr & ~0xFFu) | ((uint32_t)lane * 4u);   // one 4-byte slot per lane
+      const uint32_t la4 = laneaddr - laneoff + (uint32_t)lane * 4u;   // one 4-byte slot per lane
       if (nv == CHUNK) fin = chunk_masks<true, true>(la4, v, nv, entry, Dm, Fm, Rm);
       else fin = chunk_masks<false, true>(la4, v, nv, entry, Dm, Fm, Rm);
     } else {
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 1) k_small(const __grid_cons
       else fin = chunk_masks<false>(laneaddr, v, nv, entry, Dm, Fm, Rm);
     }
     if (fin == INV_DEV && entry != INV_DEV && nv > 0) {
-      const int p = first_inv_in_chunk(lut, a.in + cstart, nv, laneoff, entry);
+      const int p = first_inv_in_chunk(lut + 128, a.in + cstart, nv, laneoff, entry);
       if (p >= 0) atomicMax(&a.ctrl->inv_neg, ~(a.base + cstart + (unsigned)p));
     }
     unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;
