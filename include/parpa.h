@@ -302,6 +302,30 @@ int parpa_range_emit_halo(parpa_plan *plan, const parpa_schema *schema, const pa
                           const parpa_column *columns, uint64_t capacity, parpa_stats *d_stats,
                           void *stream);
 
+/* ---- skipping records ("PARPA is able to ignore a user-specified set of records and
+ * columns") ------------------------------------------------------------------------- *
+ * parpa_parse_into_skip — parpa_parse_into that does not write the records whose indices (0-based,
+ * over the whole input) are listed in d_skip_records (device uint64[nskip], sorted ascending, unique):
+ * record r is written to row r - (number of skipped records before r), stats->records counts the
+ * records written.  Columns are skipped by passing NULL pointers (see parpa_column).  Skipped records
+ * take no part in the missing-field count; their extra fields are still counted.  Errors as
+ * parpa_parse_into; PARPA_EINVAL if nskip > 0 and d_skip_records is NULL. */
+int parpa_parse_into_skip(const parpa_dfa *dfa, const parpa_schema *schema, const uint8_t *d_bytes,
+                          uint64_t len, const uint64_t *d_skip_records, uint64_t nskip,
+                          const parpa_column *columns, uint64_t capacity, parpa_stats *d_stats,
+                          void *stream, uint32_t *gpu_launches);
+
+/* parpa_compact_rows — skipping rows ("rows are different from records, as some records may span
+ * multiple rows ... PARPA ignores a set of rows by performing an initial parallel pass over the input,
+ * pruning symbols of ignored rows (i.e., parallel stream compaction)").  A row is a raw line:
+ * the bytes up to and including a '\n' (quoting is not considered), rows numbered from 0.  Copies the
+ * bytes of every row not listed in d_skip_rows (device uint64[nskip], sorted ascending, unique) from
+ * d_in (device, len bytes) to d_out (device, >= len bytes) in order and sets *out_len (host) to their
+ * count; parse d_out afterwards (offsets then refer to the compacted bytes).  Synchronous.  Errors:
+ * PARPA_EINVAL on null pointers, PARPA_ENOMEM, PARPA_ECUDA. */
+int parpa_compact_rows(const uint8_t *d_in, uint64_t len, const uint64_t *d_skip_rows, uint64_t nskip,
+                       uint8_t *d_out, uint64_t *out_len, void *stream);
+
 int parpa_parse_range(const parpa_dfa *dfa, const parpa_schema *schema, const uint8_t *d_bytes,
                       uint64_t len, const parpa_context *ctx, const uint8_t *left_context,
                       uint64_t left_len, int is_last, const parpa_column *columns,

@@ -222,14 +222,22 @@ def parse(dfa: Dfa, schema: Schema, data, stream=None) -> ParseResult:
     return ParseResult(cols, stats)
 
 
-def parse_into(dfa: Dfa, schema: Schema, data, columns, capacity: int, stats_tensor, stream=None) -> int:
+def parse_into(dfa: Dfa, schema: Schema, data, columns, capacity: int, stats_tensor, stream=None,
+               skip_records=None) -> int:
     """Parse into caller columns without a host round trip (parpa_parse_into).  Asynchronous; returns the
-    number of kernels launched."""
+    number of kernels launched.  skip_records: a sorted device int64 tensor of record indices not to write
+    (parpa_parse_into_skip)."""
     L = _lib.load()
     _check_input(data)
     sch = schema.struct()
     arr = _col_array(columns)
     n = ctypes.c_uint32(0)
+    if skip_records is not None and skip_records.numel():
+        _check(L.parpa_parse_into_skip(dfa.handle, ctypes.byref(sch), ctypes.c_void_p(data.data_ptr()), data.numel(),
+                                       ctypes.c_void_p(skip_records.data_ptr()), skip_records.numel(), arr,
+                                       int(capacity), ctypes.c_void_p(stats_tensor.data_ptr()),
+                                       _stream_handle(stream), ctypes.byref(n)), "parpa_parse_into_skip")
+        return n.value
     _check(L.parpa_parse_into(dfa.handle, ctypes.byref(sch), ctypes.c_void_p(data.data_ptr()), data.numel(), arr,
                               int(capacity), ctypes.c_void_p(stats_tensor.data_ptr()), _stream_handle(stream),
                               ctypes.byref(n)), "parpa_parse_into")
@@ -325,6 +333,22 @@ def debug_trace(dfa: Dfa, data, per_byte=True, stream=None):
 
 
 # ---- range summaries (windows / multi-GPU) -------------------------------------------------
+def compact_rows(data, skip_rows, stream=None):
+    """parpa_compact_rows: the input without the raw lines whose indices are in ``skip_rows`` (sorted device
+    int64 tensor).  Returns a new device uint8 tensor."""
+    import torch
+    L = _lib.load()
+    _check_input(data)
+    out = torch.empty(max(data.numel(), 1) + 16, dtype=torch.uint8, device=data.device)
+    n = ctypes.c_uint64(0)
+    sk = skip_rows if skip_rows is not None else torch.empty(0, dtype=torch.int64, device=data.device)
+    _check(L.parpa_compact_rows(ctypes.c_void_p(data.data_ptr()), data.numel(),
+                                ctypes.c_void_p(sk.data_ptr()) if sk.numel() else None, sk.numel(),
+                                ctypes.c_void_p(out.data_ptr()), ctypes.byref(n), _stream_handle(stream)),
+           "parpa_compact_rows")
+    return out[:n.value]
+
+
 def debug_masks(dfa: Dfa, data, stream=None):
     """The production pass-2 masks (parpa_debug_masks) as a host uint64 array [chunks, 3] (DATA, DELIM,
     RECORD; bit i = byte i of the chunk)."""

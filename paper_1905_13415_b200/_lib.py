@@ -53,7 +53,8 @@ EXPORTS = [
     "parpa_result_copy_column", "parpa_result_free", "parpa_plan_create", "parpa_plan_records", "parpa_plan_emit", "parpa_plan_destroy",
     "parpa_parse_into", "parpa_parse_host", "parpa_summarize", "parpa_count", "parpa_compose_tau",
     "parpa_compose_counts", "parpa_parse_range", "parpa_range_begin", "parpa_range_count", "parpa_range_emit",
-    "parpa_range_state_at", "parpa_range_emit_halo",
+    "parpa_range_state_at", "parpa_range_emit_halo", "parpa_parse_into_skip",
+    "parpa_compact_rows",
     "parpa_strings_size", "parpa_strings_copy", "parpa_infer_columns", "parpa_infer_types",
     "parpa_debug_trace", "parpa_debug_masks", "parpa_chunk_bytes", "parpa_tile_bytes",
     "parpa_set_profiling", "parpa_last_kernel_times", "parpa_status_string", "parpa_version",
@@ -111,6 +112,9 @@ def load(build_if_missing: bool = True):
         lib.parpa_range_emit.argtypes = [P, ctypes.POINTER(Schema_t), ctypes.POINTER(Context_t), P, u64,
                                          ctypes.c_int, ctypes.POINTER(Column_t), u64, P, P]
         lib.parpa_range_state_at.argtypes = [P, u64, ctypes.POINTER(u32)]
+        lib.parpa_compact_rows.argtypes = [P, u64, P, u64, P, ctypes.POINTER(u64), P]
+        lib.parpa_parse_into_skip.argtypes = [P, ctypes.POINTER(Schema_t), P, u64, P, u64, ctypes.POINTER(Column_t),
+                                              u64, P, P, ctypes.POINTER(u32)]
         lib.parpa_range_emit_halo.argtypes = [P, ctypes.POINTER(Schema_t), ctypes.POINTER(Context_t), P, u64, u32,
                                               ctypes.c_int, ctypes.POINTER(Column_t), u64, P, P]
         lib.parpa_parse_range.argtypes = [P, ctypes.POINTER(Schema_t), P, u64, ctypes.POINTER(Context_t), P, u64,

@@ -818,7 +818,8 @@ void parpa_result_free(parpa_result *r) {
 static int parse_into_impl(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_bytes, uint64_t len,
                            const parpa_column *cols, uint64_t cap, parpa_stats *d_stats, cudaStream_t s,
                            uint32_t seed_state, const Seg &seed, uint64_t base, const uint8_t *left,
-                           uint64_t left_len, int is_last, uint32_t *launches) {
+                           uint64_t left_len, int is_last, uint32_t *launches,
+                           const uint64_t *d_skip = nullptr, uint64_t nskip = 0) {
   if (!dfa || !sch || !d_stats || (len && !d_bytes) || (sch->num_columns && !cols)) return PARPA_EINVAL;
   ColsK ck;
   int rc = set_columns(sch, cols, sch->num_columns, ck);
@@ -844,6 +845,8 @@ static int parse_into_impl(const parpa_dfa *dfa, const parpa_schema *sch, const 
     a.left = left;
     a.left_len = left_len;
     a.is_last = is_last;
+    a.skip = (const unsigned long long *)d_skip;
+    a.nskip = d_skip ? nskip : 0;
     uint32_t n = 0;
     if (use_small(a)) {
       rc = launch_small(a, dfa->k, ck, s, &n);
@@ -865,6 +868,14 @@ int parpa_parse_into(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_
   if (!dfa) return PARPA_EINVAL;
   return parse_into_impl(dfa, sch, d_bytes, len, cols, cap, d_stats, (cudaStream_t)stream,
                          dfa->start, seg_identity(), 0, nullptr, 0, 1, gpu_launches);
+}
+
+int parpa_parse_into_skip(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_bytes, uint64_t len,
+                          const uint64_t *d_skip_records, uint64_t nskip, const parpa_column *cols, uint64_t cap,
+                          parpa_stats *d_stats, void *stream, uint32_t *gpu_launches) {
+  if (!dfa || (nskip && !d_skip_records)) return PARPA_EINVAL;
+  return parse_into_impl(dfa, sch, d_bytes, len, cols, cap, d_stats, (cudaStream_t)stream,
+                         dfa->start, seg_identity(), 0, nullptr, 0, 1, gpu_launches, d_skip_records, nskip);
 }
 
 int parpa_parse_range(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_bytes, uint64_t len,
@@ -1406,6 +1417,50 @@ int parpa_strings_copy(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t le
     return PARPA_EINVAL;
   return strings_impl(dfa, d_bytes, len, column, rows, const_cast<int64_t *>(d_offsets), nullptr, d_data,
                       (cudaStream_t)stream);
+}
+
+// ---- skipping rows (stream compaction) ---------------------------------------------------
+int parpa_compact_rows(const uint8_t *d_in, uint64_t len, const uint64_t *d_skip_rows, uint64_t nskip, uint8_t *d_out,
+                       uint64_t *out_len, void *stream) {
+  if ((len && (!d_in || !d_out)) || !out_len || (nskip && !d_skip_rows)) return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (len == 0) { *out_len = 0; return PARPA_OK; }
+  DevCfg *dc;
+  int rc = dev_cfg(&dc);
+  if (rc) return rc;
+  const uint64_t nt64 = (len + WT - 1) / WT;
+  if (nt64 > 0x07FFFFFFull) return PARPA_EUNSUPPORTED;
+  const uint32_t nt = (uint32_t)nt64;
+  const uint64_t nb = (nt + SCAN_TILE - 1) / SCAN_TILE;
+  // [lines / first row per tile : nt + 1][kept / output offset per tile : nt + 1][scan scratch]
+  const size_t o_lines = 0, o_kept = align_up((nt + 1) * 8), o_scan = o_kept + align_up((nt + 1) * 8);
+  const size_t o_agg = (16 + nb * 4 + 15) / 16 * 16, scan_bytes = o_agg + 2 * nb * 8;
+  void *blk = nullptr;
+  CK(cudaMallocAsync(&blk, o_scan + 2 * scan_bytes, s));
+  uint8_t *b = (uint8_t *)blk;
+  unsigned long long *lines = (unsigned long long *)(b + o_lines), *kept = (unsigned long long *)(b + o_kept);
+  uint8_t *sc0 = b + o_scan, *sc1 = b + o_scan + scan_bytes;
+  if (!rc && cudaMemsetAsync(sc0, 0, 2 * scan_bytes, s) != cudaSuccess) rc = PARPA_ECUDA;
+  const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)dc->sms * 8, (nt + 7) / 8);
+  const unsigned long long *skip = (const unsigned long long *)d_skip_rows;
+  if (!rc) {
+    k_rows_count<<<grid, 256, 0, s>>>(d_in, len, nt, lines);
+    k_scan_u64<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(lines, nt, (unsigned int *)sc0, (uint32_t *)(sc0 + 16),
+                                                      (unsigned long long *)(sc0 + o_agg),
+                                                      (unsigned long long *)(sc0 + o_agg + nb * 8));
+    k_rows_keep<false><<<grid, 256, 0, s>>>(d_in, len, nt, lines, skip, nskip, kept, nullptr, nullptr);
+    k_scan_u64<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(kept, nt, (unsigned int *)sc1, (uint32_t *)(sc1 + 16),
+                                                      (unsigned long long *)(sc1 + o_agg),
+                                                      (unsigned long long *)(sc1 + o_agg + nb * 8));
+    k_rows_keep<true><<<grid, 256, 0, s>>>(d_in, len, nt, lines, skip, nskip, nullptr, kept, d_out);
+    if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
+  }
+  unsigned long long total = 0;
+  if (!rc && cudaMemcpyAsync(&total, kept + nt, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = PARPA_ECUDA;
+  cudaFreeAsync(blk, s);
+  if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
+  if (!rc) *out_len = total;
+  return rc;
 }
 
 // ---- debug ----------------------------------------------------------------------------------------

@@ -114,6 +114,8 @@ struct KArgs {
   const uint8_t *left;               // bytes preceding the range (multi-GPU halo), may be null
   unsigned long long left_len;
   uint32_t left_state;               // device state before left[0] (the halo's entry state), 0xFF unknown
+  const unsigned long long *skip;    // sorted record indices not to write (skip records), may be null
+  unsigned long long nskip;
   uint32_t pad_ls;
   uint32_t ntiles, seed_dev, is_last, C;
   uint32_t seed_exact, pad_se;       // the DFA state seed_dev stands for (exact; for an empty range's EOI)
@@ -492,12 +494,29 @@ __device__ __forceinline__ void push_defer(const KArgs &a, const ColDesc *cd, un
   }
 }
 
+// Output row of record r: r - row_base, minus the skipped records before it; NONE for a skipped record
+// (every writer tests row < cap, so a skipped record is simply not written).
+__device__ __forceinline__ unsigned long long skipped_before(const KArgs &a, unsigned long long r) {
+  unsigned long long lo = 0, hi = a.nskip;
+  while (lo < hi) {
+    const unsigned long long mid = (lo + hi) >> 1;
+    if (a.skip[mid] < r) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ unsigned long long out_row(const KArgs &a, unsigned long long r) {
+  if (a.nskip == 0) return r - a.row_base;
+  const unsigned long long k = skipped_before(a, r);
+  if (k < a.nskip && a.skip[k] == r) return NONE;
+  return r - k - a.row_base;
+}
+
 template <bool TS>
 __device__ void emit_field(const KArgs &a, const ColDesc *cols, unsigned long long r, uint32_t c, unsigned long long fd,
                            unsigned long long ld, uint32_t fl, unsigned long long dpos, EmitCounters &cnt) {
   if (c >= a.C) { cnt.extra++; return; }
-  unsigned long long row = r - a.row_base;
-  if (row >= a.cap) return;                         // capacity exceeded: reported by k_finalize
+  unsigned long long row = out_row(a, r);
+  if (row >= a.cap) return;                         // capacity exceeded (reported by k_finalize) or skipped
   const ColDesc *cd = cols + c;
   if (cd->type == T_SKIP) return;
   unsigned long long off;
@@ -536,8 +555,9 @@ __device__ void emit_field(const KArgs &a, const ColDesc *cols, unsigned long lo
 __device__ void fill_missing(const KArgs &a, const ColDesc *cols, unsigned long long r, uint32_t from, unsigned long long dpos,
                              EmitCounters &cnt) {
   if (from >= a.C) return;
+  unsigned long long row = out_row(a, r);
+  if (row == NONE) return;                          // a skipped record
   cnt.missing++;
-  unsigned long long row = r - a.row_base;
   if (row >= a.cap) return;
   for (uint32_t k = from; k < a.C; k++) {
     const ColDesc *cd = cols + k;
@@ -1010,7 +1030,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
         end = closed ? (rw & 0xFFFFu) : nf;
         dpos = rw >> 16;
         cs = ji == 0 ? c0 : 0u;
-        row = r0 + ji - a.row_base;
+        row = out_row(a, r0 + ji);
         live = row < a.cap;
       }
       if ((NP == 1 || part == 0) && live && closed && end - start + cs < a.C) cnt.missing++;   // short record
@@ -1088,7 +1108,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     const uint32_t end = ji < nrec ? (ws->rows[ji] & 0xFFFFu) : nf;
     const uint32_t cs = ji == 0 ? c0 : 0u;
     if (ci < cs) continue;                                  // written by an earlier tile
-    const unsigned long long row = r0 + ji - a.row_base;
+    const unsigned long long row = out_row(a, r0 + ji);
     if (row >= a.cap) continue;
     const uint32_t k = start + (ci - cs);
     const ColDesc *cd = cols + ci;
@@ -1240,13 +1260,14 @@ __device__ void finalize_one(const KArgs &a, const DfaK &dfa, const ColsK &colsk
   unsigned long long missing = a.ctrl->n_missing + cnt.missing;
   unsigned long long extra = a.ctrl->n_extra + cnt.extra;
   unsigned int n_defer = a.ctrl->n_defer;
+  const unsigned long long nskipped = a.nskip ? skipped_before(a, R) : 0ull;   // skipped records < R
   int status = ST_OK;
   if (first_inv != NONE) status = ST_EFORMAT;
   else if (a.ctrl->unsupported || cnt.unsupported) status = ST_EUNSUPPORTED;
-  else if (R - a.row_base > a.cap) status = ST_ENEEDMORE;
+  else if (R - a.row_base - nskipped > a.cap) status = ST_ENEEDMORE;
   else if ((missing || extra) && a.strict) status = ST_ECOLUMNS;
   if (a.stats) {
-    a.stats->records = R - a.row_base;
+    a.stats->records = R - a.row_base - nskipped;
     a.stats->fields = nf - a.seed.nflds;
     a.stats->first_invalid = first_inv;
     a.stats->missing_records = missing;

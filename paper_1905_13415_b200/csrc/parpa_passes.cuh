@@ -652,3 +652,86 @@ __global__ void k_field_class(const KArgs a, const unsigned long long *off, cons
   if ((threadIdx.x & 31) == 0 && m) atomicOr(mask, m);
 }
 }  // namespace parpa
+
+// ---- skipping rows ("ignores a set of rows by performing an initial parallel
+// pass over the input, pruning symbols of ignored rows (i.e., parallel stream compaction)") ----------
+// A row is a raw line: the bytes up to and including a '\n' (rows ignore quoting: "some records may span
+// multiple rows").  Per warp tile (32 lanes x 64 bytes): k_rows_count counts '\n'; a scan gives each
+// tile its first row; k_rows_keep counts the bytes of rows not in the sorted skip list; a scan gives each
+// tile its output offset; k_rows_write compacts them.  Both passes walk the skip list with a pointer
+// that only moves forward (rows increase along a chunk).
+namespace parpa {
+
+__device__ __forceinline__ uint32_t nl_count_word(uint32_t w) {        // bytes equal to '\n' in a word
+  const uint32_t t = w ^ 0x0A0A0A0Au;
+  return (uint32_t)__popc(~(((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t) & 0x80808080u);
+}
+__global__ void k_rows_count(const uint8_t *in, unsigned long long len, uint32_t ntiles, unsigned long long *lines) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += (gridDim.x * blockDim.x) >> 5) {
+    const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
+    const int nv = cstart >= len ? 0 : (int)min((unsigned long long)CHUNK, len - cstart);
+    uint32_t v[16];
+    load_chunk(in + cstart, nv, v);
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < 16; k++) c += nl_count_word(v[k]);     // zero-filled tails count nothing
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) lines[t] = c;
+  }
+}
+// WRITE = false: kept bytes per tile into kept[t]; WRITE = true: the kept bytes to out[obase[t] + ...]
+template <bool WRITE>
+__global__ void k_rows_keep(const uint8_t *in, unsigned long long len, uint32_t ntiles, const unsigned long long *lbase,
+                            const unsigned long long *skip, unsigned long long nskip, unsigned long long *kept,
+                            const unsigned long long *obase, uint8_t *out) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntiles; t += (gridDim.x * blockDim.x) >> 5) {
+    const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
+    const int nv = cstart >= len ? 0 : (int)min((unsigned long long)CHUNK, len - cstart);
+    uint32_t v[16];
+    load_chunk(in + cstart, nv, v);
+    uint32_t nl = 0;
+#pragma unroll
+    for (int k = 0; k < 16; k++) nl += nl_count_word(v[k]);
+    uint32_t inc = nl;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += o;
+    }
+    unsigned long long row = lbase[t] + (inc - nl);           // row of the chunk's first byte
+    unsigned long long lo = 0, hi = nskip;                     // first skip entry >= row
+    while (lo < hi) {
+      const unsigned long long mid = (lo + hi) >> 1;
+      if (skip[mid] < row) lo = mid + 1; else hi = mid;
+    }
+    bool drop = lo < nskip && skip[lo] == row;
+    uint32_t keepmask[2] = {0u, 0u};
+    for (int i = 0; i < nv; i++) {
+      const uint32_t b = (v[i >> 2] >> (8 * (i & 3))) & 0xFFu;
+      if (!drop) keepmask[i >> 5] |= 1u << (i & 31);
+      if (b == 0x0Au) {                                        // the next byte starts the next row
+        row++;
+        while (lo < nskip && skip[lo] < row) lo++;
+        drop = lo < nskip && skip[lo] == row;
+      }
+    }
+    const uint32_t mine = (uint32_t)(__popc(keepmask[0]) + __popc(keepmask[1]));
+    uint32_t kinc = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, kinc, d);
+      if (lane >= d) kinc += o;
+    }
+    if (!WRITE) {
+      if (lane == 31) kept[t] = kinc;
+    } else {
+      unsigned long long o = obase[t] + (kinc - mine);
+      for (int i = 0; i < nv; i++)
+        if ((keepmask[i >> 5] >> (i & 31)) & 1u) out[o++] = (uint8_t)((v[i >> 2] >> (8 * (i & 3))) & 0xFFu);
+    }
+  }
+}
+
+}  // namespace parpa

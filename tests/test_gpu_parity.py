@@ -581,3 +581,52 @@ def test_production_masks_equal_oracle_kinds(name):
     assert np.array_equal(m[:, 0], exp_d)
     assert np.array_equal(m[:, 1], exp_f)
     assert np.array_equal(m[:, 2], exp_r)
+
+
+@pytest.mark.parametrize("name,nbytes", [("cfg1", 600_000), ("taxi", 3_000_000), ("yelp", 3_000_000)])
+def test_skip_records(name, nbytes):
+    """Skipping a user-specified set of records: the records listed (the first, a run, random
+    ones, the last) are not written; every other record lands in the next row, bit-exact vs the oracle's
+    parse with those rows removed.  (cfg1 at 600 KB runs the one-launch k_small path, the others the
+    multi-kernel path.)"""
+    import torch
+    w = datagen.WORKLOADS[name]
+    data, g = datagen.generate(name, nbytes)
+    ora = oracle.parse(w.dialect, data, w.C, list(w.types))
+    rng = random.Random(7)
+    R = ora.R
+    skip = sorted(set([0, 1, 2, R - 1] + list(range(R // 2, R // 2 + 40)) + rng.sample(range(R), R // 10)))
+    keep = np.setdiff1d(np.arange(R), np.array(skip))
+    schema = parpa.Schema(list(w.types))
+    cols = parpa.alloc_columns(schema, R)
+    st = parpa.new_stats_tensor()
+    sk = torch.tensor(skip, dtype=torch.int64, device="cuda")
+    parpa.parse_into(dfa(w.dialect), schema, dev(data), cols, R, st, skip_records=sk)
+    s = parpa.stats_from_tensor(st)
+    assert s["status"] == 0 and s["records"] == len(keep), s
+    n = len(keep)
+    for c, t in enumerate(w.types):
+        assert np.array_equal(to_np(cols[c].offset).view(np.uint64)[:n], ora.offset[c][keep]), c
+        assert np.array_equal(to_np(cols[c].length).view(np.uint32)[:n], ora.length[c][keep]), c
+        if t != oracle.SPAN:
+            assert np.array_equal(to_np(cols[c].valid)[:n], ora.valid[c][keep]), c
+            assert np.array_equal(to_np(cols[c].value).view(np.int64)[:n], ora.value[c][keep]), c
+
+
+@pytest.mark.parametrize("name,nbytes", [("cfg1", 400_000), ("yelp", 3_000_000)])
+def test_skip_rows_compaction(name, nbytes):
+    """Skipping rows: raw lines (quoting ignored — yelp records span several rows) removed by
+    the device stream compaction equal the plain definition (split after every '\\n', drop the listed
+    indices, concatenate); the compacted input then parses exactly like the oracle's parse of it."""
+    import torch
+    w = datagen.WORKLOADS[name]
+    data, _ = datagen.generate(name, nbytes)
+    data = bytes(data) + b"tail without newline"
+    lines = data.splitlines(keepends=True)
+    rng = random.Random(5)
+    skip = sorted(set([0, 1, len(lines) - 1, len(lines) // 3] + rng.sample(range(len(lines)), len(lines) // 7)))
+    exp = b"".join(l for i, l in enumerate(lines) if i not in set(skip))
+    got = parpa.compact_rows(dev(data), torch.tensor(skip, dtype=torch.int64, device="cuda"))
+    assert bytes(to_np(got).tobytes()) == exp
+    assert bytes(to_np(parpa.compact_rows(dev(data), None)).tobytes()) == data          # nothing skipped
+    run_all_paths(w.dialect, exp, w.types, label=name + "/compacted")   # valid or not, GPU == oracle
