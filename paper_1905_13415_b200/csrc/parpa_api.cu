@@ -64,11 +64,13 @@ int dev_cfg(DevCfg **out) {
     CK(cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev));
     CK(cudaFuncSetAttribute(k_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PASS_SMEM));
     CK(cudaFuncSetAttribute(k_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PASS_SMEM));
-    CK(cudaFuncSetAttribute(k_emit<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
-    CK(cudaFuncSetAttribute(k_emit<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
+    CK(cudaFuncSetAttribute(k_emit<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
+    CK(cudaFuncSetAttribute(k_emit<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
+    CK(cudaFuncSetAttribute(k_emit<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
+    CK(cudaFuncSetAttribute(k_emit<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass1, k_pass1, PASS_WARPS * 32, PASS_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass2, k_pass2, PASS_WARPS * 32, PASS_SMEM));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit<false>, EMIT_WARPS * 32, EMIT_SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit<false, false>, EMIT_WARPS * 32, EMIT_SMEM));
     CK(cudaFuncSetAttribute(k_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMALL_SMEM));
     CK(cudaFuncSetAttribute(k_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMALL_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_small, k_small<false>, SMALL_WARPS * 32, SMALL_SMEM));
@@ -83,8 +85,8 @@ int dev_cfg(DevCfg **out) {
       show("k_tau_scan", (const void *)k_tau_scan);
       show("k_pass2", (const void *)k_pass2);
       show("k_seg_scan", (const void *)k_seg_scan);
-      show("k_emit", (const void *)k_emit<false>);
-      show("k_emit<ts>", (const void *)k_emit<true>);
+      show("k_emit", (const void *)k_emit<false, false>);
+      show("k_emit<ts>", (const void *)k_emit<true, false>);
       fprintf(stderr, "[parpa] occ pass1=%d pass2=%d emit=%d sms=%d\n", c.occ_pass1, c.occ_pass2, c.occ_emit, c.sms);
     }
     cudaMemPool_t pool;
@@ -366,10 +368,12 @@ int launch_emit(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, 
   if (rc) return rc;
   {
     Launch L(s, "k_emit");
-    if (has_timestamps(a, ck))
-      CK(launch_k(k_emit<true>, grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s, true, a, ck));
-    else
-      CK(launch_k(k_emit<false>, grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS), EMIT_WARPS * 32, EMIT_SMEM, s, true, a, ck));
+    const int g = grid_for(dc->occ_emit, dc->sms, a.ntiles, EMIT_WARPS);
+    const bool ts = has_timestamps(a, ck), sk = a.nskip > 0;
+    if (ts && sk) CK(launch_k(k_emit<true, true>, g, EMIT_WARPS * 32, EMIT_SMEM, s, true, a, ck));
+    else if (ts) CK(launch_k(k_emit<true, false>, g, EMIT_WARPS * 32, EMIT_SMEM, s, true, a, ck));
+    else if (sk) CK(launch_k(k_emit<false, true>, g, EMIT_WARPS * 32, EMIT_SMEM, s, true, a, ck));
+    else CK(launch_k(k_emit<false, false>, g, EMIT_WARPS * 32, EMIT_SMEM, s, true, a, ck));
   }
   CK(cudaGetLastError());
   if (launches) (*launches)++;

@@ -504,18 +504,20 @@ __device__ __forceinline__ unsigned long long skipped_before(const KArgs &a, uns
   }
   return lo;
 }
+// SK = false: the emission kernel instantiated for parses without skipped records (no skip-list code).
+template <bool SK = true>
 __device__ __forceinline__ unsigned long long out_row(const KArgs &a, unsigned long long r) {
-  if (a.nskip == 0) return r - a.row_base;
+  if (!SK || a.nskip == 0) return r - a.row_base;
   const unsigned long long k = skipped_before(a, r);
   if (k < a.nskip && a.skip[k] == r) return NONE;
   return r - k - a.row_base;
 }
 
-template <bool TS>
+template <bool TS, bool SK = true>
 __device__ void emit_field(const KArgs &a, const ColDesc *cols, unsigned long long r, uint32_t c, unsigned long long fd,
                            unsigned long long ld, uint32_t fl, unsigned long long dpos, EmitCounters &cnt) {
   if (c >= a.C) { cnt.extra++; return; }
-  unsigned long long row = out_row(a, r);
+  unsigned long long row = out_row<SK>(a, r);
   if (row >= a.cap) return;                         // capacity exceeded (reported by k_finalize) or skipped
   const ColDesc *cd = cols + c;
   if (cd->type == T_SKIP) return;
@@ -552,10 +554,11 @@ __device__ void emit_field(const KArgs &a, const ColDesc *cols, unsigned long lo
   cd->valid[row] = (uint8_t)ok;
 }
 
+template <bool SK = true>
 __device__ void fill_missing(const KArgs &a, const ColDesc *cols, unsigned long long r, uint32_t from, unsigned long long dpos,
                              EmitCounters &cnt) {
   if (from >= a.C) return;
-  unsigned long long row = out_row(a, r);
+  unsigned long long row = out_row<SK>(a, r);
   if (row == NONE) return;                          // a skipped record
   cnt.missing++;
   if (row >= a.cap) return;
@@ -586,7 +589,7 @@ __device__ __forceinline__ void open_combine(unsigned long long &fd, unsigned lo
   }
 }
 
-template <bool TS>
+template <bool TS, bool SK = true>
 __device__ void emit_chunk(const KArgs &a, const ColDesc *cols, const Seg &st, unsigned long long Dm, unsigned long long Fm,
                            unsigned long long Rm, unsigned long long Vm, unsigned long long cbase,
                            EmitCounters &cnt) {
@@ -607,9 +610,9 @@ __device__ void emit_chunk(const KArgs &a, const ColDesc *cols, const Seg &st, u
     unsigned long long sld = fd < 0 ? NONE : cbase + (unsigned)ld;
     if (prev >= 0) { cfd = sfd; cld = sld; cfl = fl; }
     else open_combine(cfd, cld, cfl, sfd, sld, fl);
-    emit_field<TS>(a, cols, r, c, cfd, cld, cfl, cbase + (unsigned)p, cnt);
+    emit_field<TS, SK>(a, cols, r, c, cfd, cld, cfl, cbase + (unsigned)p, cnt);
     if ((Rm >> p) & 1ull) {
-      fill_missing(a, cols, r, c + 1, cbase + (unsigned)p, cnt);
+      fill_missing<SK>(a, cols, r, c + 1, cbase + (unsigned)p, cnt);
       r++;
       c = 0;
     } else {
@@ -774,7 +777,7 @@ __device__ __forceinline__ uint32_t kcount(const WarpScratch *ws, uint32_t x) { 
 // NP > 1 (k_small): NP warps share one tile — part 0 runs E0/E1 into its scratch `ws`, a named barrier
 // (bar, NP warps) publishes it, and every part writes the columns c = part, part + NP, ... in E2 (the
 // column-uniform path) or every NP-th item (the flattened path).  NP == 1 is the one-warp-per-tile path.
-template <bool TS, int NP = 1>
+template <bool TS, int NP = 1, bool SK = true>
 __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, const Seg &prefix,
                           unsigned long long Dm, unsigned long long Fm, unsigned long long Rm,
                           unsigned long long Vm, unsigned long long tbase_g, unsigned long long cbase,
@@ -799,7 +802,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   if (nf > (uint32_t)FCAP || nrec >= (uint32_t)RCAP) {       // warp-uniform: dense tile, direct path
     SegT sagg;
     const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
-    emit_chunk<TS>(a, cols, seg_op(prefix, segt_to_seg(sex, tbase_g)), Dm, Fm, Rm, Vm, cbase, cnt);
+    emit_chunk<TS, SK>(a, cols, seg_op(prefix, segt_to_seg(sex, tbase_g)), Dm, Fm, Rm, Vm, cbase, cnt);
     if (NP == 1) return;
     nf = 0u;                                                  // the other parts have nothing to write
     nrec = 0u;
@@ -892,7 +895,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
         if (rel >= 0 && L <= (unsigned long long)WT) {
           e = (uint32_t)rel | ((uint32_t)L << 11) | icf;
         } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
-          emit_field<TS>(a, cols, prefix.recs, c0, cfd, cld, cfl, tbase_g + p, cnt);
+          emit_field<TS, SK>(a, cols, prefix.recs, c0, cfd, cld, cfl, tbase_g + p, cnt);
           e = FIELD_WRITTEN;
           if (c0 >= a.C) cnt.extra--;                           // emit_field counted it already
         } else {
@@ -975,7 +978,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
             if (rel >= 0 && L <= (unsigned long long)WT) {
               e = (uint32_t)rel | ((uint32_t)L << 11) | icf;
             } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
-              emit_field<TS>(a, cols, prefix.recs + jr, c, cfd, cld, cfl, tbase_g + p, cnt);
+              emit_field<TS, SK>(a, cols, prefix.recs + jr, c, cfd, cld, cfl, tbase_g + p, cnt);
               e = FIELD_WRITTEN;
               if (c >= a.C) cnt.extra--;                      // emit_field counted it already
             } else {
@@ -1030,7 +1033,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
         end = closed ? (rw & 0xFFFFu) : nf;
         dpos = rw >> 16;
         cs = ji == 0 ? c0 : 0u;
-        row = out_row(a, r0 + ji);
+        row = out_row<SK>(a, r0 + ji);
         live = row < a.cap;
       }
       if ((NP == 1 || part == 0) && live && closed && end - start + cs < a.C) cnt.missing++;   // short record
@@ -1108,7 +1111,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     const uint32_t end = ji < nrec ? (ws->rows[ji] & 0xFFFFu) : nf;
     const uint32_t cs = ji == 0 ? c0 : 0u;
     if (ci < cs) continue;                                  // written by an earlier tile
-    const unsigned long long row = out_row(a, r0 + ji);
+    const unsigned long long row = out_row<SK>(a, r0 + ji);
     if (row >= a.cap) continue;
     const uint32_t k = start + (ci - cs);
     const ColDesc *cd = cols + ci;
@@ -1170,7 +1173,7 @@ constexpr size_t EMIT_SMEM = EMIT_WARPS * sizeof(WarpScratch);
 
 // S6+S7 per warp tile from what the scan half stored: the DATA / DELIM / RECORD masks of every chunk
 // (k_pass2) and the tile prefix (k_seg_scan).  No LUT, no re-simulation: 2 CTAs per SM.
-template <bool TS>
+template <bool TS, bool SK>
 __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const KArgs a, const ColsK colsk) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ ColDesc s_cols[MAX_COLS];
@@ -1212,7 +1215,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const
     const unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;
     const unsigned long long Dm = mk[0], Fm = mk[32], Rm = mk[64];
     const unsigned long long Vm = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull);
-    emit_tile<TS>(a, s_cols, ws, seg_op(a.seed, a.tinfo[t].excl), Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
+    emit_tile<TS, 1, SK>(a, s_cols, ws, seg_op(a.seed, a.tinfo[t].excl), Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
   }
 #ifndef PARPA_EMIT_STATIC
   if (lane == 0 && atomicAdd(&a.ctrl->emit_done, 1u) == nw - 1u) {   // last warp out: ready for the next launch
