@@ -333,7 +333,7 @@ def run_e2e(parpa, dfa, schema, data_host, cap, w, steps):
             times.append(dt)
     t = statistics.mean(times)
     return {"value": round(data_host.numel() / t / 1e9, 3), "unit": "GB/s",
-            "h2d_bytes_per_step": int(data_host.numel()), "d2h_bytes_per_step": int(out_bytes + 56),
+            "h2d_bytes_per_step": int(data_host.numel()), "d2h_bytes_per_step": int(out_bytes + 64),
             "ms_per_step": round(t * 1e3, 2), "api": "parpa_parse_host (pinned host input and columns)"}
 
 

@@ -124,9 +124,13 @@ typedef struct {
                                  EOI when the end state's action is error; PARPA_NONE if valid */
   uint64_t missing_records;   /* records with fewer than C fields */
   uint64_t extra_fields;      /* fields beyond column C-1 (dropped) */
-  uint64_t deferred_fields;   /* typed fields converted by the slow (device-tier) path */
+  uint64_t deferred_fields;   /* typed fields converted by the device tiers (thread, block, grid) */
   int32_t status;             /* PARPA_OK / EFORMAT / ECOLUMNS / EUNSUPPORTED / ENEEDMORE */
   uint32_t final_state;       /* DFA state after the last byte */
+  uint32_t block_fields;      /* of deferred_fields: int64 / float64 fields of >= 1 KB without inner control
+                                 bytes, converted by one thread block each */
+  uint32_t device_fields;     /* of deferred_fields: such fields of >= 256 KB, converted by the whole grid
+                                 (device-level collaboration) */
 } parpa_stats;
 
 /* ---- one-call parse (library-sized outputs) --------------------------------------------- *

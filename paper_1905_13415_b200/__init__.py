@@ -171,7 +171,8 @@ def stats_from_tensor(t):
     s = _lib.Stats_t.from_buffer_copy(raw[:_lib.STATS_BYTES])
     return {"records": s.records, "fields": s.fields, "first_invalid": s.first_invalid,
             "missing_records": s.missing_records, "extra_fields": s.extra_fields,
-            "deferred_fields": s.deferred_fields, "status": s.status, "final_state": s.final_state}
+            "deferred_fields": s.deferred_fields, "status": s.status, "final_state": s.final_state,
+            "block_fields": s.block_fields, "device_fields": s.device_fields}
 
 
 def new_stats_tensor(device="cuda"):

@@ -24,7 +24,8 @@ class Column_t(ctypes.Structure):
 class Stats_t(ctypes.Structure):
     _fields_ = [("records", ctypes.c_uint64), ("fields", ctypes.c_uint64), ("first_invalid", ctypes.c_uint64),
                 ("missing_records", ctypes.c_uint64), ("extra_fields", ctypes.c_uint64),
-                ("deferred_fields", ctypes.c_uint64), ("status", ctypes.c_int32), ("final_state", ctypes.c_uint32)]
+                ("deferred_fields", ctypes.c_uint64), ("status", ctypes.c_int32), ("final_state", ctypes.c_uint32),
+                ("block_fields", ctypes.c_uint32), ("device_fields", ctypes.c_uint32)]
 
 
 class Tau_t(ctypes.Structure):
@@ -43,7 +44,7 @@ class Context_t(ctypes.Structure):
 
 
 STATS_BYTES = ctypes.sizeof(Stats_t)
-assert STATS_BYTES == 56
+assert STATS_BYTES == 64
 
 _lock = threading.Lock()
 _lib = None

@@ -154,9 +154,11 @@ struct Work {
   uint8_t *chunk_state = nullptr;
   unsigned long long *masks = nullptr;
   DeferItem *dq = nullptr;
+  unsigned long long *lq = nullptr, *hq = nullptr;   // block- / device-tier queues (parpa_collab.cuh)
+  CollabAcc *hacc = nullptr;
   Stats *stats = nullptr;
   uint8_t *aligned_in = nullptr;
-  uint32_t ntiles = 0, nblk = 0, dq_cap = 0;
+  uint32_t ntiles = 0, nblk = 0, dq_cap = 0, lq_cap = 0, hq_cap = 0;
 };
 
 // One cudaMallocAsync block per call: the look-back descriptors and control words (zeroed), then the
@@ -184,6 +186,12 @@ int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cu
   size_t o_cs = o; o = align_up(o + nt * 32);
   size_t o_mk = o; o = align_up(o + nt * 96 * 8);
   size_t o_dq = o; o = align_up(o + (size_t)w.dq_cap * sizeof(DeferItem));
+  // spans are disjoint: at most len / COLLAB_MIN fields of >= COLLAB_MIN bytes (+ one reaching into a halo)
+  w.lq_cap = (uint32_t)std::min<uint64_t>(len / COLLAB_MIN + 4, 0xFFFFFFF0ull);
+  w.hq_cap = (uint32_t)(len / DEVICE_MIN + 4);
+  size_t o_lq = o; o = align_up(o + (size_t)w.lq_cap * 8);
+  size_t o_hq = o; o = align_up(o + (size_t)w.hq_cap * 8);
+  size_t o_ha = o; o = align_up(o + (size_t)w.hq_cap * sizeof(CollabAcc));
   size_t o_st = o; o = align_up(o + sizeof(Stats));
   size_t o_in = o; if (need_aligned_copy) o = align_up(o + len);
   CK(cudaMallocAsync(&w.block, o, s));
@@ -203,6 +211,9 @@ int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cu
   w.chunk_state = b + o_cs;
   w.masks = (unsigned long long *)(b + o_mk);
   w.dq = (DeferItem *)(b + o_dq);
+  w.lq = (unsigned long long *)(b + o_lq);
+  w.hq = (unsigned long long *)(b + o_hq);
+  w.hacc = (CollabAcc *)(b + o_ha);
   w.stats = (Stats *)(b + o_st);
   w.aligned_in = need_aligned_copy ? b + o_in : nullptr;
   CK(cudaMemsetAsync(w.block, 0, zero, s));
@@ -247,6 +258,12 @@ void make_args(KArgs &a, const Work &w, const uint8_t *in, uint64_t len) {
   a.ctrl = w.ctrl;
   a.dq = w.dq;
   a.dq_cap = w.dq_cap;
+  static const bool collab = !(getenv("PARPA_NO_COLLAB") && getenv("PARPA_NO_COLLAB")[0] == '1');   // A/B, tests
+  a.lq = collab ? w.lq : nullptr;
+  a.hq = w.hq;
+  a.hacc = w.hacc;
+  a.lq_cap = w.lq_cap;
+  a.hq_cap = w.hq_cap;
   a.is_last = 1;
   a.cap = 0;
   a.left_state = 0xFFu;                                     // no halo state known
@@ -303,6 +320,24 @@ cudaError_t launch_k(void (*k)(P...), unsigned grid, unsigned block, size_t smem
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl && pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+// the same with the cooperative attribute (co-resident CTAs: grid barriers are allowed)
+template <typename... P, typename... A>
+cudaError_t launch_coop(void (*k)(P...), unsigned grid, unsigned block, size_t smem, cudaStream_t s, bool pdl,
+                        A &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl && pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
 }
 
@@ -441,8 +476,9 @@ int launch_tail(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, 
   CK(cudaGetLastError());
   {
     Launch L(s, "k_deferred");
-    if (has_timestamps(a, ck)) CK(launch_k(k_deferred<true>, dc->sms * 2, 128, 0, s, true, a, k, ck));
-    else CK(launch_k(k_deferred<false>, dc->sms * 2, 128, 0, s, true, a, k, ck));
+    // cooperative: the device tier of parpa_collab.cuh separates its sweeps by grid barriers
+    if (has_timestamps(a, ck)) CK(launch_coop(k_deferred<true>, dc->sms * 2, 128, 0, s, true, a, k, ck));
+    else CK(launch_coop(k_deferred<false>, dc->sms * 2, 128, 0, s, true, a, k, ck));
   }
   CK(cudaGetLastError());
   if (launches) *launches += 2;
@@ -1025,6 +1061,8 @@ static int parse_host_stream(const parpa_dfa *dfa, const parpa_schema *sch, cons
       t.missing_records += pst[i].missing_records;
       t.extra_fields += pst[i].extra_fields;
       t.deferred_fields += pst[i].deferred_fields;
+      t.block_fields += pst[i].block_fields;
+      t.device_fields += pst[i].device_fields;
       t.first_invalid = std::min(t.first_invalid, pst[i].first_invalid);
       const int ps = pst[i].status;
       if (ps == ST_EFORMAT) st = ST_EFORMAT;

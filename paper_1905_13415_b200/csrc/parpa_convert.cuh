@@ -394,6 +394,7 @@ __device__ __noinline__ int conv_timestamp(Src &s, long long &out) {
 //   IN CONTRACT, STRICT LIABILITY, OR TORT (INCLUDING NEGLIGENCE OR OTHERWISE) ARISING IN ANY WAY OUT
 //   OF THE USE OF THIS SOFTWARE, EVEN IF ADVISED OF THE POSSIBILITY OF SUCH DAMAGE.
 constexpr int DEC_MAX = 800;
+constexpr long long EXP_SAT = 100000000000ll;     // exponent accumulation stops at >= 10^11 (12 digits)
 struct Decimal {
   uint8_t d[DEC_MAX];            // digit values 0..9, most significant first; value = 0.d × 10^dp
   int nd, dp;
@@ -579,8 +580,8 @@ __device__ int conv_float64_exact(Src &s, long long &bits) {
       more = s.next(c);
     }
     while (more && (unsigned)(c - '0') <= 9u) {
-      if (ex < 100000) ex = ex * 10 + (c - '0');
-      nex++;
+      if (ex < EXP_SAT) ex = ex * 10 + (c - '0');   // saturates beyond any significand's reach (< 2^32
+      nex++;                                        // digits), so the clamp below decides correctly
       more = s.next(c);
     }
     if (nex == 0) return 0;

@@ -14,6 +14,7 @@
 //                    drop them) and floats outside the exact fast path (exact decimal algorithm).
 //   k_debug_trace    per-byte states / emission kinds from the per-chunk entry states (tests only).
 #pragma once
+#include <cooperative_groups.h>
 #include "parpa_convert.cuh"
 #include "parpa_device.cuh"
 
@@ -87,6 +88,9 @@ struct Ctrl {
   unsigned int n_defer;
   unsigned int defer_overflow;
   unsigned int unsupported;
+  unsigned int n_long;               // fields queued for the block tier (parpa_collab.cuh)
+  unsigned int n_huge;               // fields queued for the device tier
+  unsigned int pad1;
   unsigned long long inv_neg;        // ~(first invalid byte position), 0 = none (atomicMax)
   unsigned long long n_missing;
   unsigned long long n_extra;
@@ -106,6 +110,12 @@ struct Stats {                       // mirrors parpa_stats
   unsigned long long records, fields, first_invalid, missing_records, extra_fields, deferred_fields;
   int status;
   uint32_t final_state;
+  uint32_t block_fields, device_fields;
+};
+
+struct CollabAcc {                   // per long field: reductions over its bytes (parpa_collab.cuh)
+  unsigned long long first_dot, first_e, p0, plast, pexp;   // NONE = no such position
+  uint32_t n_dot, n_e, bad, pad;
 };
 
 struct KArgs {
@@ -138,6 +148,9 @@ struct KArgs {
   Ctrl *ctrl;
   DeferItem *dq;
   uint32_t dq_cap, strict;
+  unsigned long long *lq, *hq;       // block- / device-tier queues: row | column << 56 (parpa_collab.cuh)
+  CollabAcc *hacc;                   // [hq_cap] device-tier accumulators
+  uint32_t lq_cap, hq_cap;
   Stats *stats;
   unsigned long long *prof;          // optional [gridDim][16] cycle counters (PARPA_DEBUG)
 };
@@ -260,6 +273,78 @@ __device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_
   return x & 0xFu;
 }
 
+// The same masks with a strided pack: the step result of byte i (i = 32h + 8p + s) goes into byte p of word
+// W[s] (one PRMT), so that bit-plane k of the 32 bytes is  sum_s ((W[s] >> k) & 0x01010101) << s  — bit
+// 8p + s = byte i, already in input order: one shift and one LOP3 per word and plane (the shifts on the FMA
+// pipe as multiplies), instead of a 4-byte pack plus a multiply-gather per 4 bytes.
+template <int SH>
+__device__ __forceinline__ uint32_t plane_bits(uint32_t w) {   // (w >> 4 | 5) & 0x01010101, moved up by s
+  if (SH >= 0) return w * (1u << SH);                          // IMAD.SHL (FMA pipe)
+  return __umulhi(w, 1u << (32 + SH));                         // w >> -SH (FMA pipe)
+}
+template <bool FULL, bool NS4 = false, bool DP = false>
+__device__ __forceinline__ uint32_t chunk_masks_t(uint32_t laneaddr, const uint32_t (&v)[16], int nvalid, uint32_t entry,
+                                                  unsigned long long &Dm, unsigned long long &Fm,
+                                                  unsigned long long &Rm) {
+  uint32_t x = 0x80u | entry;
+  uint32_t g4[2], g5[2];
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    uint32_t W[8];
+#pragma unroll
+    for (int s = 0; s < 8; s++) W[s] = 0u;
+#pragma unroll
+    for (int j = 0; j < 32; j++) {
+      const int i = 32 * h + j, p = j >> 3, sidx = j & 7;
+      uint32_t r = 0xFFu;                                    // outside the chunk: not data / delimiter
+      if (FULL || i < nvalid) {
+        const uint32_t ad = lut_addr<DP>(v[i >> 2], (uint32_t)(i & 3), laneaddr) + (DP ? 0u : 128u);
+        if (NS4) {
+          const uint32_t st = lds_u1(ad);
+          x = prmt(st, st, x);
+        } else {
+          const uint2 st = lds_u2<0>(ad);
+          x = prmt(st.x, st.y, x);
+        }
+        r = x;
+      }
+      W[sidx] = prmt(W[sidx], r, p == 0 ? 0x3214u : p == 1 ? 0x3240u : p == 2 ? 0x3410u : 0x4210u);
+    }
+    uint32_t a4 = 0u, a5 = 0u;
+#pragma unroll
+    for (int sidx = 0; sidx < 8; sidx++) {
+      const uint32_t m = 0x01010101u << sidx;
+      // bit 4 (5) of byte p of W[s] -> bit 8p + s
+      uint32_t u4, u5;
+      switch (sidx) {
+        case 0: u4 = plane_bits<-4>(W[0]); u5 = plane_bits<-5>(W[0]); break;
+        case 1: u4 = plane_bits<-3>(W[1]); u5 = plane_bits<-4>(W[1]); break;
+        case 2: u4 = plane_bits<-2>(W[2]); u5 = plane_bits<-3>(W[2]); break;
+        case 3: u4 = plane_bits<-1>(W[3]); u5 = plane_bits<-2>(W[3]); break;
+        case 4: u4 = W[4]; u5 = plane_bits<-1>(W[4]); break;
+        case 5: u4 = plane_bits<1>(W[5]); u5 = W[5]; break;
+        case 6: u4 = plane_bits<2>(W[6]); u5 = plane_bits<1>(W[6]); break;
+        default: u4 = plane_bits<3>(W[7]); u5 = plane_bits<2>(W[7]); break;
+      }
+      a4 |= u4 & m;
+      a5 |= u5 & m;
+    }
+    g4[h] = a4;
+    g5[h] = a5;
+  }
+  const unsigned long long b4 = (unsigned long long)g4[0] | ((unsigned long long)g4[1] << 32);
+  const unsigned long long b5 = (unsigned long long)g5[0] | ((unsigned long long)g5[1] << 32);
+  Dm = ~(b4 | b5);
+  Fm = b4 ^ b5;
+  Rm = b5 & ~b4;
+  return x & 0xFu;
+}
+#ifdef PARPA_MASK_GATHER
+#define CHUNK_MASKS chunk_masks
+#else
+#define CHUNK_MASKS chunk_masks_t
+#endif
+
 // ---- 4-way ILP τ: the chunk is cut into four 16-byte quarters with independent PRMT chains, composed
 // at the end.  qt[q] = nibble τ of quarter q (q = 0..2).
 // NS4: at most four device states (+ INV): τ in byte form fits one register, and one PRMT per byte
@@ -331,6 +416,30 @@ __device__ __forceinline__ uint32_t warp_scan_tau(uint32_t t0, uint32_t t1, uint
   }
   agg = __shfl_sync(0xffffffffu, inc, 31);
   uint32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
+  return lane == 0 ? NIB_IDENT : ex;
+}
+
+// At most four device states (chunk_tau4<NS4>): t0 = τ in byte form (entries 0-3; INV = 0xFF); entries 4-7
+// stay the identity, so each step is one PRMT with the earlier prefix's nibbles as selector (an INV nibble
+// replicates the sign of byte 3: INV stays INV) and a 3-instruction repack of four nibbles.
+__device__ __forceinline__ uint32_t nib4(uint32_t b) {        // byte form (entries 0-3) -> nibble form
+  uint32_t x = b & 0x0F0F0F0Fu;
+  x |= x >> 4;
+  return prmt(x, 0x7654u, 0x5420u);
+}
+__device__ __forceinline__ uint32_t warp_scan_tau4(uint32_t t0, uint32_t &agg) {
+  const int lane = threadIdx.x & 31;
+  uint32_t b = t0, inc = nib4(t0);
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) {                         // inc <- o ∘ inc
+      b = prmt(b, b, o);
+      inc = nib4(b);
+    }
+  }
+  agg = __shfl_sync(0xffffffffu, inc, 31);
+  const uint32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
   return lane == 0 ? NIB_IDENT : ex;
 }
 
@@ -482,8 +591,10 @@ struct RawSrc {                       // the raw span [pos, end] of a field with
 // its valid byte (VALID_REDO_IC / VALID_REDO) and k_deferred, seeing defer_overflow, converts every marked
 // row of the typed columns from its span: any number of deferred fields parses.
 constexpr uint8_t VALID_REDO = 0xFF, VALID_REDO_IC = 0xFE;
+#include "parpa_collab.cuh"
 __device__ __forceinline__ void push_defer(const KArgs &a, const ColDesc *cd, unsigned long long fd,
                                            unsigned long long ld, unsigned long long row, uint32_t c, uint32_t ic) {
+  if (!ic && push_collab(a, cd, fd, ld, row, c)) return;   // long numeric fields: block / device tier
   uint32_t idx = atomicAdd(&a.ctrl->n_defer, 1u);
   if (idx < a.dq_cap) {
     cd->valid[row] = 0;              // k_deferred's overflow sweep must only see markers of this launch
@@ -544,7 +655,8 @@ __device__ void emit_field(const KArgs &a, const ColDesc *cols, unsigned long lo
     return;
   } else {
     RawSrc src{&a, fd, ld, true};
-    int res = conv_typed<TS>(src, type, v);
+    // long fields skip the one-thread attempt: push_defer hands them to the block / device tier
+    int res = ld + 1 - fd < COLLAB_MIN ? conv_typed<TS>(src, type, v) : 2;
     if (!src.ok) res = 2;                           // bytes outside this range: device tier
     if (res == 2) { push_defer(a, cd, fd, ld, row, c, 0u); return; }
     ok = res;
@@ -715,7 +827,7 @@ __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, u
                           __funnelshift_r(w3, w4, sh), (uint32_t)L, isf, v);
       }
     }
-    if (res == 2) {
+    if (res == 2 && L < COLLAB_MIN) {                // (long fields: push_defer -> block / device tier)
       TileSrc src{&a, tb, tbase, fd, ld, true};
       res = conv_typed<TS>(src, cd->type, v);
       if (!src.ok) res = 2;
@@ -1193,11 +1305,30 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const
   // share the boundary sectors of every output column) stay together in time: with a static grid stride
   // the warps drift apart over ~500 tiles each and the boundary sectors leave L2 half written (DRAM
   // read-modify-write; measured at 4.8 GB of taxi).
+#ifdef PARPA_EMIT_TICKET2
+  // Tickets are taken one tile ahead: the atomic for the tile after next is in flight while this tile is
+  // processed, and the next tile's bytes, masks and prefix are prefetched into L2 as soon as it is known.
+  uint32_t tk = 0;
+  if (lane == 0) tk = atomicAdd(&a.ctrl->emit_ticket, 2u);
+  tk = __shfl_sync(0xffffffffu, tk, 0);
+  uint32_t t = tk, tn = tk + 1;
+  while (true) {
+    if (t >= a.ntiles) break;
+    uint32_t tnn = 0;
+    if (lane == 0 && tn < a.ntiles) tnn = atomicAdd(&a.ctrl->emit_ticket, 1u);
+    if (tn < a.ntiles) {                                   // the warp's next tile into L2
+      const unsigned long long tb = (unsigned long long)tn;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in + tb * WT + (unsigned long long)lane * CHUNK));
+      if (lane < 6) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.masks + tb * 96 + lane * 16));
+      if (lane == 6) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.tinfo + tb));
+    }
+#else
   while (true) {
     uint32_t t = 0;
     if (lane == 0) t = atomicAdd(&a.ctrl->emit_ticket, 1u);
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= a.ntiles) break;
+#endif
 #endif
     const unsigned long long tstart = (unsigned long long)t * WT;
     const unsigned long long cstart = tstart + (unsigned long long)lane * CHUNK;
@@ -1207,15 +1338,21 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const
       load_chunk(a.in + cstart, nvalid, v);
       stash_chunk(ws->bytes, lane, v);
     }
+#if defined(PARPA_EMIT_STATIC) || !defined(PARPA_EMIT_TICKET2)
     if (t + nw < a.ntiles) {                              // the warp's next tile into L2 (2 KB + 768 B masks):
       const unsigned long long tn = (unsigned long long)(t + nw);   // its loads then wait on L2, not DRAM
       asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in + tn * WT + (unsigned long long)lane * CHUNK));
       if (lane < 6) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.masks + tn * 96 + lane * 16));
     }
+#endif
     const unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;
     const unsigned long long Dm = mk[0], Fm = mk[32], Rm = mk[64];
     const unsigned long long Vm = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull);
     emit_tile<TS, 1, SK>(a, s_cols, ws, seg_op(a.seed, a.tinfo[t].excl), Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
+#if !defined(PARPA_EMIT_STATIC) && defined(PARPA_EMIT_TICKET2)
+    t = tn;
+    tn = __shfl_sync(0xffffffffu, tnn, 0);
+#endif
   }
 #ifndef PARPA_EMIT_STATIC
   if (lane == 0 && atomicAdd(&a.ctrl->emit_done, 1u) == nw - 1u) {   // last warp out: ready for the next launch
@@ -1275,7 +1412,9 @@ __device__ void finalize_one(const KArgs &a, const DfaK &dfa, const ColsK &colsk
     a.stats->first_invalid = first_inv;
     a.stats->missing_records = missing;
     a.stats->extra_fields = extra;
-    a.stats->deferred_fields = n_defer;
+    a.stats->block_fields = a.lq ? min(ld_volatile_u32(&a.ctrl->n_long), a.lq_cap) : 0u;
+    a.stats->device_fields = a.lq ? min(ld_volatile_u32(&a.ctrl->n_huge), a.hq_cap) : 0u;
+    a.stats->deferred_fields = (unsigned long long)n_defer + a.stats->block_fields + a.stats->device_fields;
     a.stats->status = status;
     a.stats->final_state = fin_exact;
   }
@@ -1383,6 +1522,9 @@ __global__ void k_deferred(const __grid_constant__ KArgs a, const __grid_constan
   const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
   const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
   deferred_all<TS>(a, dfa, colsk, tid, nth);
+  __shared__ CollabSmem s_collab;                  // long numeric fields: block tier, then device tier
+  collab_block_tier<TS>(a, colsk, s_collab);
+  if (a.lq && ld_volatile_u32(&a.ctrl->n_huge)) collab_device_tier<TS>(a, colsk, s_collab);   // (cooperative launch)
   // the last block to finish settles the status (every block's conversions are done by then)
   __syncthreads();
   if (threadIdx.x == 0) {

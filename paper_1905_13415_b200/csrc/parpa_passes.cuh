@@ -64,11 +64,13 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src, uint32_t 
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ void stage_chunk(const KArgs &a, uint4 *buf, uint32_t t, int lane) {
+// nfull = tiles entirely inside the input (a 32-bit compare per tile: the pass kernels are ALU-bound)
+__device__ __forceinline__ void stage_chunk(const KArgs &a, uint4 *buf, uint32_t t, int lane, uint32_t nfull) {
   const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
-  if ((unsigned long long)(t + 1) * WT <= a.len) {                  // whole tile in range (all but the last):
-#pragma unroll                                                         // no per-unit clamps (the pass kernels
-    for (int u = 0; u < 4; u++) cp_async16(buf + pswz(lane, u), a.in + cstart + 16 * u, 16u);   // are ALU-bound)
+  if (t < nfull) {                                                     // whole tile in range (all but the last):
+    const uint8_t *src = a.in + cstart;                                // no per-unit clamps
+#pragma unroll
+    for (int u = 0; u < 4; u++) cp_async16(buf + pswz(lane, u), src + 16 * u, 16u);
     return;
   }
   const int nv = chunk_valid(a, cstart);
@@ -97,27 +99,34 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass1(const KArgs a, con
   pdl_wait();
   uint4 *bufs = ps.bufs;
   const uint32_t nw = gridDim.x * PASS_WARPS;
+  const uint32_t nfull = (uint32_t)(a.len / WT);
   uint32_t t = blockIdx.x * PASS_WARPS + warp;
-  if (t < a.ntiles) stage_chunk(a, bufs, t, lane);
+  if (t < a.ntiles) stage_chunk(a, bufs, t, lane, nfull);
   cp_async_commit();
   for (uint32_t i = 0; t < a.ntiles; t += nw, i ^= 1u) {
-    if (t + nw < a.ntiles) stage_chunk(a, bufs + (i ^ 1u) * (WT / 16), t + nw, lane);
+    if (t + nw < a.ntiles) stage_chunk(a, bufs + (i ^ 1u) * (WT / 16), t + nw, lane, nfull);
     cp_async_commit();
     cp_async_wait1();
-    const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
-    const int nv = chunk_valid(a, cstart);
-    uint32_t v[16], t0, t1, qt[3];
+    uint32_t v[16], t0, t1, qt[3], agg, ex;
     read_chunk(bufs + i * (WT / 16), lane, v);
     if (dfa.nlive <= 4) {                                   // warp-uniform (kernel parameter)
       const uint32_t la4 = ps.laneaddr - ps.laneoff + (uint32_t)lane * 4u;   // one 4-byte slot per lane
-      if (nv == CHUNK) chunk_tau4<true, true>(la4, v, nv, t0, t1, qt);
-      else chunk_tau4<false, true>(la4, v, nv, t0, t1, qt);
+      if (t < nfull) {
+        chunk_tau4<true, true>(la4, v, CHUNK, t0, t1, qt);
+      } else {
+        const int nv = chunk_valid(a, (unsigned long long)t * WT + (unsigned long long)lane * CHUNK);
+        chunk_tau4<false, true>(la4, v, nv, t0, t1, qt);
+      }
+      ex = warp_scan_tau4(t0, agg);
     } else {
-      if (nv == CHUNK) chunk_tau4<true>(ps.laneaddr, v, nv, t0, t1, qt);
-      else chunk_tau4<false>(ps.laneaddr, v, nv, t0, t1, qt);
+      if (t < nfull) {
+        chunk_tau4<true>(ps.laneaddr, v, CHUNK, t0, t1, qt);
+      } else {
+        const int nv = chunk_valid(a, (unsigned long long)t * WT + (unsigned long long)lane * CHUNK);
+        chunk_tau4<false>(ps.laneaddr, v, nv, t0, t1, qt);
+      }
+      ex = warp_scan_tau(t0, t1, agg);
     }
-    uint32_t agg;
-    const uint32_t ex = warp_scan_tau(t0, t1, agg);
     a.lex[(unsigned long long)t * 32 + lane] = ex;
     if (lane == 0) a.wtau[t] = agg;
   }
@@ -237,15 +246,16 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, con
   pdl_wait();
   uint4 *bufs = ps.bufs;
   const uint32_t nw = gridDim.x * PASS_WARPS;
+  const uint32_t nfull = (uint32_t)(a.len / WT);
   uint32_t t = blockIdx.x * PASS_WARPS + warp;
-  if (t < a.ntiles) stage_chunk(a, bufs, t, lane);
+  if (t < a.ntiles) stage_chunk(a, bufs, t, lane, nfull);
   cp_async_commit();
   for (uint32_t i = 0; t < a.ntiles; t += nw, i ^= 1u) {
-    if (t + nw < a.ntiles) stage_chunk(a, bufs + (i ^ 1u) * (WT / 16), t + nw, lane);
+    if (t + nw < a.ntiles) stage_chunk(a, bufs + (i ^ 1u) * (WT / 16), t + nw, lane, nfull);
     cp_async_commit();
     cp_async_wait1();
     const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
-    const int nv = chunk_valid(a, cstart);
+    const int nv = t < nfull ? CHUNK : chunk_valid(a, cstart);
     uint32_t v[16];
     read_chunk(bufs + i * (WT / 16), lane, v);
     const uint32_t entry = nib_at(a.lex[(unsigned long long)t * 32 + lane], nib_at(a.wpre[t], a.seed_dev));
@@ -254,11 +264,11 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, con
     uint32_t fin;
     if (dfa.nlive <= 4) {
       const uint32_t la4 = lbase - ps.laneoff + (uint32_t)lane * 4u;   // one 4-byte slot per lane
-      if (nv == CHUNK) fin = chunk_masks<true, true, true>(la4, v, nv, entry, Dm, Fm, Rm);
-      else fin = chunk_masks<false, true, true>(la4, v, nv, entry, Dm, Fm, Rm);
+      if (nv == CHUNK) fin = CHUNK_MASKS<true, true, true>(la4, v, nv, entry, Dm, Fm, Rm);
+      else fin = CHUNK_MASKS<false, true, true>(la4, v, nv, entry, Dm, Fm, Rm);
     } else {
-      if (nv == CHUNK) fin = chunk_masks<true, false, true>(lbase, v, nv, entry, Dm, Fm, Rm);
-      else fin = chunk_masks<false, false, true>(lbase, v, nv, entry, Dm, Fm, Rm);
+      if (nv == CHUNK) fin = CHUNK_MASKS<true, false, true>(lbase, v, nv, entry, Dm, Fm, Rm);
+      else fin = CHUNK_MASKS<false, false, true>(lbase, v, nv, entry, Dm, Fm, Rm);
     }
     if (fin == INV_DEV && entry != INV_DEV && nv > 0) {
       int p = first_inv_in_chunk(ps.lut, a.in + cstart, nv, ps.laneoff, entry, STEP_ROW_DP);

@@ -252,6 +252,11 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 1) k_small(const __grid_cons
   SMALL_MARK(11);
   deferred_all<TS>(a, dfa, colsk, (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
                    (unsigned long long)gridDim.x * blockDim.x);
+  {
+    __shared__ CollabSmem s_collab;                // long numeric fields: block tier, then device tier
+    collab_block_tier<TS>(a, colsk, s_collab);
+    if (a.lq && ld_volatile_u32(&a.ctrl->n_huge)) collab_device_tier<TS>(a, colsk, s_collab);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
