@@ -264,6 +264,33 @@ int parpa_strings_copy(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t le
                        const parpa_column *column, uint64_t rows, const int64_t *d_offsets,
                        uint8_t *d_data, void *stream);
 
+/* ---- the CSS from a plan, three layouts (alternative tagging modes P:493-502) --------- *
+ * The same string materialisation as above, but from a parpa_plan of the same bytes (its chunk masks are
+ * reused: no second scan half).  column / rows: a column emitted from this plan (device offset / length).
+ * mode PARPA_CSS_ARROW  : d_data = the DATA bytes of every field in row order; d_offsets[r] = start of
+ *                         field r, d_offsets[rows] = total.
+ * mode PARPA_CSS_INLINE : inline-terminated CSS: each field's bytes followed by `terminator`
+ *                         (e.g. 0x1F, unit separator); d_offsets[r] = start of field r, its terminator at
+ *                         d_offsets[r + 1] - 1; total = Arrow total + rows.  The terminator must not occur
+ *                         in the column's CSS: if it does the copy returns PARPA_EUNSUPPORTED (bytes written).
+ * mode PARPA_CSS_VECTOR : vector-delimited CSS: d_data as ARROW, plus d_aux (device, total
+ *                         bytes): 1 at the last symbol of every non-empty field, else 0.
+ * parpa_plan_strings_size fills d_offsets (rows + 1 int64) and *total; parpa_plan_strings_copy writes d_data
+ * (>= total bytes) and, for VECTOR, d_aux.  Both synchronous on `stream`.  Errors: PARPA_EINVAL (null
+ * pointers, mode > 2, terminator > 255, VECTOR without d_aux).
+ * parpa_css_index — the CSS's index the way the paper builds it: the positions, in order,
+ * of every terminator (INLINE: d_data[k] == terminator) or nonzero auxiliary entry (VECTOR: d_aux[k] != 0)
+ * among n bytes, written to d_index (device, room for the number of fields); *count = how many.  Stream
+ * compaction (per-tile counts, exclusive scan, ordered writes); synchronous.  Errors: PARPA_EINVAL. */
+enum { PARPA_CSS_ARROW = 0, PARPA_CSS_INLINE = 1, PARPA_CSS_VECTOR = 2 };
+int parpa_plan_strings_size(parpa_plan *plan, const parpa_column *column, uint64_t rows, uint32_t mode,
+                            int64_t *d_offsets, uint64_t *total, void *stream);
+int parpa_plan_strings_copy(parpa_plan *plan, const parpa_column *column, uint64_t rows, uint32_t mode,
+                            uint32_t terminator, const int64_t *d_offsets, uint8_t *d_data, uint8_t *d_aux,
+                            void *stream);
+int parpa_css_index(uint32_t mode, uint32_t terminator, const uint8_t *d_data, const uint8_t *d_aux, uint64_t n,
+                    uint64_t *d_index, uint64_t *count, void *stream);
+
 /* ---- staged range plan: the same exchange with every pass run once per rank ------------- *
  * parpa_range_begin  runs S1-S3 on the device range [d_bytes, d_bytes+len) at global offset
  *                    `base` and returns the range's transition vector (host *tau_out) — the

@@ -231,6 +231,45 @@ def strings(dialect, data, C: int, col: int, types=None):
     return offs, bytes(buf[:n])
 
 
+CSS_ARROW, CSS_INLINE, CSS_VECTOR = 0, 1, 2
+
+
+def css(dialect, data, C: int, col: int, types=None, mode=CSS_ARROW, terminator=0x1F):
+    """The column's CSS in one of the paper's layouts (alternative tagging modes P:493-502),
+    written out from ``strings`` (the DATA bytes of each field, in row order):
+      CSS_ARROW  -> (offsets, data)
+      CSS_INLINE -> (offsets, data): "replaces delimiters with a terminator": every field's bytes
+                    followed by the terminator; offsets[r] = start of field r (its terminator at
+                    offsets[r + 1] - 1)
+      CSS_VECTOR -> (offsets, data, aux): "its own auxiliary boolean vector that delimits the fields"
+                    (P:499): the ARROW bytes, aux = 1 at the last symbol of every non-empty field
+    Plain Python loops over the fields."""
+    offs, buf = strings(dialect, data, C, col, types)
+    R = len(offs) - 1
+    if mode == CSS_ARROW:
+        return offs, buf
+    if mode == CSS_INLINE:
+        out, o2 = bytearray(), [0]
+        for r in range(R):
+            out += buf[offs[r]:offs[r + 1]]
+            out.append(terminator)
+            o2.append(len(out))
+        return np.array(o2, np.int64), bytes(out)
+    aux = bytearray(len(buf))
+    for r in range(R):
+        if offs[r + 1] > offs[r]:
+            aux[offs[r + 1] - 1] = 1
+    return offs, buf, bytes(aux)
+
+
+def css_index(mode, buf: bytes, terminator=0x1F):
+    """The CSS index as P:497 / P:501-502 generate it: the positions of all terminators (CSS_INLINE) or of
+    the nonzero auxiliary entries (CSS_VECTOR), in order."""
+    if mode == CSS_INLINE:
+        return np.array([k for k, c in enumerate(buf) if c == terminator], np.int64)
+    return np.array([k for k, c in enumerate(buf) if c != 0], np.int64)
+
+
 def conv_timestamp(s: bytes):
     """R29: (ok, seconds since 1970-01-01T00:00:00Z) for ISO or CLF datetimes."""
     lib = _load()

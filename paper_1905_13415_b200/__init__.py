@@ -480,6 +480,94 @@ def strings(dfa: Dfa, data, column, rows: int, stream=None):
     return offs, buf[:int(total.value)]
 
 
+CSS_ARROW, CSS_INLINE, CSS_VECTOR = 0, 1, 2     # CSS layouts
+
+
+class Plan:
+    """A two-phase parse kept open (parpa_plan_create ... parpa_plan_destroy): ``emit(schema)`` writes the
+    columns; ``strings(column, rows, mode)`` materialises a string column from the plan's chunk masks
+    (parpa_plan_strings_size / _copy: no second scan half)."""
+
+    def __init__(self, dfa: Dfa, data, stream=None):
+        L = _lib.load()
+        _check_input(data)
+        self._data, self._stream = data, stream
+        self._plan = ctypes.c_void_p()
+        _check(L.parpa_plan_create(dfa.handle, ctypes.c_void_p(data.data_ptr()), data.numel(), _stream_handle(stream),
+                                   ctypes.byref(self._plan)), "parpa_plan_create")
+        R = ctypes.c_uint64()
+        _check(L.parpa_plan_records(self._plan, ctypes.byref(R)), "parpa_plan_records")
+        self.records = R.value
+
+    def emit(self, schema: Schema):
+        cols = alloc_columns(schema, self.records, self._data.device)
+        st = new_stats_tensor(self._data.device)
+        _check(_lib.load().parpa_plan_emit(self._plan, ctypes.byref(schema.struct()), _col_array(cols),
+                                           ctypes.c_void_p(st.data_ptr()), _stream_handle(self._stream)),
+               "parpa_plan_emit")
+        stats = stats_from_tensor(st)
+        n = stats["records"]
+        for c in cols:
+            c.offset, c.length = c.offset[:n], c.length[:n]
+            if c.value is not None:
+                c.value, c.valid = c.value[:n], c.valid[:n]
+        return ParseResult(cols, stats)
+
+    def strings(self, column, rows: int, mode: int = CSS_ARROW, terminator: int = 0x1F):
+        """(offsets int64[rows + 1], data uint8[total]) — plus aux uint8[total] for CSS_VECTOR."""
+        import torch
+        L = _lib.load()
+        dev = self._data.device
+        offs = torch.empty(int(rows) + 1, dtype=torch.int64, device=dev)
+        total = ctypes.c_uint64(0)
+        col = column.struct()
+        s = _stream_handle(self._stream)
+        _check(L.parpa_plan_strings_size(self._plan, ctypes.byref(col), int(rows), int(mode),
+                                         ctypes.c_void_p(offs.data_ptr()), ctypes.byref(total), s),
+               "parpa_plan_strings_size")
+        n = int(total.value)
+        buf = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        aux = torch.empty(max(n, 1), dtype=torch.uint8, device=dev) if mode == CSS_VECTOR else None
+        _check(L.parpa_plan_strings_copy(self._plan, ctypes.byref(col), int(rows), int(mode), int(terminator),
+                                         ctypes.c_void_p(offs.data_ptr()), ctypes.c_void_p(buf.data_ptr()),
+                                         ctypes.c_void_p(aux.data_ptr() if aux is not None else 0), s),
+               "parpa_plan_strings_copy")
+        return (offs, buf[:n]) if aux is None else (offs, buf[:n], aux[:n])
+
+    def close(self):
+        if self._plan:
+            _lib.load().parpa_plan_destroy(self._plan)
+            self._plan = ctypes.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def css_index(mode: int, buf, terminator: int = 0x1F, stream=None):
+    """The CSS index as the paper generates it (parpa_css_index): positions of the terminators in an
+    inline-terminated CSS (mode CSS_INLINE, buf = data) or of the nonzero entries of the auxiliary vector
+    (CSS_VECTOR, buf = aux).  Returns an int64 tensor on buf's device."""
+    import torch
+    L = _lib.load()
+    n = buf.numel()
+    idx = torch.empty(max(n, 1), dtype=torch.int64, device=buf.device)
+    cnt = ctypes.c_uint64(0)
+    p = ctypes.c_void_p(buf.data_ptr() if n else 0)
+    _check(L.parpa_css_index(int(mode), int(terminator), p if mode == CSS_INLINE else None,
+                             p if mode == CSS_VECTOR else None, n, ctypes.c_void_p(idx.data_ptr()), ctypes.byref(cnt),
+                             _stream_handle(stream)), "parpa_css_index")
+    return idx[:int(cnt.value)]
+
+
 STATE_UNKNOWN = 0xFFFFFFFF
 
 

@@ -56,7 +56,8 @@ EXPORTS = [
     "parpa_compose_counts", "parpa_parse_range", "parpa_range_begin", "parpa_range_count", "parpa_range_emit",
     "parpa_range_state_at", "parpa_range_emit_halo", "parpa_parse_into_skip",
     "parpa_compact_rows",
-    "parpa_strings_size", "parpa_strings_copy", "parpa_infer_columns", "parpa_infer_types",
+    "parpa_strings_size", "parpa_strings_copy", "parpa_plan_strings_size", "parpa_plan_strings_copy",
+    "parpa_css_index", "parpa_infer_columns", "parpa_infer_types",
     "parpa_debug_trace", "parpa_debug_masks", "parpa_chunk_bytes", "parpa_tile_bytes",
     "parpa_set_profiling", "parpa_last_kernel_times", "parpa_status_string", "parpa_version",
     "parpa_last_error",
@@ -108,6 +109,9 @@ def load(build_if_missing: bool = True):
         lib.parpa_infer_types.argtypes = [P, P, u64, u32, P, P, P, ctypes.POINTER(u64)]
         lib.parpa_strings_size.argtypes = [P, P, u64, ctypes.POINTER(Column_t), u64, P, ctypes.POINTER(u64), P]
         lib.parpa_strings_copy.argtypes = [P, P, u64, ctypes.POINTER(Column_t), u64, P, P, P]
+        lib.parpa_plan_strings_size.argtypes = [P, ctypes.POINTER(Column_t), u64, u32, P, ctypes.POINTER(u64), P]
+        lib.parpa_plan_strings_copy.argtypes = [P, ctypes.POINTER(Column_t), u64, u32, u32, P, P, P, P]
+        lib.parpa_css_index.argtypes = [u32, u32, P, P, u64, P, ctypes.POINTER(u64), P]
         lib.parpa_range_begin.argtypes = [P, P, u64, u64, P, pp, ctypes.POINTER(Tau_t)]
         lib.parpa_range_count.argtypes = [P, u32, ctypes.POINTER(Counts_t)]
         lib.parpa_range_emit.argtypes = [P, ctypes.POINTER(Schema_t), ctypes.POINTER(Context_t), P, u64,

@@ -1398,6 +1398,65 @@ int parpa_infer_types(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len
 }
 
 // ---- string materialisation ---------------------------------------------------------------
+// The CSS of one column (layouts P:493-502) from a completed scan half over the same bytes (a.masks).
+// Sizes (d_data null): per-row DATA counts (+1 per field for the inline terminator), exclusive scan -> d_offsets,
+// total.  Copy: the bytes, the terminators (INLINE) or the auxiliary vector (VECTOR).  Synchronous.
+static int strings_core(const KArgs &a, const parpa_column *col, uint64_t rows, uint32_t mode, uint32_t term,
+                        int64_t *d_offsets, uint64_t *total, uint8_t *d_data, uint8_t *d_aux, cudaStream_t s) {
+  DevCfg *dc = nullptr;
+  int rc = dev_cfg(&dc);
+  if (rc) return rc;
+  const unsigned long long *off = (const unsigned long long *)col->offset;
+  unsigned long long *v = (unsigned long long *)d_offsets;
+  if (!d_data) {
+    if (!rows) {
+      CK(cudaMemsetAsync(d_offsets, 0, 8, s));
+      CK(cudaStreamSynchronize(s));
+      if (total) *total = 0;
+      return PARPA_OK;
+    }
+    k_str_len<<<dc->sms * 8, 256, 0, s>>>(a, off, col->length, rows, v, mode == CSS_INLINE ? 1u : 0u);
+    CK(cudaGetLastError());
+    const uint64_t nb = (rows + SCAN_TILE - 1) / SCAN_TILE;
+    void *sb = nullptr;
+    const size_t o_agg = (16 + nb * 4 + 15) / 16 * 16;                  // 8-byte payloads stay aligned
+    const size_t bytes = o_agg + 2 * nb * 8;
+    CK(cudaMallocAsync(&sb, bytes, s));
+    if (cudaMemsetAsync(sb, 0, bytes, s) != cudaSuccess) rc = PARPA_ECUDA;
+    if (!rc) {
+      uint8_t *b = (uint8_t *)sb;
+      k_scan_u64<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(v, rows, (unsigned int *)b, (uint32_t *)(b + 16),
+                                                        (unsigned long long *)(b + o_agg),
+                                                        (unsigned long long *)(b + o_agg + nb * 8));
+      if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
+    }
+    cudaFreeAsync(sb, s);
+    if (!rc && total && cudaMemcpyAsync(total, v + rows, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = PARPA_ECUDA;
+    if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
+    return rc;
+  }
+  if (!rows) return PARPA_OK;
+  unsigned int *clash = nullptr;
+  CK(cudaMallocAsync(&clash, 4, s));
+  if (cudaMemsetAsync(clash, 0, 4, s) != cudaSuccess) rc = PARPA_ECUDA;
+  if (!rc && mode == CSS_VECTOR) {                                      // the auxiliary vector starts zeroed
+    uint64_t n = 0;
+    if (cudaMemcpyAsync(&n, v + rows, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+      rc = PARPA_ECUDA;
+    if (!rc && n && cudaMemsetAsync(d_aux, 0, n, s) != cudaSuccess) rc = PARPA_ECUDA;
+  }
+  if (!rc) {
+    k_str_copy<<<dc->sms * 8, 256, 0, s>>>(a, off, col->length, rows, v, d_data, mode, term, d_aux, clash);
+    if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
+  }
+  unsigned int h = 0;
+  if (!rc && (cudaMemcpyAsync(&h, clash, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess))
+    rc = PARPA_ECUDA;
+  cudaFreeAsync(clash, s);
+  if (!rc && h) rc = PARPA_EUNSUPPORTED;                                // the terminator occurs in the CSS
+  return rc;
+}
+
 static int strings_impl(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, const parpa_column *col,
                         uint64_t rows, int64_t *d_offsets, uint64_t *total, uint8_t *d_data, cudaStream_t s) {
   Work w;
@@ -1410,37 +1469,7 @@ static int strings_impl(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t l
   a.seed_dev = dfa->dmap[dfa->start];
   a.seed_exact = dfa->start;
   if (!rc) rc = launch_passes(MODE_COUNT, a, dfa->k, s, nullptr);       // the chunk masks
-  DevCfg *dc = nullptr;
-  if (!rc) rc = dev_cfg(&dc);
-  const unsigned long long *off = (const unsigned long long *)col->offset;
-  unsigned long long *v = (unsigned long long *)d_offsets;
-  if (!rc && rows) {
-    if (!d_data) {                                                      // sizes: per-row counts, scan
-      k_str_len<<<dc->sms * 8, 256, 0, s>>>(a, off, col->length, rows, v);
-      if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
-      const uint64_t nb = (rows + SCAN_TILE - 1) / SCAN_TILE;
-      void *sb = nullptr;
-      const size_t o_agg = (16 + nb * 4 + 15) / 16 * 16;                // 8-byte payloads stay aligned
-      const size_t bytes = o_agg + 2 * nb * 8;
-      if (!rc && cudaMallocAsync(&sb, bytes, s) != cudaSuccess) rc = PARPA_ENOMEM;
-      if (!rc && cudaMemsetAsync(sb, 0, bytes, s) != cudaSuccess) rc = PARPA_ECUDA;
-      if (!rc) {
-        uint8_t *b = (uint8_t *)sb;
-        k_scan_u64<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(v, rows, (unsigned int *)b, (uint32_t *)(b + 16),
-                                                          (unsigned long long *)(b + o_agg),
-                                                          (unsigned long long *)(b + o_agg + nb * 8));
-        if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
-      }
-      if (sb) cudaFreeAsync(sb, s);
-      if (!rc && total && cudaMemcpyAsync(total, v + rows, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) rc = PARPA_ECUDA;
-    } else {
-      k_str_copy<<<dc->sms * 8, 256, 0, s>>>(a, off, col->length, rows, v, d_data);
-      if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
-    }
-  } else if (!rc && !d_data) {
-    if (cudaMemsetAsync(d_offsets, 0, 8, s) != cudaSuccess) rc = PARPA_ECUDA;
-    if (total) *total = 0;
-  }
+  if (!rc) rc = strings_core(a, col, rows, CSS_ARROW, 0u, d_offsets, total, d_data, nullptr, s);
   work_free(w, s);
   if (!rc && cudaStreamSynchronize(s) != cudaSuccess) rc = PARPA_ECUDA;
   return rc;
@@ -1459,6 +1488,58 @@ int parpa_strings_copy(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t le
     return PARPA_EINVAL;
   return strings_impl(dfa, d_bytes, len, column, rows, const_cast<int64_t *>(d_offsets), nullptr, d_data,
                       (cudaStream_t)stream);
+}
+
+// ---- CSS from a plan (reuses the plan's chunk masks: no second scan half) -----------------------------
+int parpa_plan_strings_size(parpa_plan *plan, const parpa_column *column, uint64_t rows, uint32_t mode,
+                            int64_t *d_offsets, uint64_t *total, void *stream) {
+  if (!plan || !column || !d_offsets || !total || mode > CSS_VECTOR || (rows && (!column->offset || !column->length)))
+    return PARPA_EINVAL;
+  return strings_core(plan->a, column, rows, mode, 0u, d_offsets, total, nullptr, nullptr, (cudaStream_t)stream);
+}
+int parpa_plan_strings_copy(parpa_plan *plan, const parpa_column *column, uint64_t rows, uint32_t mode,
+                            uint32_t terminator, const int64_t *d_offsets, uint8_t *d_data, uint8_t *d_aux,
+                            void *stream) {
+  if (!plan || !column || !d_offsets || !d_data || mode > CSS_VECTOR || terminator > 255 ||
+      (mode == CSS_VECTOR && !d_aux) || (rows && (!column->offset || !column->length)))
+    return PARPA_EINVAL;
+  return strings_core(plan->a, column, rows, mode, terminator, const_cast<int64_t *>(d_offsets), nullptr, d_data,
+                      d_aux, (cudaStream_t)stream);
+}
+
+int parpa_css_index(uint32_t mode, uint32_t terminator, const uint8_t *d_data, const uint8_t *d_aux, uint64_t n,
+                    uint64_t *d_index, uint64_t *count, void *stream) {
+  if ((mode != CSS_INLINE && mode != CSS_VECTOR) || terminator > 255 || !count || (n && !d_index) ||
+      (n && mode == CSS_INLINE && !d_data) || (n && mode == CSS_VECTOR && !d_aux))
+    return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  *count = 0;
+  if (n == 0) return PARPA_OK;
+  DevCfg *dc;
+  int rc = dev_cfg(&dc);
+  if (rc) return rc;
+  const uint64_t nt = (n + WT - 1) / WT, nb = (nt + SCAN_TILE - 1) / SCAN_TILE;
+  const size_t o_scan = align_up((nt + 1) * 8), o_agg = (16 + nb * 4 + 15) / 16 * 16, scan_bytes = o_agg + 2 * nb * 8;
+  void *blk = nullptr;
+  CK(cudaMallocAsync(&blk, o_scan + scan_bytes, s));
+  uint8_t *b = (uint8_t *)blk;
+  unsigned long long *cnt = (unsigned long long *)b;
+  uint8_t *sc = b + o_scan;
+  if (cudaMemsetAsync(sc, 0, scan_bytes, s) != cudaSuccess) rc = PARPA_ECUDA;
+  const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)dc->sms * 8, (nt + 7) / 8);
+  if (!rc) {
+    k_css_count<<<grid, 256, 0, s>>>(mode, d_data, d_aux, terminator, n, cnt);
+    k_scan_u64<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(cnt, nt, (unsigned int *)sc, (uint32_t *)(sc + 16),
+                                                      (unsigned long long *)(sc + o_agg),
+                                                      (unsigned long long *)(sc + o_agg + nb * 8));
+    k_css_write<<<grid, 256, 0, s>>>(mode, d_data, d_aux, terminator, n, cnt, (unsigned long long *)d_index);
+    if (cudaGetLastError() != cudaSuccess) rc = PARPA_ECUDA;
+  }
+  if (!rc && (cudaMemcpyAsync(count, cnt + nt, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+              cudaStreamSynchronize(s) != cudaSuccess))
+    rc = PARPA_ECUDA;
+  cudaFreeAsync(blk, s);
+  return rc;
 }
 
 // ---- skipping rows (stream compaction) ---------------------------------------------------

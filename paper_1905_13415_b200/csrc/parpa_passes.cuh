@@ -428,12 +428,18 @@ __device__ unsigned long long data_bytes_in(const KArgs &a, unsigned long long p
   return cnt;
 }
 
+// CSS layouts: ARROW = the DATA bytes of every field concatenated (offsets index);
+// INLINE = each field followed by a terminator byte (inline-terminated CSS); VECTOR = ARROW bytes plus an
+// auxiliary byte vector, nonzero at the last symbol of every non-empty field (vector-delimited CSS).
+enum { CSS_ARROW = 0, CSS_INLINE = 1, CSS_VECTOR = 2 };
+
+// extra = 1 for the inline-terminated layout (one terminator per field, missing / empty fields included)
 __global__ void k_str_len(const KArgs a, const unsigned long long *off, const uint32_t *len, unsigned long long rows,
-                          unsigned long long *lens) {
+                          unsigned long long *lens, uint32_t extra) {
   for (unsigned long long r = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; r < rows;
        r += (unsigned long long)gridDim.x * blockDim.x) {
     const uint32_t L = len[r];
-    lens[r] = (L == MISSING_LEN_DEV || L == 0) ? 0ull : data_bytes_in(a, off[r] - a.base, L);
+    lens[r] = ((L == MISSING_LEN_DEV || L == 0) ? 0ull : data_bytes_in(a, off[r] - a.base, L)) + extra;
   }
 }
 
@@ -518,17 +524,25 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_u64(unsigned long long *v
   }
 }
 
-// one warp per row: copy the DATA bytes of the span to data[offsets[r] ...]
+// one warp per row: copy the DATA bytes of the span to data[offsets[r] ...]; INLINE: the terminator after
+// them (a DATA byte equal to the terminator sets *clash: the layout needs it absent); VECTOR:
+// aux (zeroed by the caller) gets a 1 at the field's last symbol
 __global__ void k_str_copy(const KArgs a, const unsigned long long *off, const uint32_t *len, unsigned long long rows,
-                           const unsigned long long *offsets, uint8_t *data) {
+                           const unsigned long long *offsets, uint8_t *data, uint32_t mode, uint32_t term,
+                           uint8_t *aux, unsigned int *clash) {
   const int lane = threadIdx.x & 31;
   const unsigned long long nw = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  const uint32_t extra = mode == CSS_INLINE ? 1u : 0u;
+  bool hit = false;
   for (unsigned long long r = blockIdx.x * (unsigned long long)(blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
        r += nw) {
     const uint32_t L = len[r];
-    if (L == MISSING_LEN_DEV || L == 0) continue;
-    const unsigned long long p0 = off[r] - a.base, o0 = offsets[r];
-    const bool all = offsets[r + 1] - o0 == L;                 // no control byte inside: plain copy
+    const unsigned long long o0 = offsets[r], n = offsets[r + 1] - o0 - extra;   // DATA bytes of the field
+    if (extra && lane == 0) data[o0 + n] = (uint8_t)term;
+    if (L == MISSING_LEN_DEV || L == 0 || n == 0) continue;
+    if (mode == CSS_VECTOR && lane == 0) aux[o0 + n - 1] = 1;
+    const unsigned long long p0 = off[r] - a.base;
+    const bool all = n == L;                                   // no control byte inside: plain copy
     unsigned long long o = o0;
     for (unsigned long long q = 0; q < L; q += 32) {
       const unsigned long long p = p0 + q + lane;
@@ -537,8 +551,47 @@ __global__ void k_str_copy(const KArgs a, const unsigned long long *off, const u
       bool keep = in;
       if (!all && in) keep = (dmask_of_chunk(a, p >> 6) >> (p & 63)) & 1ull;
       const unsigned m = __ballot_sync(0xffffffffu, keep);
-      if (keep) data[o + __popc(m & ((1u << lane) - 1u))] = c;
+      if (keep) {
+        data[o + __popc(m & ((1u << lane) - 1u))] = c;
+        hit |= extra && c == (uint8_t)term;
+      }
       o += __popc(m);
+    }
+  }
+  if (hit) atomicOr(clash, 1u);
+}
+
+// ---- CSS index generation: the positions of the terminators (INLINE: data[k] == term) or of the
+// nonzero auxiliary entries (VECTOR), in order.  Per 2 KB tile a count, an exclusive scan, then the writes.
+__device__ __forceinline__ bool css_mark(uint32_t mode, const uint8_t *data, const uint8_t *aux, uint32_t term,
+                                         unsigned long long k) {
+  return mode == CSS_INLINE ? data[k] == (uint8_t)term : aux[k] != 0;
+}
+__global__ void k_css_count(uint32_t mode, const uint8_t *data, const uint8_t *aux, uint32_t term, unsigned long long n,
+                            unsigned long long *cnt) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long ntile = (n + WT - 1) / WT;
+  for (unsigned long long t = blockIdx.x * (unsigned long long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < ntile;
+       t += (unsigned long long)gridDim.x * (blockDim.x >> 5)) {
+    uint32_t c = 0;
+    for (unsigned long long k = t * WT + lane; k < min(n, (t + 1) * WT); k += 32) c += css_mark(mode, data, aux, term, k);
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) cnt[t] = c;
+  }
+}
+__global__ void k_css_write(uint32_t mode, const uint8_t *data, const uint8_t *aux, uint32_t term, unsigned long long n,
+                            const unsigned long long *base, unsigned long long *idx) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long ntile = (n + WT - 1) / WT;
+  for (unsigned long long t = blockIdx.x * (unsigned long long)(blockDim.x >> 5) + (threadIdx.x >> 5); t < ntile;
+       t += (unsigned long long)gridDim.x * (blockDim.x >> 5)) {
+    unsigned long long o = base[t];
+    for (unsigned long long k0 = t * WT; k0 < min(n, (t + 1) * WT); k0 += 32) {
+      const unsigned long long k = k0 + lane;
+      const bool m = k < n && css_mark(mode, data, aux, term, k);
+      const unsigned b = __ballot_sync(0xffffffffu, m);
+      if (m) idx[o + __popc(b & ((1u << lane) - 1u))] = k;
+      o += __popc(b);
     }
   }
 }

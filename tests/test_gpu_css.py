@@ -1,0 +1,70 @@
+"""GPU: string materialisation from a plan (the chunk masks reused) in the paper's three CSS layouts
+ and the CSS index generation, element by element against the oracle."""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+import paper_1905_13415_b200 as parpa  # noqa: E402
+
+
+def dev(data):
+    a = np.frombuffer(bytes(data), np.uint8)
+    t = torch.empty(max(a.size, 1), dtype=torch.uint8, device="cuda")
+    if a.size:
+        t[:a.size].copy_(torch.from_numpy(a.copy()))
+    return t[:a.size]
+
+
+@pytest.mark.parametrize("name,cols,nbytes", [("cfg1", [0, 3, 5, 7], 1_500_000), ("yelp", [0, 7, 8], 6_000_000),
+                                              ("clf", [2, 3, 4], 4_000_000), ("taxi", [1, 6], 3_000_000)])
+def test_plan_css_layouts(name, cols, nbytes):
+    w = datagen.WORKLOADS[name]
+    data, g = datagen.generate(name, nbytes)
+    d = dev(data)
+    with parpa.Plan(parpa.Dfa.dialect(w.dialect), d) as plan:
+        res = plan.emit(parpa.Schema(list(w.types)))
+        R = res.records
+        assert R == g.records
+        for c in cols:
+            for mode in (parpa.CSS_ARROW, parpa.CSS_INLINE, parpa.CSS_VECTOR):
+                want = oracle.css(w.dialect, data, w.C, c, list(w.types), mode=mode, terminator=0x1F)
+                got = plan.strings(res.columns[c], R, mode=mode, terminator=0x1F)
+                assert np.array_equal(got[0].cpu().numpy(), want[0]), (name, c, mode)
+                assert bytes(got[1].cpu().numpy()) == want[1], (name, c, mode)
+                if mode == parpa.CSS_VECTOR:
+                    assert bytes(got[2].cpu().numpy()) == want[2], (name, c)
+                if mode != parpa.CSS_ARROW:
+                    buf = got[1] if mode == parpa.CSS_INLINE else got[2]
+                    idx = parpa.css_index(mode, buf, 0x1F).cpu().numpy()
+                    ref = oracle.css_index(mode, want[1] if mode == parpa.CSS_INLINE else want[2], 0x1F)
+                    assert np.array_equal(idx, ref), (name, c, mode)
+
+
+def test_plan_strings_equal_one_shot_strings():
+    """the plan path (masks reused) and the one-shot parpa_strings_* path (scan re-run) agree"""
+    w = datagen.WORKLOADS["yelp"]
+    data, _ = datagen.generate("yelp", 3_000_000)
+    d = dev(data)
+    dfa = parpa.Dfa.dialect("csv")
+    with parpa.Plan(dfa, d) as plan:
+        res = plan.emit(parpa.Schema(list(w.types)))
+        for c in (0, 7):
+            o1, b1 = plan.strings(res.columns[c], res.records)
+            o2, b2 = parpa.strings(dfa, d, res.columns[c], res.records)
+            assert torch.equal(o1, o2) and torch.equal(b1, b2)
+
+
+def test_inline_terminator_clash_reported():
+    """the inline-terminated layout needs a terminator absent from the CSS"""
+    data = b"a,b\nx\x1fy,z\n" * 100
+    d = dev(data)
+    with parpa.Plan(parpa.Dfa.dialect("csv"), d) as plan:
+        res = plan.emit(parpa.Schema([oracle.SPAN, oracle.SPAN]))
+        with pytest.raises(parpa.ParpaError):
+            plan.strings(res.columns[0], res.records, mode=parpa.CSS_INLINE, terminator=0x1F)
+        offs, buf = plan.strings(res.columns[0], res.records, mode=parpa.CSS_INLINE, terminator=0x1E)
+        assert bytes(buf.cpu().numpy()) == b"a\x1ex\x1fy\x1e" * 100
