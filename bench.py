@@ -405,9 +405,14 @@ def run_config(args, config, ctx, main=True):
         gs = torch.cuda.Stream()
         gs.wait_stream(stream)
         graph = torch.cuda.CUDAGraph()
+        # a caller-owned workspace (parpa_parse_into_ws): the graph is the parse kernel(s) alone, no
+        # allocation / memset nodes
+        ws = parpa.Workspace(d.numel(), stream=gs)
         with torch.cuda.stream(gs):
+            parpa.parse_into(dfa, schema, d, cols, cap, st, stream=gs, workspace=ws)
+            torch.cuda.synchronize()
             with torch.cuda.graph(graph, stream=gs):
-                per_step = parpa.parse_into(dfa, schema, d, cols, cap, st, stream=gs)
+                per_step = parpa.parse_into(dfa, schema, d, cols, cap, st, stream=gs, workspace=ws)
         torch.cuda.synchronize()
         for _ in range(args.warmup):
             graph.replay()
@@ -501,7 +506,7 @@ def run_config(args, config, ctx, main=True):
                               "range_begin + allgather(tau) + range_count + allgather(counts) + range_emit",
                       "l2": "input >> 126 MB L2 (no flush needed)" if n > (512 << 20) else
                             "input < L2: outputs and inputs stay L2-resident between steps (latency-bound size)",
-                      "launch": "CUDA graph replay per step" if use_graph else "eager",
+                      "launch": "CUDA graph replay per step (parse_into with a caller workspace)" if use_graph else "eager",
                       "generate_s": round(t_gen, 1),
                       "kernel_ms": {k: round(statistics.mean(v), 4) for k, v in per_kernel.items()},
                       "kernel_ms_source": "separate profiled steps after the timed region"},

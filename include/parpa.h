@@ -146,10 +146,23 @@ int parpa_parse(const parpa_dfa *dfa, const parpa_schema *schema, const uint8_t 
 /* Accessors of a parpa_result (host-side handles; column pointers are device memory owned by the
  * result and freed by parpa_result_free). */
 int parpa_result_stats(const parpa_result *res, parpa_stats *out);
+/* the same, field by field: the record count; the status with the first invalid byte offset
+ * and the missing-record / extra-field counts (each out-pointer but `status` may be NULL) */
+int parpa_result_records(const parpa_result *res, uint64_t *records);
+int parpa_result_status(const parpa_result *res, int *status, uint64_t *first_invalid, uint64_t *n_missing_records,
+                        uint64_t *n_extra_fields);
 int parpa_result_column(const parpa_result *res, uint32_t c, parpa_column *out);
 /* copy column c (records rows) into caller device columns `dst` on `stream` (asynchronous) */
 int parpa_result_copy_column(const parpa_result *res, uint32_t c, const parpa_column *dst, void *stream);
 void parpa_result_free(parpa_result *res);
+/* Allocator hook for result-owned buffers (SURVEY §8(b) ownership): alloc(bytes, stream, ctx) returns device
+ * memory usable on `stream` (NULL = out of memory -> PARPA_ENOMEM); free(ptr, stream, ctx) releases it.  Both
+ * NULL restores the default (cudaMallocAsync / cudaFreeAsync on the parse's stream).  A result keeps the
+ * allocator it was created with; the hook is process-wide (mutex-protected).  PARPA_EINVAL if exactly one is
+ * NULL.  Workspaces are internal and always stream-ordered cudaMallocAsync. */
+typedef void *(*parpa_alloc_fn)(size_t bytes, void *stream, void *ctx);
+typedef void (*parpa_free_fn)(void *ptr, void *stream, void *ctx);
+int parpa_set_allocator(parpa_alloc_fn alloc, parpa_free_fn free_fn, void *ctx);
 
 /* ---- two-phase parse into caller-owned columns ---------------------------------------- *
  * parpa_plan_create — run the scan kernel over the input and keep its per-tile prefixes
@@ -290,6 +303,21 @@ int parpa_plan_strings_copy(parpa_plan *plan, const parpa_column *column, uint64
                             void *stream);
 int parpa_css_index(uint32_t mode, uint32_t terminator, const uint8_t *d_data, const uint8_t *d_aux, uint64_t n,
                     uint64_t *d_index, uint64_t *count, void *stream);
+
+/* ---- caller-owned workspace (latency: no allocation, memset or host sync per parse) ------------ *
+ * parpa_workspace_create allocates (stream-ordered on `stream`) the device workspace of parses of up to max_len
+ * bytes (about 0.45 * max_len bytes) and zeroes its control words.  parpa_parse_into_ws is parpa_parse_into
+ * using it: nothing is allocated or synchronised, so a CUDA graph of it is a single kernel node for inputs up
+ * to 2 MB (the cooperative k_small leaves the control words zeroed for the next parse; larger inputs add one
+ * memset).  One parse at a time per workspace (stream order).  d_bytes must be 16-byte aligned.  Errors:
+ * PARPA_EINVAL (len > max_len, misaligned input, null pointers), else as parpa_parse_into.
+ * parpa_workspace_destroy frees it (synchronous). */
+typedef struct parpa_workspace parpa_workspace;
+int parpa_workspace_create(uint64_t max_len, void *stream, parpa_workspace **out);
+void parpa_workspace_destroy(parpa_workspace *ws);
+int parpa_parse_into_ws(parpa_workspace *ws, const parpa_dfa *dfa, const parpa_schema *schema, const uint8_t *d_bytes,
+                        uint64_t len, const parpa_column *columns, uint64_t capacity, parpa_stats *d_stats,
+                        void *stream, uint32_t *gpu_launches);
 
 /* ---- staged range plan: the same exchange with every pass run once per rank ------------- *
  * parpa_range_begin  runs S1-S3 on the device range [d_bytes, d_bytes+len) at global offset

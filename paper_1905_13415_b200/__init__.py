@@ -223,16 +223,45 @@ def parse(dfa: Dfa, schema: Schema, data, stream=None) -> ParseResult:
     return ParseResult(cols, stats)
 
 
+class Workspace:
+    """A reusable parse workspace (parpa_workspace_create): parse_into(..., workspace=ws) then allocates,
+    zeroes and synchronises nothing (one kernel for inputs up to 2 MB; CUDA-graph friendly)."""
+
+    def __init__(self, max_len: int, stream=None):
+        L = _lib.load()
+        self._ws = ctypes.c_void_p()
+        _check(L.parpa_workspace_create(int(max_len), _stream_handle(stream), ctypes.byref(self._ws)),
+               "parpa_workspace_create")
+        self.max_len = int(max_len)
+
+    def close(self):
+        if self._ws:
+            _lib.load().parpa_workspace_destroy(self._ws)
+            self._ws = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def parse_into(dfa: Dfa, schema: Schema, data, columns, capacity: int, stats_tensor, stream=None,
-               skip_records=None) -> int:
+               skip_records=None, workspace: "Workspace" = None) -> int:
     """Parse into caller columns without a host round trip (parpa_parse_into).  Asynchronous; returns the
     number of kernels launched.  skip_records: a sorted device int64 tensor of record indices not to write
-    (parpa_parse_into_skip)."""
+    (parpa_parse_into_skip).  workspace: a Workspace (parpa_parse_into_ws: no allocation or memset)."""
     L = _lib.load()
     _check_input(data)
     sch = schema.struct()
     arr = _col_array(columns)
     n = ctypes.c_uint32(0)
+    if workspace is not None:
+        assert skip_records is None, "skip_records is not combined with a workspace"
+        _check(L.parpa_parse_into_ws(workspace._ws, dfa.handle, ctypes.byref(sch), ctypes.c_void_p(data.data_ptr()),
+                                     data.numel(), arr, int(capacity), ctypes.c_void_p(stats_tensor.data_ptr()),
+                                     _stream_handle(stream), ctypes.byref(n)), "parpa_parse_into_ws")
+        return n.value
     if skip_records is not None and skip_records.numel():
         _check(L.parpa_parse_into_skip(dfa.handle, ctypes.byref(sch), ctypes.c_void_p(data.data_ptr()), data.numel(),
                                        ctypes.c_void_p(skip_records.data_ptr()), skip_records.numel(), arr,
@@ -478,6 +507,35 @@ def strings(dfa: Dfa, data, column, rows: int, stream=None):
                                 int(rows), ctypes.c_void_p(offs.data_ptr()), ctypes.c_void_p(buf.data_ptr()),
                                 _stream_handle(stream)), "parpa_strings_copy")
     return offs, buf[:int(total.value)]
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+_ALLOC_KEEP = []
+
+
+def use_torch_allocator(enable: bool = True):
+    """Route result-owned buffers (parpa_parse / parse_c_owned) through torch's caching allocator
+    (parpa_set_allocator); enable=False restores the library default (cudaMallocAsync)."""
+    import torch
+    L = _lib.load()
+    if not enable:
+        _check(L.parpa_set_allocator(None, None, None), "parpa_set_allocator")
+        return
+
+    def _alloc(n, stream, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(n), stream=int(stream or 0))
+        except Exception:
+            return None
+
+    def _free(ptr, stream, ctx):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    fa, ff = _ALLOC_FN(_alloc), _FREE_FN(_free)
+    _ALLOC_KEEP[:] = [fa, ff]                      # the C side keeps raw pointers to these thunks
+    _check(L.parpa_set_allocator(ctypes.cast(fa, ctypes.c_void_p), ctypes.cast(ff, ctypes.c_void_p), None),
+           "parpa_set_allocator")
 
 
 CSS_ARROW, CSS_INLINE, CSS_VECTOR = 0, 1, 2     # CSS layouts (P:439-457, P:493-502)

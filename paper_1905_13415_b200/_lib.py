@@ -51,6 +51,8 @@ _lib = None
 
 EXPORTS = [
     "parpa_create_dfa", "parpa_destroy_dfa", "parpa_parse", "parpa_result_stats", "parpa_result_column",
+    "parpa_result_records", "parpa_result_status", "parpa_set_allocator",
+    "parpa_workspace_create", "parpa_workspace_destroy", "parpa_parse_into_ws",
     "parpa_result_copy_column", "parpa_result_free", "parpa_plan_create", "parpa_plan_records", "parpa_plan_emit", "parpa_plan_destroy",
     "parpa_parse_into", "parpa_parse_host", "parpa_summarize", "parpa_count", "parpa_compose_tau",
     "parpa_compose_counts", "parpa_parse_range", "parpa_range_begin", "parpa_range_count", "parpa_range_emit",
@@ -87,6 +89,15 @@ def load(build_if_missing: bool = True):
         lib.parpa_destroy_dfa.restype = None
         lib.parpa_parse.argtypes = [P, ctypes.POINTER(Schema_t), P, u64, P, pp]
         lib.parpa_result_stats.argtypes = [P, ctypes.POINTER(Stats_t)]
+        lib.parpa_result_records.argtypes = [P, ctypes.POINTER(u64)]
+        lib.parpa_result_status.argtypes = [P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(u64), ctypes.POINTER(u64),
+                                            ctypes.POINTER(u64)]
+        lib.parpa_set_allocator.argtypes = [P, P, P]
+        lib.parpa_workspace_create.argtypes = [u64, P, pp]
+        lib.parpa_workspace_destroy.argtypes = [P]
+        lib.parpa_workspace_destroy.restype = None
+        lib.parpa_parse_into_ws.argtypes = [P, P, ctypes.POINTER(Schema_t), P, u64, ctypes.POINTER(Column_t), u64, P, P,
+                                            ctypes.POINTER(u32)]
         lib.parpa_result_column.argtypes = [P, u32, ctypes.POINTER(Column_t)]
         lib.parpa_result_copy_column.argtypes = [P, u32, ctypes.POINTER(Column_t), P]
         lib.parpa_result_free.argtypes = [P]

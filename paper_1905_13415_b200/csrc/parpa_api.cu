@@ -341,6 +341,15 @@ cudaError_t launch_coop(void (*k)(P...), unsigned grid, unsigned block, size_t s
   return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
 }
 
+// The DFA as the LUT-building kernels see it: the prebuilt image only on the device it lives on.
+const DfaK &dfa_for_device(const DfaK &k, DfaK &tmp) {
+  int dev = -1;
+  if (!k.img || (cudaGetDevice(&dev) == cudaSuccess && dev == k.img_dev)) return k;
+  tmp = k;
+  tmp.img = nullptr;
+  return tmp;
+}
+
 int grid_for(int occ, int sms, uint32_t ntiles, int warps_per_cta) {
   long long g = (long long)std::max(occ, 1) * sms;
   long long need = ((long long)ntiles + warps_per_cta - 1) / warps_per_cta;
@@ -350,8 +359,10 @@ int grid_for(int occ, int sms, uint32_t ntiles, int warps_per_cta) {
 // S1-S3: pass 1 and the τ scan (unseeded); S4-S5: pass 2 (seeded by a.seed_dev) and the
 // record/column scan (unseeded; a.seed is applied by k_emit / k_finalize).
 int launch_half2(const KArgs &a, const DfaK &k, cudaStream_t s, uint32_t *launches);
-int launch_passes(int mode, const KArgs &a, const DfaK &k, cudaStream_t s, uint32_t *launches) {
+int launch_passes(int mode, const KArgs &a, const DfaK &k0, cudaStream_t s, uint32_t *launches) {
   if (a.ntiles == 0) return PARPA_OK;
+  DfaK tmp;
+  const DfaK &k = dfa_for_device(k0, tmp);
   DevCfg *dc;
   int rc = dev_cfg(&dc);
   if (rc) return rc;
@@ -370,8 +381,10 @@ int launch_passes(int mode, const KArgs &a, const DfaK &k, cudaStream_t s, uint3
   return mode == MODE_TAU ? PARPA_OK : launch_half2(a, k, s, launches);
 }
 
-int launch_half2(const KArgs &a, const DfaK &k, cudaStream_t s, uint32_t *launches) {
+int launch_half2(const KArgs &a, const DfaK &k0, cudaStream_t s, uint32_t *launches) {
   if (a.ntiles == 0) return PARPA_OK;
+  DfaK tmp;
+  const DfaK &k = dfa_for_device(k0, tmp);
   DevCfg *dc;
   int rc = dev_cfg(&dc);
   if (rc) return rc;
@@ -427,7 +440,9 @@ bool use_small(const KArgs &a) {
   if (dev_cfg(&dc)) return false;
   return dc->occ_small >= 1;
 }
-int launch_small(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, uint32_t *launches) {
+int launch_small(const KArgs &a, const DfaK &k0, const ColsK &ck, cudaStream_t s, uint32_t *launches) {
+  DfaK tmp;
+  const DfaK &k = dfa_for_device(k0, tmp);
   DevCfg *dc;
   int rc0 = dev_cfg(&dc);
   if (rc0) return rc0;
@@ -552,10 +567,25 @@ struct parpa_plan {
   cudaStream_t s;
 };
 
+// Allocator of result-owned buffers (parpa_set_allocator; default stream-ordered cudaMallocAsync / cudaFreeAsync).
+struct Allocator {
+  parpa_alloc_fn alloc = nullptr;
+  parpa_free_fn free = nullptr;
+  void *ctx = nullptr;
+};
+static std::mutex g_alloc_mu;
+static Allocator g_alloc;
+static Allocator current_allocator() {
+  std::lock_guard<std::mutex> g(g_alloc_mu);
+  return g_alloc;
+}
+
 struct parpa_result {
   uint32_t C;
   std::vector<parpa_column> cols;
   std::vector<void *> allocs;
+  Allocator al;                       // the allocator the buffers came from (freed with its free)
+  cudaStream_t s = nullptr;
   parpa_stats stats;
 };
 
@@ -595,6 +625,40 @@ const char *parpa_status_string(int st) {
   case PARPA_ENEEDMORE: return "output capacity too small";
   default: return "unknown status";
   }
+}
+
+// The shared-memory LUT images of a DFA (the layouts build_lut / build_lut_step_dp write), in device memory of
+// the current device: the pass kernels and k_small copy them instead of building entry by entry.
+static void make_lut_image(parpa_dfa *d) {
+  int dev = -1, n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0 || cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  const bool ns4 = d->k.nlive <= 4;
+  std::vector<uint32_t> h((LUT_BYTES + 256 * STEP_ROW_DP) / 4);
+  for (int b = 0; b < 256; b++)
+    for (int half = 0; half < 2; half++)
+      for (int slot = 0; slot < 16; slot++) {
+        const size_t o = ((size_t)b * 256 + half * 128 + slot * 8) / 4;
+        h[o] = half ? d->k.lut[b][2] : d->k.lut[b][0];
+        h[o + 1] = half ? (ns4 ? d->k.lut[b][2] : d->k.lut[b][3]) : (ns4 ? d->k.lut[b][0] : d->k.lut[b][1]);
+      }
+  for (int b = 0; b < 256; b++)
+    for (int slot = 0; slot < 16; slot++) {
+      const size_t o = (LUT_BYTES + (size_t)b * STEP_ROW_DP + slot * 8) / 4;
+      h[o] = d->k.lut[b][2];
+      h[o + 1] = ns4 ? d->k.lut[b][2] : d->k.lut[b][3];
+    }
+  void *p = nullptr;
+  if (cudaMalloc(&p, h.size() * 4) != cudaSuccess) { cudaGetLastError(); return; }
+  if (cudaMemcpy(p, h.data(), h.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(p);
+    return;
+  }
+  d->k.img = (const uint4 *)p;
+  d->k.img_dev = dev;
 }
 
 int parpa_create_dfa(uint32_t S, uint32_t start, uint32_t inv, uint32_t G, const uint8_t *gob,
@@ -669,11 +733,18 @@ int parpa_create_dfa(uint32_t S, uint32_t start, uint32_t inv, uint32_t G, const
     d->k.lut[b][2] = step[0] | (step[1] << 8) | (step[2] << 16) | ((uint32_t)step[3] << 24);
     d->k.lut[b][3] = step[4] | (step[5] << 8) | (step[6] << 16) | ((uint32_t)step[7] << 24);
   }
+  d->k.img = nullptr;
+  d->k.img_dev = -1;
+  make_lut_image(d);                                     // (no device: the kernels build the LUTs themselves)
   *out = d;
   return PARPA_OK;
 }
 
-void parpa_destroy_dfa(parpa_dfa *d) { delete d; }
+void parpa_destroy_dfa(parpa_dfa *d) {
+  if (!d) return;
+  if (d->k.img) cudaFree((void *)d->k.img);
+  delete d;
+}
 
 int parpa_set_profiling(int enable) {
   prof_clear();
@@ -799,11 +870,15 @@ int parpa_parse(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_
   r->C = C;
   r->cols.resize(C);
   uint64_t R = std::max<uint64_t>(p->records, 1);
+  r->al = current_allocator();
+  r->s = s;
   for (uint32_t c = 0; c < C; c++) {
     uint8_t type = sch->types ? sch->types[c] : PARPA_SPAN;
     void *a = nullptr;
     size_t per = 8 + 4 + (type != PARPA_SPAN ? 9 : 0);
-    if (cudaMallocAsync(&a, R * per + 64, s) != cudaSuccess) { rc = PARPA_ENOMEM; break; }
+    if (r->al.alloc) a = r->al.alloc(R * per + 64, stream, r->al.ctx);
+    else if (cudaMallocAsync(&a, R * per + 64, s) != cudaSuccess) a = nullptr;
+    if (!a) { rc = PARPA_ENOMEM; break; }
     r->allocs.push_back(a);
     uint8_t *b = (uint8_t *)a;
     r->cols[c].offset = (uint64_t *)b;
@@ -830,6 +905,20 @@ int parpa_result_stats(const parpa_result *r, parpa_stats *out) {
   *out = r->stats;
   return PARPA_OK;
 }
+int parpa_result_records(const parpa_result *r, uint64_t *records) {
+  if (!r || !records) return PARPA_EINVAL;
+  *records = r->stats.records;
+  return PARPA_OK;
+}
+int parpa_result_status(const parpa_result *r, int *status, uint64_t *first_invalid, uint64_t *n_missing_records,
+                        uint64_t *n_extra_fields) {
+  if (!r || !status) return PARPA_EINVAL;
+  *status = r->stats.status;
+  if (first_invalid) *first_invalid = r->stats.first_invalid;
+  if (n_missing_records) *n_missing_records = r->stats.missing_records;
+  if (n_extra_fields) *n_extra_fields = r->stats.extra_fields;
+  return PARPA_OK;
+}
 int parpa_result_column(const parpa_result *r, uint32_t c, parpa_column *out) {
   if (!r || !out || c >= r->C) return PARPA_EINVAL;
   *out = r->cols[c];
@@ -850,8 +939,21 @@ int parpa_result_copy_column(const parpa_result *r, uint32_t c, const parpa_colu
 
 void parpa_result_free(parpa_result *r) {
   if (!r) return;
-  for (void *a : r->allocs) cudaFree(a);
+  for (void *a : r->allocs) {
+    if (r->al.free) r->al.free(a, (void *)r->s, r->al.ctx);
+    else cudaFreeAsync(a, r->s);
+  }
+  if (!r->al.free && !r->allocs.empty()) cudaStreamSynchronize(r->s);
   delete r;
+}
+
+int parpa_set_allocator(parpa_alloc_fn alloc, parpa_free_fn free_fn, void *ctx) {
+  if ((alloc == nullptr) != (free_fn == nullptr)) return PARPA_EINVAL;
+  std::lock_guard<std::mutex> g(g_alloc_mu);
+  g_alloc.alloc = alloc;
+  g_alloc.free = free_fn;
+  g_alloc.ctx = ctx;
+  return PARPA_OK;
 }
 
 // ---- single-pass capacity path ------------------------------------------------------------------
@@ -908,6 +1010,70 @@ int parpa_parse_into(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_
   if (!dfa) return PARPA_EINVAL;
   return parse_into_impl(dfa, sch, d_bytes, len, cols, cap, d_stats, (cudaStream_t)stream,
                          dfa->start, seg_identity(), 0, nullptr, 0, 1, gpu_launches);
+}
+
+// ---- caller-owned workspace: parse_into without allocation, memset or host synchronisation --------------
+struct parpa_workspace {
+  Work w;
+  uint64_t max_len = 0;
+  size_t zero_bytes = 0;                // the look-back descriptors + control words (zeroed before a staged parse)
+  bool clean = true;                    // control words zero (k_small leaves them so; the staged kernels do not)
+};
+
+int parpa_workspace_create(uint64_t max_len, void *stream, parpa_workspace **out) {
+  if (!out) return PARPA_EINVAL;
+  parpa_workspace *ws = new (std::nothrow) parpa_workspace;
+  if (!ws) return PARPA_ENOMEM;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = work_alloc(ws->w, std::max<uint64_t>(max_len, 1), 0, false, s);
+  if (rc) { delete ws; return rc; }
+  ws->max_len = max_len;
+  ws->zero_bytes = (size_t)((uint8_t *)ws->w.lex - (uint8_t *)ws->w.block);
+  *out = ws;
+  return PARPA_OK;
+}
+
+void parpa_workspace_destroy(parpa_workspace *ws) {
+  if (!ws) return;
+  if (ws->w.block) cudaFree(ws->w.block);
+  delete ws;
+}
+
+int parpa_parse_into_ws(parpa_workspace *ws, const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_bytes,
+                        uint64_t len, const parpa_column *cols, uint64_t cap, parpa_stats *d_stats, void *stream,
+                        uint32_t *gpu_launches) {
+  if (!ws || !dfa || !sch || !d_stats || (len && !d_bytes) || (sch->num_columns && !cols) || len > ws->max_len ||
+      (len && misaligned(d_bytes)))
+    return PARPA_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  ColsK ck;
+  int rc = set_columns(sch, cols, sch->num_columns, ck);
+  if (rc) return rc;
+  prof_begin();
+  KArgs a;
+  make_args(a, ws->w, d_bytes, len);
+  a.ntiles = (uint32_t)((len + WT - 1) / WT);
+  a.C = sch->num_columns;
+  a.strict = sch->strict;
+  a.cap = cap;
+  a.stats = (Stats *)d_stats;
+  a.seed_dev = dfa->dmap[dfa->start];
+  a.seed_exact = dfa->start;
+  uint32_t n = 0;
+  if (use_small(a)) {
+    if (!ws->clean) CK(cudaMemsetAsync(ws->w.block, 0, ws->zero_bytes, s));
+    rc = launch_small(a, dfa->k, ck, s, &n);
+    ws->clean = true;
+  } else {
+    CK(cudaMemsetAsync(ws->w.block, 0, ws->zero_bytes, s));
+    rc = launch_passes(MODE_COUNT, a, dfa->k, s, &n);
+    if (!rc) rc = launch_emit(a, dfa->k, ck, s, &n);
+    if (!rc) rc = launch_tail(a, dfa->k, ck, s, &n);
+    ws->clean = false;
+  }
+  if (gpu_launches) *gpu_launches = n;
+  prof_end();
+  return rc;
 }
 
 int parpa_parse_into_skip(const parpa_dfa *dfa, const parpa_schema *sch, const uint8_t *d_bytes, uint64_t len,

@@ -61,6 +61,8 @@ struct DfaK {                       // compiled DFA, passed by value (kernel par
   uint8_t next_exact[16][16];       // [device state][group] -> exact DFA state after the byte
   uint8_t eoi_state[16];            // EOI action by DFA state
   uint32_t nlive, merged, inv_state, pad;   // device states in use; 1 if some class has > 1 member
+  const uint4 *img;                 // prebuilt shared-memory LUT images in device memory (on device img_dev), or
+  int img_dev, pad2;                // null: [PRMT layout LUT_BYTES][DP4A step layout 32 KB] (see build_lut)
 };
 
 struct ColDesc {
@@ -97,7 +99,7 @@ struct Ctrl {
   unsigned int deferred_done;        // k_deferred blocks finished (the last one settles the status)
   unsigned int emit_ticket;          // k_emit: next warp tile to take (reset by the last warp out)
   unsigned int emit_done;            // k_emit: warps finished
-  unsigned int pad0;
+  unsigned int last_cls;             // 0x100 | device class before the range's last byte (pass 2), 0 = unknown
 };
 
 struct TileInfo {
@@ -185,7 +187,14 @@ __device__ __forceinline__ uint32_t lut_addr(uint32_t v, uint32_t k, uint32_t lb
   return prmt(v, lbase, 0x5604u | (k << 4));
 }
 constexpr uint32_t STEP_ROW_DP = 128;
+// With a prebuilt image (DfaK::img) the LUTs are plain coalesced 16-byte copies from L2 instead of per-entry
+// constant-bank reads (which serialise over the warp's distinct addresses).
 __device__ __forceinline__ void build_lut_step_dp(uint8_t *lut, const DfaK &d) {    // DP4A layout
+  if (d.img) {
+    const uint4 *src = d.img + LUT_BYTES / 16;
+    for (int i = threadIdx.x; i < 256 * STEP_ROW_DP / 16; i += blockDim.x) reinterpret_cast<uint4 *>(lut)[i] = __ldg(src + i);
+    return;
+  }
   const bool ns4 = d.nlive <= 4;
   for (int i = threadIdx.x; i < 256 * 16; i += blockDim.x) {
     const int b = i >> 4, slot = i & 15;
@@ -193,6 +202,10 @@ __device__ __forceinline__ void build_lut_step_dp(uint8_t *lut, const DfaK &d) {
   }
 }
 __device__ __forceinline__ void build_lut(uint8_t *lut, const DfaK &d) {
+  if (d.img) {
+    for (int i = threadIdx.x; i < LUT_BYTES / 16; i += blockDim.x) reinterpret_cast<uint4 *>(lut)[i] = __ldg(d.img + i);
+    return;
+  }
   for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
     int b = i >> 5, half = (i >> 4) & 1, slot = i & 15;
     // (at most four device states: the τ half holds sel_lo in 32 four-byte slots, one per lane, so the
@@ -237,8 +250,9 @@ __device__ __forceinline__ uint32_t gather4(uint32_t x, uint32_t bitmask, uint32
 template <bool FULL, bool NS4 = false, bool DP = false>
 __device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_t (&v)[16], int nvalid, uint32_t entry,
                                                 unsigned long long &Dm, unsigned long long &Fm,
-                                                unsigned long long &Rm) {
+                                                unsigned long long &Rm, uint32_t &xprev) {
   uint32_t x = 0x80u | entry;
+  xprev = x;
   uint32_t g4[2] = {0, 0}, g5[2] = {0, 0};                // kind-code bits 4 / 5 of every byte
 #pragma unroll
   for (int w = 0; w < 16; w++) {
@@ -247,6 +261,7 @@ __device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_
     for (int k = 0; k < 4; k++) {
       int i = 4 * w + k;
       if (FULL || i < nvalid) {
+        if (FULL ? i == CHUNK - 1 : i == nvalid - 1) xprev = x;   // the class before the chunk's last byte
         const uint32_t ad = lut_addr<DP>(v[w], (uint32_t)k, laneaddr) + (DP ? 0u : 128u);
         if (NS4) {
           const uint32_t st = lds_u1(ad);
@@ -285,8 +300,9 @@ __device__ __forceinline__ uint32_t plane_bits(uint32_t w) {   // (w >> 4 | 5) &
 template <bool FULL, bool NS4 = false, bool DP = false>
 __device__ __forceinline__ uint32_t chunk_masks_t(uint32_t laneaddr, const uint32_t (&v)[16], int nvalid, uint32_t entry,
                                                   unsigned long long &Dm, unsigned long long &Fm,
-                                                  unsigned long long &Rm) {
+                                                  unsigned long long &Rm, uint32_t &xprev) {
   uint32_t x = 0x80u | entry;
+  xprev = x;
   uint32_t g4[2], g5[2];
 #pragma unroll
   for (int h = 0; h < 2; h++) {
@@ -298,6 +314,7 @@ __device__ __forceinline__ uint32_t chunk_masks_t(uint32_t laneaddr, const uint3
       const int i = 32 * h + j, p = j >> 3, sidx = j & 7;
       uint32_t r = 0xFFu;                                    // outside the chunk: not data / delimiter
       if (FULL || i < nvalid) {
+        if (FULL ? i == CHUNK - 1 : i == nvalid - 1) xprev = x;   // the class before the chunk's last byte
         const uint32_t ad = lut_addr<DP>(v[i >> 2], (uint32_t)(i & 3), laneaddr) + (DP ? 0u : 128u);
         if (NS4) {
           const uint32_t st = lds_u1(ad);
@@ -764,7 +781,11 @@ struct alignas(16) WarpScratch {
 #define PARPA_E2_ROWS_MIN 16
 #endif
 constexpr uint32_t E2_ROWS_MIN = PARPA_E2_ROWS_MIN;  // tiles with at least this many rows: column-uniform E2
+constexpr int E2_ROWS_MIN_MAX = 16;
+static_assert(E2_ROWS_MIN <= E2_ROWS_MIN_MAX, "c_rcp16 covers nrows < 16");
 constexpr uint32_t E1A_SELECT_MAX = 32;              // tiles with at most this many delimiters: one select round
+__constant__ uint32_t c_rcp16[E2_ROWS_MIN_MAX] = {0u, 65537u, 32769u, 21846u, 16385u, 13108u, 10923u, 9363u, 8193u,
+                                                   7282u, 6554u, 5958u, 5462u, 5042u, 4682u, 4370u};   // 65536/d + 1
 constexpr uint32_t FIELD_WRITTEN = 0xFFFFFFFFu;   // E1 already wrote this field
 constexpr uint32_t FIELD_FAR = 0xFFFFFFFEu;       // field 0 began before the tile: see WarpScratch::f0
 
@@ -1212,8 +1233,10 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   // columns share one converter, so mixed int / float steps do not diverge.
   const uint32_t total = a.C * nrows;
   const uint32_t it0 = (uint32_t)lane + 32u * (NP == 1 ? 0u : part), step = 32u * NP;
-  uint32_t c = it0 / nrows, jr = it0 - c * nrows;            // nrows >= 1 here
-  const uint32_t dc = step / nrows, djr = step - dc * nrows;
+  // division by nrows (1..15 here) as a multiply by a 16-bit reciprocal: exact for numerators < 4096
+  const uint32_t rcp = c_rcp16[nrows];
+  uint32_t c = (it0 * rcp) >> 16, jr = it0 - c * nrows;
+  const uint32_t dc = (step * rcp) >> 16, djr = step - dc * nrows;
   for (uint32_t it = it0; it < total; it += step) {
     const uint32_t ci = c, ji = jr;
     jr += djr;
@@ -1372,6 +1395,9 @@ __device__ void finalize_one(const KArgs &a, const DfaK &dfa, const ColsK &colsk
   uint32_t fin_exact = dfa.hmap[fin];
   if (a.len == 0) {
     fin_exact = a.seed_exact;
+  } else if (dfa.merged && (ld_volatile_u32(&a.ctrl->last_cls) & 0x100u)) {   // recorded by pass 2
+    const uint32_t cb = ld_volatile_u32(&a.ctrl->last_cls) & 0xFu;
+    fin_exact = cb == INV_DEV ? dfa.inv_state : dfa.next_exact[cb][dfa.gob[a.in[a.len - 1]]];
   } else if (dfa.merged) {
     const unsigned long long kc = (a.len - 1) / CHUNK;
     uint32_t x = 0x80u | a.chunk_state[kc];

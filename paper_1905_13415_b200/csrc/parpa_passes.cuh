@@ -261,19 +261,20 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, con
     const uint32_t entry = nib_at(a.lex[(unsigned long long)t * 32 + lane], nib_at(a.wpre[t], a.seed_dev));
     a.chunk_state[(unsigned long long)t * 32 + lane] = (uint8_t)entry;
     unsigned long long Dm, Fm, Rm;
-    uint32_t fin;
+    uint32_t fin, xprev;
     if (dfa.nlive <= 4) {
       const uint32_t la4 = lbase - ps.laneoff + (uint32_t)lane * 4u;   // one 4-byte slot per lane
-      if (nv == CHUNK) fin = CHUNK_MASKS<true, true, true>(la4, v, nv, entry, Dm, Fm, Rm);
-      else fin = CHUNK_MASKS<false, true, true>(la4, v, nv, entry, Dm, Fm, Rm);
+      if (nv == CHUNK) fin = CHUNK_MASKS<true, true, true>(la4, v, nv, entry, Dm, Fm, Rm, xprev);
+      else fin = CHUNK_MASKS<false, true, true>(la4, v, nv, entry, Dm, Fm, Rm, xprev);
     } else {
-      if (nv == CHUNK) fin = CHUNK_MASKS<true, false, true>(lbase, v, nv, entry, Dm, Fm, Rm);
-      else fin = CHUNK_MASKS<false, false, true>(lbase, v, nv, entry, Dm, Fm, Rm);
+      if (nv == CHUNK) fin = CHUNK_MASKS<true, false, true>(lbase, v, nv, entry, Dm, Fm, Rm, xprev);
+      else fin = CHUNK_MASKS<false, false, true>(lbase, v, nv, entry, Dm, Fm, Rm, xprev);
     }
     if (fin == INV_DEV && entry != INV_DEV && nv > 0) {
       int p = first_inv_in_chunk(ps.lut, a.in + cstart, nv, ps.laneoff, entry, STEP_ROW_DP);
       if (p >= 0) atomicMax(&a.ctrl->inv_neg, ~(a.base + cstart + (unsigned)p));
     }
+    if (nv > 0 && cstart + (unsigned)nv == a.len) a.ctrl->last_cls = 0x100u | (xprev & 0xFu);   // for the EOI action
     unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;   // for k_emit
     mk[0] = Dm;
     mk[32] = Fm;

@@ -151,19 +151,20 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 1) k_small(const __grid_cons
     const uint32_t entry = nib_at(__ldcg(a.lex + (unsigned long long)t * 32 + lane), nib_at(s_pre[t], a.seed_dev));
     a.chunk_state[(unsigned long long)t * 32 + lane] = (uint8_t)entry;
     unsigned long long Dm, Fm, Rm;
-    uint32_t fin;
+    uint32_t fin, xprev;
     if (dfa.nlive <= 4) {
       const uint32_t la4 = laneaddr - laneoff + (uint32_t)lane * 4u;   // one 4-byte slot per lane
-      if (nv == CHUNK) fin = chunk_masks<true, true>(la4, v, nv, entry, Dm, Fm, Rm);
-      else fin = chunk_masks<false, true>(la4, v, nv, entry, Dm, Fm, Rm);
+      if (nv == CHUNK) fin = chunk_masks<true, true>(la4, v, nv, entry, Dm, Fm, Rm, xprev);
+      else fin = chunk_masks<false, true>(la4, v, nv, entry, Dm, Fm, Rm, xprev);
     } else {
-      if (nv == CHUNK) fin = chunk_masks<true>(laneaddr, v, nv, entry, Dm, Fm, Rm);
-      else fin = chunk_masks<false>(laneaddr, v, nv, entry, Dm, Fm, Rm);
+      if (nv == CHUNK) fin = chunk_masks<true>(laneaddr, v, nv, entry, Dm, Fm, Rm, xprev);
+      else fin = chunk_masks<false>(laneaddr, v, nv, entry, Dm, Fm, Rm, xprev);
     }
     if (fin == INV_DEV && entry != INV_DEV && nv > 0) {
       const int p = first_inv_in_chunk(lut + 128, a.in + cstart, nv, laneoff, entry);
       if (p >= 0) atomicMax(&a.ctrl->inv_neg, ~(a.base + cstart + (unsigned)p));
     }
+    if (nv > 0 && cstart + (unsigned)nv == a.len) a.ctrl->last_cls = 0x100u | (xprev & 0xFu);   // for the EOI action
     unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;
     mk[0] = Dm;
     mk[32] = Fm;
@@ -260,10 +261,14 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 1) k_small(const __grid_cons
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(&a.ctrl->deferred_done, 1u) + 1u == gridDim.x && a.stats &&
-        *reinterpret_cast<volatile unsigned int *>(&a.ctrl->unsupported) &&
-        *reinterpret_cast<volatile int *>(&a.stats->status) != ST_EFORMAT)
-      a.stats->status = ST_EUNSUPPORTED;
+    if (atomicAdd(&a.ctrl->deferred_done, 1u) + 1u == gridDim.x) {   // the last block out
+      if (a.stats && *reinterpret_cast<volatile unsigned int *>(&a.ctrl->unsupported) &&
+          *reinterpret_cast<volatile int *>(&a.stats->status) != ST_EFORMAT)
+        a.stats->status = ST_EUNSUPPORTED;
+      // leave the control words zeroed: a reused workspace (parpa_parse_into_ws) needs no memset per parse
+      volatile unsigned int *c = reinterpret_cast<volatile unsigned int *>(a.ctrl);
+      for (int i = 0; i < (int)(sizeof(Ctrl) / 4); i++) c[i] = 0u;
+    }
   }
   SMALL_MARK(12);
 }

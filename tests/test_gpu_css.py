@@ -68,3 +68,36 @@ def test_inline_terminator_clash_reported():
             plan.strings(res.columns[0], res.records, mode=parpa.CSS_INLINE, terminator=0x1F)
         offs, buf = plan.strings(res.columns[0], res.records, mode=parpa.CSS_INLINE, terminator=0x1E)
         assert bytes(buf.cpu().numpy()) == b"a\x1ex\x1fy\x1e" * 100
+
+
+def test_result_accessors_and_allocator_hook():
+    """parpa_result_records / parpa_result_status, and result buffers from a caller-set
+    allocator (torch's caching allocator through parpa_set_allocator)"""
+    import ctypes
+    from paper_1905_13415_b200 import _lib
+    w = datagen.WORKLOADS["cfg1"]
+    data, g = datagen.generate("cfg1", 500_000)
+    d = dev(data)
+    dfa = parpa.Dfa.dialect("csv")
+    schema = parpa.Schema(list(w.types))
+    ora = oracle.parse("csv", data, w.C, list(w.types))
+    before = torch.cuda.memory_allocated()
+    parpa.use_torch_allocator(True)
+    try:
+        res = parpa.parse_c_owned(dfa, schema, d)
+        assert res.records == ora.R
+        assert np.array_equal(res.columns[1].value.cpu().numpy().view(np.int64)[:ora.R], ora.value[1])
+        L = _lib.load()
+        r = ctypes.c_void_p()
+        sch = schema.struct()
+        assert L.parpa_parse(dfa.handle, ctypes.byref(sch), ctypes.c_void_p(d.data_ptr()), d.numel(), None,
+                             ctypes.byref(r)) == 0
+        assert torch.cuda.memory_allocated() > before            # the buffers came from torch
+        R, st, fi, nm, ne = ctypes.c_uint64(), ctypes.c_int(), ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        assert L.parpa_result_records(r, ctypes.byref(R)) == 0 and R.value == ora.R
+        assert L.parpa_result_status(r, ctypes.byref(st), ctypes.byref(fi), ctypes.byref(nm), ctypes.byref(ne)) == 0
+        assert st.value == 0 and nm.value == ora.n_missing and ne.value == ora.n_extra
+        L.parpa_result_free(r)
+        torch.cuda.synchronize()
+    finally:
+        parpa.use_torch_allocator(False)
