@@ -301,3 +301,20 @@ __device__ void collab_device_tier(const KArgs &a, const ColsK &colsk, CollabSme
   }
 }
 
+
+// After the thread tier (which routes the long fields): a grid barrier, then the block tier and, if any field
+// is huge, the device tier.  Entered by every thread of every CTA; the decision reads n_defer, which is final
+// before the tiers start (every CTA sees the same value), so either all CTAs meet the barriers or none does.
+template <bool TS>
+__device__ __forceinline__ void collab_tiers(const KArgs &a, const ColsK &colsk, CollabSmem &sm) {
+  if (!a.lq || ld_volatile_u32(&a.ctrl->n_defer) == 0u) return;
+  __threadfence();
+  cooperative_groups::this_grid().sync();          // the queues are complete
+  collab_block_tier<TS>(a, colsk, sm);
+  if (ld_volatile_u32(&a.ctrl->n_huge)) collab_device_tier<TS>(a, colsk, sm);
+}
+// (the last CTA out) the block- / device-tier counts into the stats
+__device__ __forceinline__ void collab_stats(const KArgs &a) {
+  a.stats->block_fields = a.lq ? min(ld_volatile_u32(&a.ctrl->n_long), a.lq_cap) : 0u;
+  a.stats->device_fields = a.lq ? min(ld_volatile_u32(&a.ctrl->n_huge), a.hq_cap) : 0u;
+}

@@ -611,7 +611,6 @@ constexpr uint8_t VALID_REDO = 0xFF, VALID_REDO_IC = 0xFE;
 #include "parpa_collab.cuh"
 __device__ __forceinline__ void push_defer(const KArgs &a, const ColDesc *cd, unsigned long long fd,
                                            unsigned long long ld, unsigned long long row, uint32_t c, uint32_t ic) {
-  if (!ic && push_collab(a, cd, fd, ld, row, c)) return;   // long numeric fields: block / device tier
   uint32_t idx = atomicAdd(&a.ctrl->n_defer, 1u);
   if (idx < a.dq_cap) {
     cd->valid[row] = 0;              // k_deferred's overflow sweep must only see markers of this launch
@@ -1438,9 +1437,9 @@ __device__ void finalize_one(const KArgs &a, const DfaK &dfa, const ColsK &colsk
     a.stats->first_invalid = first_inv;
     a.stats->missing_records = missing;
     a.stats->extra_fields = extra;
-    a.stats->block_fields = a.lq ? min(ld_volatile_u32(&a.ctrl->n_long), a.lq_cap) : 0u;
-    a.stats->device_fields = a.lq ? min(ld_volatile_u32(&a.ctrl->n_huge), a.hq_cap) : 0u;
-    a.stats->deferred_fields = (unsigned long long)n_defer + a.stats->block_fields + a.stats->device_fields;
+    a.stats->deferred_fields = n_defer;              // (of which the block / device tiers: set by k_deferred)
+    a.stats->block_fields = 0u;
+    a.stats->device_fields = 0u;
     a.stats->status = status;
     a.stats->final_state = fin_exact;
   }
@@ -1523,6 +1522,9 @@ __device__ __forceinline__ void deferred_all(const KArgs &a, const DfaK &dfa, co
   unsigned int n = min(a.ctrl->n_defer, a.dq_cap);
   for (unsigned long long i = tid; i < n; i += nth) {
     const DeferItem it = a.dq[i];
+    // long numeric fields without inner control bytes: queued for the block / device tier (the emission
+    // kernels only test the length; the routing lives here, out of their code)
+    if (!it.ic && push_collab(a, colsk.c + it.col, it.fd, it.ld, it.row, it.col)) continue;
     convert_deferred<TS>(a, dfa, colsk.c + it.col, it.fd, it.ld, it.row, it.ic);
   }
   if (a.ctrl->defer_overflow) {                     // the queue was full: convert the marked rows
@@ -1533,8 +1535,9 @@ __device__ __forceinline__ void deferred_all(const KArgs &a, const DfaK &dfa, co
       for (unsigned long long r = tid; r < R; r += nth) {
         const uint8_t m = cd->valid[r];
         if (m == VALID_REDO || m == VALID_REDO_IC) {
-          const unsigned long long fd = cd->off[r];
-          convert_deferred<TS>(a, dfa, cd, fd, fd + cd->len[r] - 1, r, m == VALID_REDO_IC ? 1u : 0u);
+          const unsigned long long fd = cd->off[r], ld = fd + cd->len[r] - 1;
+          if (m == VALID_REDO && push_collab(a, cd, fd, ld, r, c)) continue;
+          convert_deferred<TS>(a, dfa, cd, fd, ld, r, m == VALID_REDO_IC ? 1u : 0u);
         }
       }
     }
@@ -1549,16 +1552,17 @@ __global__ void k_deferred(const __grid_constant__ KArgs a, const __grid_constan
   const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
   deferred_all<TS>(a, dfa, colsk, tid, nth);
   __shared__ CollabSmem s_collab;                  // long numeric fields: block tier, then device tier
-  collab_block_tier<TS>(a, colsk, s_collab);
-  if (a.lq && ld_volatile_u32(&a.ctrl->n_huge)) collab_device_tier<TS>(a, colsk, s_collab);   // (cooperative launch)
+  collab_tiers<TS>(a, colsk, s_collab);            // (cooperative launch)
   // the last block to finish settles the status (every block's conversions are done by then)
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     // (modulo the grid: a plan emitted more than once keeps counting)
-    if ((atomicAdd(&a.ctrl->deferred_done, 1u) + 1u) % gridDim.x == 0u && a.stats &&
-        *reinterpret_cast<volatile unsigned int *>(&a.ctrl->unsupported) && a.stats->status != ST_EFORMAT)
-      a.stats->status = ST_EUNSUPPORTED;             // k_finalize's order: EFORMAT > EUNSUPPORTED > the rest
+    if ((atomicAdd(&a.ctrl->deferred_done, 1u) + 1u) % gridDim.x == 0u && a.stats) {
+      collab_stats(a);
+      if (*reinterpret_cast<volatile unsigned int *>(&a.ctrl->unsupported) && a.stats->status != ST_EFORMAT)
+        a.stats->status = ST_EUNSUPPORTED;           // k_finalize's order: EFORMAT > EUNSUPPORTED > the rest
+    }
   }
 }
 

@@ -249,19 +249,19 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 1) k_small(const __grid_cons
   // only after a queue overflow), and the status the last block to finish settles ----
   if (blockIdx.x == 0 && threadIdx.x == 0) finalize_one(a, dfa, colsk);
   SMALL_MARK(10);
-  if (a.ctrl->defer_overflow) grid.sync();             // the overflow sweep reads stats->records
+  grid.sync();           // the end-of-input field may have been queued; the sweep reads stats->records
   SMALL_MARK(11);
   deferred_all<TS>(a, dfa, colsk, (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
                    (unsigned long long)gridDim.x * blockDim.x);
   {
     __shared__ CollabSmem s_collab;                // long numeric fields: block tier, then device tier
-    collab_block_tier<TS>(a, colsk, s_collab);
-    if (a.lq && ld_volatile_u32(&a.ctrl->n_huge)) collab_device_tier<TS>(a, colsk, s_collab);
+    collab_tiers<TS>(a, colsk, s_collab);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&a.ctrl->deferred_done, 1u) + 1u == gridDim.x) {   // the last block out
+      if (a.stats) collab_stats(a);
       if (a.stats && *reinterpret_cast<volatile unsigned int *>(&a.ctrl->unsupported) &&
           *reinterpret_cast<volatile int *>(&a.stats->status) != ST_EFORMAT)
         a.stats->status = ST_EUNSUPPORTED;
