@@ -241,3 +241,31 @@ def test_virtual_ranks_exact_halo_long_and_inner_control_fields(seed):
         if t != oracle.SPAN:
             assert np.array_equal(ok, ora.valid[c]), c
             assert np.array_equal(val, ora.value[c]), c
+
+
+@pytest.mark.parametrize("big", [3000, 300_000])
+def test_virtual_ranks_collab_numbers_across_cuts(big):
+    """Long raw numbers (block tier >= 1 KB, device tier >= 256 KB) cut by a range boundary:
+    the owner reads the leading digits from the exact halo; values and validity equal the oracle's."""
+    rng = random.Random(big)
+    rows = [f"{i},{i}.25,r\n" for i in range(2000)]
+    z = "0" * big
+    nums = [("i", z + "77"), ("f", "1" * big + "." + "25"), ("f", "0." + z + "5e" + str(big + 3)),
+            ("i", "9" * big), ("f", z + "x")]
+    pos = sorted(rng.sample(range(50, 1950), len(nums)))
+    for (kind, s), p in zip(nums, pos):
+        rows[p] = f"{s},0.5,i\n" if kind == "i" else f"4,{s},f\n"
+    data = "".join(rows).encode()
+    types = [oracle.INT64, oracle.FLOAT64, oracle.SPAN]
+    ora = oracle.parse("csv", data, 3, types)
+    starts = [data.index(s.encode()) for _, s in nums]
+    inner = sorted(set(s0 + len(nums[k][1]) // 2 for k, s0 in enumerate(starts)))
+    cuts = [0] + inner + [len(data)]
+    cols = sharded_parse("csv", data, types, cuts, staged=True, halo=True)
+    for c, t in enumerate(types):
+        off, ln, val, ok = cols[c]
+        assert np.array_equal(off, ora.offset[c]), c
+        assert np.array_equal(ln, ora.length[c]), c
+        if t != oracle.SPAN:
+            assert np.array_equal(ok, ora.valid[c]), c
+            assert np.array_equal(val, ora.value[c]), c
