@@ -78,7 +78,9 @@ typedef struct parpa_result parpa_result;
  *   emit            host uint8[G][S] row per group: emission kind of the symbol, by SOURCE state
  *   eoi             host uint8[S]: end-of-input action of each final state
  * On success *out owns a heap object; free it with parpa_destroy_dfa.  Validation failures
- * return PARPA_EINVAL (SPEC S:32-36 invariants).  Synchronous, no device work. */
+ * return PARPA_EINVAL (SPEC S:32-36 invariants).  Synchronous.  When a device is present the DFA's two
+ * shared-memory LUT images (96 KB) are also placed in the current device's memory (the kernels copy them
+ * instead of building them; on another device, or without one, the kernels build them). */
 int parpa_create_dfa(uint32_t num_states, uint32_t start_state, uint32_t invalid_state,
                      uint32_t num_groups, const uint8_t *group_of_byte, const uint8_t *transition,
                      const uint8_t *emit, const uint8_t *eoi, parpa_dfa **out);
@@ -170,7 +172,8 @@ int parpa_set_allocator(parpa_alloc_fn alloc, parpa_free_fn free_fn, void *ctx);
  * parpa_plan_records — the number of rows the emit phase will produce.
  * parpa_plan_emit — run emit + finalize + deferred conversion into caller columns (each with
  * room for parpa_plan_records rows); d_stats (device pointer to a parpa_stats, may be NULL) is
- * written on the stream.  Asynchronous.  The input must still be valid. */
+ * written on the stream.  Asynchronous.  The input must still be valid.  The plan refers to `dfa`: the DFA
+ * must outlive it (destroy the plan first). */
 int parpa_plan_create(const parpa_dfa *dfa, const uint8_t *d_bytes, uint64_t len, void *stream,
                       parpa_plan **out);
 int parpa_plan_records(const parpa_plan *plan, uint64_t *records);

@@ -550,6 +550,7 @@ class Plan:
         L = _lib.load()
         _check_input(data)
         self._data, self._stream = data, stream
+        self._dfa = dfa                                  # the plan's kernels read the DFA: keep it alive
         self._plan = ctypes.c_void_p()
         _check(L.parpa_plan_create(dfa.handle, ctypes.c_void_p(data.data_ptr()), data.numel(), _stream_handle(stream),
                                    ctypes.byref(self._plan)), "parpa_plan_create")

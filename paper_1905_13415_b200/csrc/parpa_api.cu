@@ -49,7 +49,7 @@ int cuda_status(cudaError_t e) {
 struct DevCfg {
   bool init = false;
   int sms = 0;
-  int occ_pass1 = 0, occ_pass2 = 0, occ_emit = 0, occ_small = 0;
+  int occ_pass1 = 0, occ_pass2 = 0, occ_emit = 0, occ_sparse = 0, occ_small = 0;
 };
 std::mutex g_mu;
 DevCfg g_dev[64];
@@ -68,9 +68,14 @@ int dev_cfg(DevCfg **out) {
     CK(cudaFuncSetAttribute(k_emit<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
     CK(cudaFuncSetAttribute(k_emit<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
     CK(cudaFuncSetAttribute(k_emit<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
+    CK(cudaFuncSetAttribute(k_emit_sparse<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
+    CK(cudaFuncSetAttribute(k_emit_sparse<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
+    CK(cudaFuncSetAttribute(k_emit_sparse<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
+    CK(cudaFuncSetAttribute(k_emit_sparse<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass1, k_pass1, PASS_WARPS * 32, PASS_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass2, k_pass2, PASS_WARPS * 32, PASS_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit<false, false>, EMIT_WARPS * 32, EMIT_SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_sparse, k_emit_sparse<false, false>, EMIT_WARPS * 32, EMIT_SMEM));
     CK(cudaFuncSetAttribute(k_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMALL_SMEM));
     CK(cudaFuncSetAttribute(k_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMALL_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_small, k_small<false>, SMALL_WARPS * 32, SMALL_SMEM));
@@ -264,6 +269,8 @@ void make_args(KArgs &a, const Work &w, const uint8_t *in, uint64_t len) {
   a.hacc = w.hacc;
   a.lq_cap = w.lq_cap;
   a.hq_cap = w.hq_cap;
+  const char *ek = getenv("PARPA_EMIT_K");                   // A/B and tests: force the emission unit
+  a.emit_k = ek ? (uint32_t)atoi(ek) : 0u;
   a.is_last = 1;
   a.cap = 0;
   a.left_state = 0xFFu;                                     // no halo state known
@@ -424,7 +431,24 @@ int launch_emit(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, 
     else CK(launch_k(k_emit<false, false>, g, EMIT_WARPS * 32, EMIT_SMEM, s, true, a, ck));
   }
   CK(cudaGetLastError());
-  if (launches) (*launches)++;
+  {
+    // sparse ranges (>= 32 bytes per field): super tiles; k_emit above returned at once for them, this one
+    // returns at once for the others (both read the range's field count on the device)
+    Launch L(s, "k_emit_sparse");
+    const int g = grid_for(dc->occ_sparse, dc->sms, (a.ntiles + SPARSE_K - 1) / SPARSE_K, EMIT_WARPS);
+    const bool ts = has_timestamps(a, ck), sk = a.nskip > 0;
+#ifdef PARPA_SPARSE_NOPDL
+    const bool pdl = false;
+#else
+    const bool pdl = true;
+#endif
+    if (ts && sk) CK(launch_k(k_emit_sparse<true, true>, g, EMIT_WARPS * 32, EMIT_SMEM, s, pdl, a, ck));
+    else if (ts) CK(launch_k(k_emit_sparse<true, false>, g, EMIT_WARPS * 32, EMIT_SMEM, s, pdl, a, ck));
+    else if (sk) CK(launch_k(k_emit_sparse<false, true>, g, EMIT_WARPS * 32, EMIT_SMEM, s, pdl, a, ck));
+    else CK(launch_k(k_emit_sparse<false, false>, g, EMIT_WARPS * 32, EMIT_SMEM, s, pdl, a, ck));
+  }
+  CK(cudaGetLastError());
+  if (launches) *launches += 2;
   return PARPA_OK;
 }
 
@@ -629,9 +653,18 @@ const char *parpa_status_string(int st) {
 
 // The shared-memory LUT images of a DFA (the layouts build_lut / build_lut_step_dp write), in device memory of
 // the current device: the pass kernels and k_small copy them instead of building entry by entry.
+static bool have_device() {                              // probed once (no device: no runtime re-probing per DFA)
+  static const bool yes = [] {
+    int n = 0;
+    const bool ok = cudaGetDeviceCount(&n) == cudaSuccess && n > 0;
+    cudaGetLastError();
+    return ok;
+  }();
+  return yes;
+}
 static void make_lut_image(parpa_dfa *d) {
-  int dev = -1, n = 0;
-  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0 || cudaGetDevice(&dev) != cudaSuccess) {
+  int dev = -1;
+  if (!have_device() || cudaGetDevice(&dev) != cudaSuccess) {
     cudaGetLastError();
     return;
   }

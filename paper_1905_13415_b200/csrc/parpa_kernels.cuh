@@ -150,6 +150,7 @@ struct KArgs {
   Ctrl *ctrl;
   DeferItem *dq;
   uint32_t dq_cap, strict;
+  uint32_t emit_k, pad_ek;           // k_emit unit: 0 = by field density, 1 = warp tiles, SPARSE_K = super tiles
   unsigned long long *lq, *hq;       // block- / device-tier queues: row | column << 56 (parpa_collab.cuh)
   CollabAcc *hacc;                   // [hq_cap] device-tier accumulators
   uint32_t lq_cap, hq_cap;
@@ -294,8 +295,8 @@ __device__ __forceinline__ uint32_t chunk_masks(uint32_t laneaddr, const uint32_
 // pipe as multiplies), instead of a 4-byte pack plus a multiply-gather per 4 bytes.
 template <int SH>
 __device__ __forceinline__ uint32_t plane_bits(uint32_t w) {   // (w >> 4 | 5) & 0x01010101, moved up by s
-  if (SH >= 0) return w * (1u << SH);                          // IMAD.SHL (FMA pipe)
-  return __umulhi(w, 1u << (32 + SH));                         // w >> -SH (FMA pipe)
+  if constexpr (SH >= 0) return w * (1u << SH);                // IMAD.SHL (FMA pipe)
+  else return __umulhi(w, 1u << (32 + SH));                    // w >> -SH (FMA pipe)
 }
 template <bool FULL, bool NS4 = false, bool DP = false>
 __device__ __forceinline__ uint32_t chunk_masks_t(uint32_t laneaddr, const uint32_t (&v)[16], int nvalid, uint32_t entry,
@@ -766,15 +767,34 @@ __device__ __forceinline__ void flush_counters(const KArgs &a, EmitCounters &cnt
 //     "partition by column, then convert per column" at warp-tile granularity.
 constexpr int FCAP = 512;                   // fields per warp tile handled by E1/E2
 constexpr int RCAP = 128;                   // records per warp tile handled by E1/E2
-struct alignas(16) WarpScratch {
-  uint32_t bytes[WT / 4 + 8];               // the tile (plain layout) + a tail pad for 16-byte windows
-  uint32_t fields[FCAP];                    // tile offset (11 bits) | length << 11 (12 bits) | IC << 31
-  uint2 f0;                                 // field 0 when it starts before the tile: {rel, len | IC << 31}
+// K = warp tiles per emission unit: 1 (the tile's bytes staged in shared memory), or SPARSE_K for inputs
+// with few fields per byte (a super tile of K consecutive warp tiles per warp: the per-tile work — delimiter
+// list, field-0 carry, E2 set-up — is paid once per K tiles, and the few typed fields read their bytes from
+// global memory instead of a staged copy).
+template <int K>
+struct alignas(16) WarpScratchT {
+  uint32_t bytes[K == 1 ? WT / 4 + 8 : 4];  // the tile (plain layout) + a tail pad for 16-byte windows (K = 1)
+  uint32_t fields[FCAP];                    // unit offset | length << POS_BITS | IC << 31
+  uint2 f0;                                 // field 0 when it starts before the unit: {rel, len | IC << 31}
   uint32_t rows[RCAP];                      // end field index (low 16) | record delimiter position (high 16)
-  uint16_t dlist[FCAP];                     // delimiter positions (tile-local) | record bit << 15
-  uint32_t dmask[WT / 32], kmask[WT / 32];  // DATA / CTRL bits of the tile, 32 per word
-  uint16_t kpre[WT / 32];                   // CTRL bits before each word
+  uint16_t dlist[FCAP];                     // delimiter positions (unit-local) | record bit << 15
+  uint32_t dmask[WT * K / 32], kmask[WT * K / 32];  // DATA / CTRL bits of the unit, 32 per word
+  uint16_t kpre[WT * K / 32];               // CTRL bits before each word
   uint32_t e1_nf, e1_nrec, e1_plain;        // E1 -> E2 when several warps share a tile (k_small)
+};
+using WarpScratch = WarpScratchT<1>;
+#ifndef PARPA_SPARSE_K
+#define PARPA_SPARSE_K 4
+#endif
+constexpr int SPARSE_K = PARPA_SPARSE_K;    // super tiles of SPARSE_K * 2 KB
+template <int K> struct UnitBits {          // unit-local positions: POS_BITS bits; field lengths: LEN_MASK
+  static constexpr uint32_t POS_BITS = K == 1 ? 11u : K == 2 ? 12u : 13u;
+  static constexpr uint32_t POS_MASK = (1u << POS_BITS) - 1u;
+  static constexpr uint32_t LEN_MASK = K == 1 ? 0xFFFu : (1u << (31u - POS_BITS)) - 1u;
+};
+static_assert(SPARSE_K == 2 || SPARSE_K == 4, "UnitBits covers K = 1, 2, 4");
+template <int K> struct Masks {             // a lane's K chunks (chunk lane * K + j of the unit)
+  unsigned long long D[K], F[K], R[K], V[K];
 };
 #ifndef PARPA_E2_ROWS_MIN
 #define PARPA_E2_ROWS_MIN 16
@@ -811,7 +831,8 @@ struct TileSrc {                       // raw field bytes: shared-memory tile co
 template <bool TS>
 __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, uint32_t c, unsigned long long row,
                                             unsigned long long fd, unsigned long long ld, bool ic, bool empty,
-                                            const uint8_t *tb, unsigned long long tbase) {
+                                            const uint8_t *tb, unsigned long long tbase,
+                                            unsigned long long tb_lim = ~0ull) {
   long long v = 0;
   int ok = 0;
   if (empty) {
@@ -825,7 +846,11 @@ __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, u
     // the field's first bytes as a register window from the tile copy in shared memory (a field that
     // began in an earlier tile — at most field 0 of the tile — takes the byte-wise path below)
     const bool is_ts = TS && cd->type == T_TIMESTAMP;
+#ifdef PARPA_BISECT_A
     if (fd >= tbase && L <= (is_ts ? 26ull : 16ull)) {
+#else
+    if (fd >= tbase && L <= (is_ts ? 26ull : 16ull) && fd - tbase + 36u <= tb_lim) {
+#endif
       const uint32_t o = (uint32_t)(fd - tbase), sh = (o & 3u) * 8u;
       const uint32_t *w = reinterpret_cast<const uint32_t *>(tb) + (o >> 2);
       const bool isf = cd->type == T_FLOAT64;
@@ -866,10 +891,16 @@ __device__ __forceinline__ void write_value(const KArgs &a, const ColDesc *cd, u
 template <bool TS>
 __device__ __forceinline__ void write_value_tile(const KArgs &a, const ColDesc *cd, uint32_t type, uint32_t c,
                                                  unsigned long long row, uint32_t o, uint32_t len, bool ic, bool far,
-                                                 unsigned long long off, const uint8_t *tb, unsigned long long tbase) {
+                                                 unsigned long long off, const uint8_t *tb, unsigned long long tbase,
+                                                 unsigned long long tb_lim = ~0ull) {
   long long v = 0;
   int res = 2;
+  // (tb_lim: bytes readable from tb — the staged tile's pad, or the input's end for a global-memory unit)
+#ifdef PARPA_BISECT_A
   if (!(ic || far) && len - 1u < (TS && type == T_TIMESTAMP ? 26u : 8u)) {
+#else
+  if (!(ic || far) && len - 1u < (TS && type == T_TIMESTAMP ? 26u : 8u) && o + 36u <= tb_lim) {
+#endif
     const uint32_t sh = (o & 3u) * 8u;
     const uint32_t *w = reinterpret_cast<const uint32_t *>(tb) + (o >> 2);
     const bool isf = type == T_FLOAT64;
@@ -888,7 +919,7 @@ __device__ __forceinline__ void write_value_tile(const KArgs &a, const ColDesc *
     }
   }
   if (res == 2) {
-    write_value<TS>(a, cd, c, row, off, off + len - 1, ic, len == 0, tb, tbase);
+    write_value<TS>(a, cd, c, row, off, off + len - 1, ic, len == 0, tb, tbase, tb_lim);
     return;
   }
   st_col(reinterpret_cast<long long *>(cd->val) + row, v);
@@ -903,25 +934,32 @@ __device__ __forceinline__ void write_value_tile(const KArgs &a, const ColDesc *
 //      column from ballots over the record bits.  Only field 0 can have begun in an earlier tile; it
 //      is combined with the prefix's open-field carry (P:408-414 extended with the carries).
 // E2:  column-major writes (below).
-__device__ __forceinline__ uint32_t kcount(const WarpScratch *ws, uint32_t x) {   // CTRL bytes before x
+template <class WS>
+__device__ __forceinline__ uint32_t kcount(const WS *ws, uint32_t x) {   // CTRL bytes before x
   return ws->kpre[x >> 5] + __popc(ws->kmask[x >> 5] & ((1u << (x & 31u)) - 1u));
 }
 // NP > 1 (k_small): NP warps share one tile — part 0 runs E0/E1 into its scratch `ws`, a named barrier
 // (bar, NP warps) publishes it, and every part writes the columns c = part, part + NP, ... in E2 (the
 // column-uniform path) or every NP-th item (the flattened path).  NP == 1 is the one-warp-per-tile path.
-template <bool TS, int NP = 1, bool SK = true>
-__device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, const Seg &prefix,
-                          unsigned long long Dm, unsigned long long Fm, unsigned long long Rm,
-                          unsigned long long Vm, unsigned long long tbase_g, unsigned long long cbase,
+template <bool TS, int NP = 1, bool SK = true, int K = 1>
+__device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratchT<K> *ws, const Seg &prefix,
+                          const Masks<K> &m, unsigned long long tbase_g, unsigned long long cbase,
                           EmitCounters &cnt, uint32_t part = 0, int bar = 0) {
+  static_assert(K == 1 || NP == 1, "super tiles are one warp per unit");
+  constexpr uint32_t POSM = UnitBits<K>::POS_MASK, LSH = UnitBits<K>::POS_BITS, LENM = UnitBits<K>::LEN_MASK;
   const int lane = threadIdx.x & 31;
   uint32_t nf = 0, nrec = 0;
   bool plain = false;
   if (NP == 1 || part == 0) {
-  const unsigned long long Km = Vm & ~Dm & ~Fm;
+  unsigned long long Kmj[K];
   // per-lane (delimiters << 16 | records) and CTRL counts -> exclusive offsets, tile totals
-  const uint32_t mine = (uint32_t)__popcll(Rm) | ((uint32_t)__popcll(Fm) << 16);
-  const uint32_t kmine = (uint32_t)__popcll(Km);
+  uint32_t mine = 0, kmine = 0;
+#pragma unroll
+  for (int j = 0; j < K; j++) {
+    Kmj[j] = m.V[j] & ~m.D[j] & ~m.F[j];
+    mine += (uint32_t)__popcll(m.R[j]) | ((uint32_t)__popcll(m.F[j]) << 16);
+    kmine += (uint32_t)__popcll(Kmj[j]);
+  }
   uint32_t inc = mine, kinc = kmine;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -933,14 +971,29 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
   nrec = tot & 0xFFFFu;
   if (nf > (uint32_t)FCAP || nrec >= (uint32_t)RCAP) {       // warp-uniform: dense tile, direct path
     SegT sagg;
-    const SegT sex = warp_scan_segt(chunk_segt(Dm, Fm, Rm, Vm, (uint32_t)lane * CHUNK), sagg);
-    emit_chunk<TS, SK>(a, cols, seg_op(prefix, segt_to_seg(sex, tbase_g)), Dm, Fm, Rm, Vm, cbase, cnt);
+    if constexpr (K == 1) {
+      const SegT sex = warp_scan_segt(chunk_segt(m.D[0], m.F[0], m.R[0], m.V[0], (uint32_t)lane * CHUNK), sagg);
+      emit_chunk<TS, SK>(a, cols, seg_op(prefix, segt_to_seg(sex, tbase_g)), m.D[0], m.F[0], m.R[0], m.V[0], cbase, cnt);
+    } else {
+      SegT ls = segt_ident();
+#pragma unroll
+      for (int j = 0; j < K; j++)
+        ls = segt_op(ls, chunk_segt(m.D[j], m.F[j], m.R[j], m.V[j], ((uint32_t)lane * K + (uint32_t)j) * CHUNK));
+      SegT run = warp_scan_segt(ls, sagg);
+#pragma unroll
+      for (int j = 0; j < K; j++) {
+        emit_chunk<TS, SK>(a, cols, seg_op(prefix, segt_to_seg(run, tbase_g)), m.D[j], m.F[j], m.R[j], m.V[j],
+                           cbase + (unsigned long long)j * CHUNK, cnt);
+        if (j + 1 < K) run = segt_op(run, chunk_segt(m.D[j], m.F[j], m.R[j], m.V[j], ((uint32_t)lane * K + (uint32_t)j) * CHUNK));
+      }
+    }
     if (NP == 1) return;
     nf = 0u;                                                  // the other parts have nothing to write
     nrec = 0u;
   } else {
   // ---- E1a ----
-  if (nf <= E1A_SELECT_MAX) {
+  if (K == 1 && nf <= E1A_SELECT_MAX) {
+    const unsigned long long Fm = m.F[0], Rm = m.R[0];
     // few delimiters (long fields, e.g. yelp text): lane k selects the k-th delimiter of the tile — the
     // owning chunk by a shuffle binary search over the lanes' exclusive counts, the bit by a popcount
     // binary search — instead of every lane walking its own mask with most lanes idle.
@@ -973,28 +1026,45 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     }
   } else {
     uint32_t k = (inc - mine) >> 16, jr = (inc - mine) & 0xFFFFu;
-    const uint32_t base = (uint32_t)lane * CHUNK;
 #pragma unroll
-    for (int h = 0; h < 2; h++) {                        // 32-bit halves: no 64-bit bit arithmetic per step
-      uint32_t fm = (uint32_t)(Fm >> (32 * h));
-      const uint32_t rm = (uint32_t)(Rm >> (32 * h)), hb = base + 32u * (uint32_t)h;
-      while (fm) {
-        const uint32_t p = (uint32_t)__ffs(fm) - 1u;
-        fm &= fm - 1u;
-        const uint32_t pos = hb + p, isrec = (rm >> p) & 1u;
-        ws->dlist[k++] = (uint16_t)(pos | (isrec << 15));
-        if (isrec) ws->rows[jr++] = k | (pos << 16);     // end field index | record delimiter position
+    for (int j = 0; j < K; j++) {
+      const uint32_t base = ((uint32_t)lane * K + (uint32_t)j) * CHUNK;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {                      // 32-bit halves: no 64-bit bit arithmetic per step
+        uint32_t fm = (uint32_t)(m.F[j] >> (32 * h));
+        const uint32_t rm = (uint32_t)(m.R[j] >> (32 * h)), hb = base + 32u * (uint32_t)h;
+        while (fm) {
+          const uint32_t p = (uint32_t)__ffs(fm) - 1u;
+          fm &= fm - 1u;
+          const uint32_t pos = hb + p, isrec = (rm >> p) & 1u;
+          ws->dlist[k++] = (uint16_t)(pos | (isrec << 15));
+          if (isrec) ws->rows[jr++] = k | (pos << 16);   // end field index | record delimiter position
+        }
       }
     }
   }
-  {
-    ws->dmask[2 * lane] = (uint32_t)Dm;
-    ws->dmask[2 * lane + 1] = (uint32_t)(Dm >> 32);
-    ws->kmask[2 * lane] = (uint32_t)Km;
-    ws->kmask[2 * lane + 1] = (uint32_t)(Km >> 32);
+  if constexpr (K == 1) {
+    ws->dmask[2 * lane] = (uint32_t)m.D[0];
+    ws->dmask[2 * lane + 1] = (uint32_t)(m.D[0] >> 32);
+    ws->kmask[2 * lane] = (uint32_t)Kmj[0];
+    ws->kmask[2 * lane + 1] = (uint32_t)(Kmj[0] >> 32);
     const uint32_t kex = kinc - kmine;
     ws->kpre[2 * lane] = (uint16_t)kex;
-    ws->kpre[2 * lane + 1] = (uint16_t)(kex + __popc((uint32_t)Km));
+    ws->kpre[2 * lane + 1] = (uint16_t)(kex + __popc((uint32_t)Kmj[0]));
+  } else {
+    uint32_t kex = kinc - kmine;
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+      const uint32_t wi = 2u * ((uint32_t)lane * K + (uint32_t)j);
+      ws->dmask[wi] = (uint32_t)m.D[j];
+      ws->dmask[wi + 1] = (uint32_t)(m.D[j] >> 32);
+      ws->kmask[wi] = (uint32_t)Kmj[j];
+      ws->kmask[wi + 1] = (uint32_t)(Kmj[j] >> 32);
+      ws->kpre[wi] = (uint16_t)kex;
+      kex += __popc((uint32_t)Kmj[j]);
+      ws->kpre[wi + 1] = (uint16_t)kex;
+      kex += __popc((uint32_t)(Kmj[j] >> 32));
+    }
   }
   __syncwarp();
   const uint32_t ktot = __shfl_sync(0xffffffffu, kinc, 31);    // CTRL bytes in the tile (warp-uniform)
@@ -1013,7 +1083,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
       if (hi > lo) extra += hi - lo;
     }
     if (lane == 0 && nf) {
-      const uint32_t p = ws->dlist[0] & 0x7FFu;
+      const uint32_t p = ws->dlist[0] & POSM;
       unsigned long long cfd = prefix.fd, cld = prefix.ld;
       uint32_t cfl = prefix.flags & (F_IC | F_PC | F_PRE);
       open_combine(cfd, cld, cfl, p ? tbase_g : NONE, p ? tbase_g + p - 1u : NONE, 0u);
@@ -1024,8 +1094,8 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
         const unsigned long long L = cld + 1 - cfd;
         const long long rel = (long long)cfd - (long long)tbase_g;
         const uint32_t icf = (cfl & F_IC) ? 0x80000000u : 0u;
-        if (rel >= 0 && L <= (unsigned long long)WT) {
-          e = (uint32_t)rel | ((uint32_t)L << 11) | icf;
+        if (rel >= 0 && L <= (unsigned long long)WT * K) {
+          e = (uint32_t)rel | ((uint32_t)L << LSH) | icf;
         } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
           emit_field<TS, SK>(a, cols, prefix.recs, c0, cfd, cld, cfl, tbase_g + p, cnt);
           e = FIELD_WRITTEN;
@@ -1049,7 +1119,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
       const uint32_t k = kb + (uint32_t)lane;
       const bool act = k < nf;
       const uint32_t dl = act ? ws->dlist[k] : 0u;
-      const uint32_t p = dl & 0x7FFu;
+      const uint32_t p = dl & POSM;
       const bool isrec = act && (dl >> 15);
       const unsigned recm = __ballot_sync(0xffffffffu, isrec);
       const uint32_t jr = jcarry + __popc(recm & lt);
@@ -1058,7 +1128,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
       const uint32_t c = lr >= 0 ? k - (uint32_t)lr - 1u : c0 + k;
       extra += (uint32_t)__popc(__ballot_sync(0xffffffffu, act && c >= a.C));
       if (act) {
-        const uint32_t x = k ? (ws->dlist[k - 1] & 0x7FFu) + 1u : 0u;   // field bytes [x, p)
+        const uint32_t x = k ? (ws->dlist[k - 1] & POSM) + 1u : 0u;   // field bytes [x, p)
         // inner / surrounding control bytes only matter for converted columns (a span is [first, last DATA])
         const uint32_t ty = c < a.C ? cols[c].type : (uint32_t)T_SKIP;
         const bool typed = ty != T_SPAN && ty != T_SKIP;
@@ -1086,7 +1156,7 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
             if (typed && ld > fd && kcount(ws, (uint32_t)ld) > kcount(ws, (uint32_t)fd + 1u)) ic = 0x80000000u;
           }
         }
-        uint32_t e = fd < 0 ? p : ((uint32_t)fd | ((uint32_t)(ld + 1 - fd) << 11) | ic);  // empty: (delim, 0)
+        uint32_t e = fd < 0 ? p : ((uint32_t)fd | ((uint32_t)(ld + 1 - fd) << LSH) | ic);  // empty: (delim, 0)
         if (k == 0) {                                         // may continue a field of an earlier tile
           uint32_t fl = ic ? F_IC : 0u;
           if (ktot && typed) {
@@ -1107,8 +1177,8 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
             const unsigned long long L = cld + 1 - cfd;
             const long long rel = (long long)cfd - (long long)tbase_g;
             const uint32_t icf = (cfl & F_IC) ? 0x80000000u : 0u;
-            if (rel >= 0 && L <= (unsigned long long)WT) {
-              e = (uint32_t)rel | ((uint32_t)L << 11) | icf;
+            if (rel >= 0 && L <= (unsigned long long)WT * K) {
+              e = (uint32_t)rel | ((uint32_t)L << LSH) | icf;
             } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
               emit_field<TS, SK>(a, cols, prefix.recs + jr, c, cfd, cld, cfl, tbase_g + p, cnt);
               e = FIELD_WRITTEN;
@@ -1138,7 +1208,9 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     plain = ws->e1_plain != 0u;
   }
   // ---- E2 ----
-  const uint8_t *tb = reinterpret_cast<const uint8_t *>(ws->bytes);
+  // the unit's bytes: the staged copy (K = 1), or global memory (super tiles: few typed fields)
+  const uint8_t *tb = K == 1 ? reinterpret_cast<const uint8_t *>(ws->bytes) : a.in + (tbase_g - a.base);
+  const unsigned long long tb_lim = K == 1 ? ~0ull : a.len - (tbase_g - a.base);
   const uint32_t last_end = nrec ? (ws->rows[nrec - 1] & 0xFFFFu) : 0u;
   const uint32_t nrows = nrec + (nf > last_end ? 1u : 0u);
   if (nrows == 0) {                                         // no delimiter: the open field continues
@@ -1177,20 +1249,20 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
         const uint32_t k = start + (c - cs);
         if (k < end) {
           if (plain && k) {                                    // the common case: [x, p), all DATA, in the tile
-            const uint32_t x = (ws->dlist[k - 1] & 0x7FFu) + 1u, len = (ws->dlist[k] & 0x7FFu) - x;
+            const uint32_t x = (ws->dlist[k - 1] & POSM) + 1u, len = (ws->dlist[k] & POSM) - x;
             const unsigned long long off = tbase_g + x;        // empty (x == p): (delimiter position, 0)
             st_col(cd->off + row, off);
             st_col(cd->len + row, len);
-            if (type != T_SPAN) write_value_tile<TS>(a, cd, type, c, row, x, len, false, false, off, tb, tbase_g);
+            if (type != T_SPAN) write_value_tile<TS>(a, cd, type, c, row, x, len, false, false, off, tb, tbase_g, tb_lim);
             continue;
           }
           const uint32_t e = ws->fields[k];
           if (k) {                                             // only field 0 can carry a special entry
-            const uint32_t o = e & 0x7FFu, len = (e >> 11) & 0xFFFu;
+            const uint32_t o = e & POSM, len = (e >> LSH) & LENM;
             const unsigned long long off = tbase_g + o;
             st_col(cd->off + row, off);
             st_col(cd->len + row, len);
-            if (type != T_SPAN) write_value_tile<TS>(a, cd, type, c, row, o, len, (e >> 31) != 0, false, off, tb, tbase_g);
+            if (type != T_SPAN) write_value_tile<TS>(a, cd, type, c, row, o, len, (e >> 31) != 0, false, off, tb, tbase_g, tb_lim);
             continue;
           }
           if (e == FIELD_WRITTEN) continue;
@@ -1205,14 +1277,14 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
             ic = (f.y >> 31) != 0;
             o = 0u;
           } else {
-            o = e & 0x7FFu;
+            o = e & POSM;
             off = tbase_g + o;
-            len = (e >> 11) & 0xFFFu;
+            len = (e >> LSH) & LENM;
             ic = (e >> 31) != 0;
           }
           st_col(cd->off + row, off);
           st_col(cd->len + row, len);
-          if (type != T_SPAN) write_value_tile<TS>(a, cd, type, c, row, o, len, ic, far, off, tb, tbase_g);
+          if (type != T_SPAN) write_value_tile<TS>(a, cd, type, c, row, o, len, ic, far, off, tb, tbase_g, tb_lim);
         } else if (closed) {
           st_col(cd->off + row, tbase_g + dpos);
           st_col(cd->len + row, 0xFFFFFFFFu);
@@ -1253,8 +1325,8 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
     if (k < end) {
       uint32_t e;
       if (plain && k) {                                     // [x, p) between two delimiters, all DATA
-        const uint32_t x = (ws->dlist[k - 1] & 0x7FFu) + 1u, p = ws->dlist[k] & 0x7FFu;
-        e = x < p ? x | ((p - x) << 11) : p;
+        const uint32_t x = (ws->dlist[k - 1] & POSM) + 1u, p = ws->dlist[k] & POSM;
+        e = x < p ? x | ((p - x) << LSH) : p;
       } else {
         e = ws->fields[k];
       }
@@ -1270,14 +1342,14 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratch *ws, 
         ic = (f.y >> 31) != 0;
         o = 0u;
       } else {
-        o = e & 0x7FFu;
+        o = e & POSM;
         off = tbase_g + o;
-        len = (e >> 11) & 0xFFFu;
+        len = (e >> LSH) & LENM;
         ic = (e >> 31) != 0;
       }
       st_col(cd->off + row, off);
       st_col(cd->len + row, len);
-      if (cd->type != T_SPAN) write_value_tile<TS>(a, cd, cd->type, ci, row, o, len, ic, far, off, tb, tbase_g);
+      if (cd->type != T_SPAN) write_value_tile<TS>(a, cd, cd->type, ci, row, o, len, ic, far, off, tb, tbase_g, tb_lim);
     } else if (ji < nrec) {                                 // record closed with fewer fields
       if (k == end) cnt.missing++;
       if (skip) continue;
@@ -1303,10 +1375,67 @@ namespace parpa {
 #define PARPA_EMIT_MINB 2
 #endif
 constexpr int EMIT_WARPS = PARPA_EMIT_WARPS;
-constexpr size_t EMIT_SMEM = EMIT_WARPS * sizeof(WarpScratch);
+constexpr size_t EMIT_SMEM = EMIT_WARPS * (sizeof(WarpScratchT<1>) > sizeof(WarpScratchT<SPARSE_K>)
+                                                ? sizeof(WarpScratchT<1>) : sizeof(WarpScratchT<SPARSE_K>));
 
 // S6+S7 per warp tile from what the scan half stored: the DATA / DELIM / RECORD masks of every chunk
 // (k_pass2) and the tile prefix (k_seg_scan).  No LUT, no re-simulation: 2 CTAs per SM.
+// Emission of sparse inputs (on average >= 32 bytes per field, e.g. yelp's long text): super tiles of SPARSE_K
+// warp tiles per warp.  A kernel of its own, launched next to k_emit (each returns at once when the range is
+// not its kind: the decision reads the range's field count, so both agree): in one kernel the 4-chunk masks
+// raised the register pressure of the per-tile path until it spilled (taxi +2%, CLF +9%).
+__device__ __forceinline__ bool emit_is_sparse(const KArgs &a) {
+  const unsigned long long nfl = a.tot_seg ? a.tot_seg->nflds : 0ull;
+  return a.emit_k == (uint32_t)SPARSE_K || (a.emit_k == 0u && a.len >= 32ull * (nfl + 1ull));
+}
+template <bool TS, bool SK>
+#ifndef PARPA_SPARSE_MINB
+#define PARPA_SPARSE_MINB PARPA_EMIT_MINB
+#endif
+__global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_SPARSE_MINB) k_emit_sparse(const KArgs a, const ColsK colsk) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ ColDesc s_cols[MAX_COLS];
+  PdlTrigger pdl_trigger;
+  for (int c = threadIdx.x; c < (int)a.C; c += blockDim.x) s_cols[c] = colsk.c[c];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  EmitCounters cnt{0ull, 0ull, 0u};
+  __syncthreads();
+  pdl_wait();
+  if (!emit_is_sparse(a)) return;
+  const uint32_t nw = gridDim.x * EMIT_WARPS;
+  WarpScratchT<SPARSE_K> *ws4 = reinterpret_cast<WarpScratchT<SPARSE_K> *>(smem) + warp;
+  const uint32_t nunits = (a.ntiles + SPARSE_K - 1) / SPARSE_K;
+  while (true) {
+    uint32_t u = 0;
+    if (lane == 0) u = atomicAdd(&a.ctrl->emit_ticket, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= nunits) break;
+    const uint32_t t0 = u * SPARSE_K;
+    const unsigned long long ustart = (unsigned long long)t0 * WT;
+    Masks<SPARSE_K> mm;
+#pragma unroll
+    for (int j = 0; j < SPARSE_K; j++) {                 // chunk lane * K + j of the unit
+      const unsigned long long ch = (unsigned long long)t0 * 32 + (unsigned long long)lane * SPARSE_K + j;
+      const unsigned long long cs = ch * CHUNK;
+      const int nv = cs >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cs);
+      if (nv > 0) {
+        const unsigned long long *mk = a.masks + (ch >> 5) * 96 + (ch & 31);
+        mm.D[j] = mk[0]; mm.F[j] = mk[32]; mm.R[j] = mk[64];
+      } else {
+        mm.D[j] = mm.F[j] = mm.R[j] = 0ull;
+      }
+      mm.V[j] = nv >= 64 ? ~0ull : ((1ull << nv) - 1ull);
+    }
+    emit_tile<TS, 1, SK, SPARSE_K>(a, s_cols, ws4, seg_op(a.seed, a.tinfo[t0].excl), mm, a.base + ustart,
+                                   a.base + ustart + (unsigned long long)lane * SPARSE_K * CHUNK, cnt);
+  }
+  if (lane == 0 && atomicAdd(&a.ctrl->emit_done, 1u) == nw - 1u) {   // last warp out: ready for the next launch
+    a.ctrl->emit_done = 0u;
+    a.ctrl->emit_ticket = 0u;
+  }
+  flush_counters(a, cnt);
+}
+
 template <bool TS, bool SK>
 __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const KArgs a, const ColsK colsk) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -1319,9 +1448,10 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const
   __syncthreads();
   pdl_wait();
   const uint32_t nw = gridDim.x * EMIT_WARPS;
+  const uint32_t ntiles = emit_is_sparse(a) ? 0u : a.ntiles;   // k_emit_sparse's range: no tiles here
 #ifdef PARPA_EMIT_STATIC
   const uint32_t gw = blockIdx.x * EMIT_WARPS + warp;
-  for (uint32_t t = gw; t < a.ntiles; t += nw) {
+  for (uint32_t t = gw; t < ntiles; t += nw) {
 #else
   // Tiles are taken in input order from one atomic counter, so the warps writing adjacent tiles (which
   // share the boundary sectors of every output column) stay together in time: with a static grid stride
@@ -1335,10 +1465,10 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const
   tk = __shfl_sync(0xffffffffu, tk, 0);
   uint32_t t = tk, tn = tk + 1;
   while (true) {
-    if (t >= a.ntiles) break;
+    if (t >= ntiles) break;
     uint32_t tnn = 0;
-    if (lane == 0 && tn < a.ntiles) tnn = atomicAdd(&a.ctrl->emit_ticket, 1u);
-    if (tn < a.ntiles) {                                   // the warp's next tile into L2
+    if (lane == 0 && tn < ntiles) tnn = atomicAdd(&a.ctrl->emit_ticket, 1u);
+    if (tn < ntiles) {                                   // the warp's next tile into L2
       const unsigned long long tb = (unsigned long long)tn;
       asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in + tb * WT + (unsigned long long)lane * CHUNK));
       if (lane < 6) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.masks + tb * 96 + lane * 16));
@@ -1349,7 +1479,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const
     uint32_t t = 0;
     if (lane == 0) t = atomicAdd(&a.ctrl->emit_ticket, 1u);
     t = __shfl_sync(0xffffffffu, t, 0);
-    if (t >= a.ntiles) break;
+    if (t >= ntiles) break;
 #endif
 #endif
     const unsigned long long tstart = (unsigned long long)t * WT;
@@ -1361,7 +1491,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const
       stash_chunk(ws->bytes, lane, v);
     }
 #if defined(PARPA_EMIT_STATIC) || !defined(PARPA_EMIT_TICKET2)
-    if (t + nw < a.ntiles) {                              // the warp's next tile into L2 (2 KB + 768 B masks):
+    if (t + nw < ntiles) {                              // the warp's next tile into L2 (2 KB + 768 B masks):
       const unsigned long long tn = (unsigned long long)(t + nw);   // its loads then wait on L2, not DRAM
       asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in + tn * WT + (unsigned long long)lane * CHUNK));
       if (lane < 6) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.masks + tn * 96 + lane * 16));
@@ -1370,7 +1500,8 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const
     const unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;
     const unsigned long long Dm = mk[0], Fm = mk[32], Rm = mk[64];
     const unsigned long long Vm = nvalid >= 64 ? ~0ull : ((1ull << nvalid) - 1ull);
-    emit_tile<TS, 1, SK>(a, s_cols, ws, seg_op(a.seed, a.tinfo[t].excl), Dm, Fm, Rm, Vm, a.base + tstart, a.base + cstart, cnt);
+    const Masks<1> mm{{Dm}, {Fm}, {Rm}, {Vm}};
+    emit_tile<TS, 1, SK>(a, s_cols, ws, seg_op(a.seed, a.tinfo[t].excl), mm, a.base + tstart, a.base + cstart, cnt);
 #if !defined(PARPA_EMIT_STATIC) && defined(PARPA_EMIT_TICKET2)
     t = tn;
     tn = __shfl_sync(0xffffffffu, tnn, 0);

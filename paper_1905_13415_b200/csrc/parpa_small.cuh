@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(SMALL_WARPS * 32, 1) k_small(const __grid_cons
       Dm = __ldcg(mk); Fm = __ldcg(mk + 32); Rm = __ldcg(mk + 64);
     }
     const unsigned long long Vm = nv >= 64 ? ~0ull : ((1ull << nv) - 1ull);
-    emit_tile<TS, SMALL_NP>(a, s_cols, gws, seg_op(a.seed, a.tinfo[t].excl), Dm, Fm, Rm, Vm, a.base + tstart,
+    const Masks<1> mm{{Dm}, {Fm}, {Rm}, {Vm}};
+    emit_tile<TS, SMALL_NP>(a, s_cols, gws, seg_op(a.seed, a.tinfo[t].excl), mm, a.base + tstart,
                             a.base + cstart, cnt, part, 1 + warp / SMALL_NP);
   }
   flush_counters(a, cnt);

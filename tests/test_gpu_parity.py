@@ -70,6 +70,22 @@ def test_workload_slices_full_compare(name):
     assert ora.R == g.records
 
 
+@pytest.mark.parametrize("unit", ["1", "4"])
+@pytest.mark.parametrize("name", ["cfg1", "taxi", "yelp", "clf"])
+def test_emission_units_forced(name, unit, monkeypatch):
+    """Both emission kernels on every workload, whatever its field density: k_emit's 2 KB warp tiles
+    (PARPA_EMIT_K=1) and k_emit_sparse's 8 KB super tiles (PARPA_EMIT_K=4), staged path (> 2 MB), plus ragged
+    tails of the last super tile."""
+    monkeypatch.setenv("PARPA_EMIT_K", unit)
+    w = datagen.WORKLOADS[name]
+    data, g = datagen.generate(name, 2_600_000)
+    for n in (len(data), len(data) - 2047, len(data) - 6000):
+        d = data[:n]
+        ora = oracle.parse(w.dialect, d, w.C, list(w.types))
+        res = parpa.parse(dfa(w.dialect), parpa.Schema(list(w.types)), dev(d))
+        compare(res, ora, w.types, f"{name}-K{unit}-{n}")
+
+
 @pytest.mark.parametrize("n", [0, 1, 2, 63, 64, 65, 127, 4095, 16383, 16384, 16385, 16384 * 3 + 17, 200_003])
 def test_ragged_sizes(n):
     data, _ = datagen.generate("cfg1", 400_000)
