@@ -68,14 +68,14 @@ int dev_cfg(DevCfg **out) {
     CK(cudaFuncSetAttribute(k_emit<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
     CK(cudaFuncSetAttribute(k_emit<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
     CK(cudaFuncSetAttribute(k_emit<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
-    CK(cudaFuncSetAttribute(k_emit_sparse<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
-    CK(cudaFuncSetAttribute(k_emit_sparse<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
-    CK(cudaFuncSetAttribute(k_emit_sparse<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
-    CK(cudaFuncSetAttribute(k_emit_sparse<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM));
+    CK(cudaFuncSetAttribute(k_emit_sparse<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SPARSE_SMEM));
+    CK(cudaFuncSetAttribute(k_emit_sparse<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SPARSE_SMEM));
+    CK(cudaFuncSetAttribute(k_emit_sparse<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SPARSE_SMEM));
+    CK(cudaFuncSetAttribute(k_emit_sparse<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SPARSE_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass1, k_pass1, PASS_WARPS * 32, PASS_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_pass2, k_pass2, PASS_WARPS * 32, PASS_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_emit, k_emit<false, false>, EMIT_WARPS * 32, EMIT_SMEM));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_sparse, k_emit_sparse<false, false>, EMIT_WARPS * 32, EMIT_SMEM));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_sparse, k_emit_sparse<false, false>, SPARSE_WARPS * 32, SPARSE_SMEM));
     CK(cudaFuncSetAttribute(k_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMALL_SMEM));
     CK(cudaFuncSetAttribute(k_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMALL_SMEM));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.occ_small, k_small<false>, SMALL_WARPS * 32, SMALL_SMEM));
@@ -435,17 +435,17 @@ int launch_emit(const KArgs &a, const DfaK &k, const ColsK &ck, cudaStream_t s, 
     // sparse ranges (>= 32 bytes per field): super tiles; k_emit above returned at once for them, this one
     // returns at once for the others (both read the range's field count on the device)
     Launch L(s, "k_emit_sparse");
-    const int g = grid_for(dc->occ_sparse, dc->sms, (a.ntiles + SPARSE_K - 1) / SPARSE_K, EMIT_WARPS);
+    const int g = grid_for(dc->occ_sparse, dc->sms, (a.ntiles + SPARSE_K - 1) / SPARSE_K, SPARSE_WARPS);
     const bool ts = has_timestamps(a, ck), sk = a.nskip > 0;
 #ifdef PARPA_SPARSE_NOPDL
     const bool pdl = false;
 #else
     const bool pdl = true;
 #endif
-    if (ts && sk) CK(launch_k(k_emit_sparse<true, true>, g, EMIT_WARPS * 32, EMIT_SMEM, s, pdl, a, ck));
-    else if (ts) CK(launch_k(k_emit_sparse<true, false>, g, EMIT_WARPS * 32, EMIT_SMEM, s, pdl, a, ck));
-    else if (sk) CK(launch_k(k_emit_sparse<false, true>, g, EMIT_WARPS * 32, EMIT_SMEM, s, pdl, a, ck));
-    else CK(launch_k(k_emit_sparse<false, false>, g, EMIT_WARPS * 32, EMIT_SMEM, s, pdl, a, ck));
+    if (ts && sk) CK(launch_k(k_emit_sparse<true, true>, g, SPARSE_WARPS * 32, SPARSE_SMEM, s, pdl, a, ck));
+    else if (ts) CK(launch_k(k_emit_sparse<true, false>, g, SPARSE_WARPS * 32, SPARSE_SMEM, s, pdl, a, ck));
+    else if (sk) CK(launch_k(k_emit_sparse<false, true>, g, SPARSE_WARPS * 32, SPARSE_SMEM, s, pdl, a, ck));
+    else CK(launch_k(k_emit_sparse<false, false>, g, SPARSE_WARPS * 32, SPARSE_SMEM, s, pdl, a, ck));
   }
   CK(cudaGetLastError());
   if (launches) *launches += 2;

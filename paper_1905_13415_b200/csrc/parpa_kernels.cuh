@@ -1388,11 +1388,16 @@ __device__ __forceinline__ bool emit_is_sparse(const KArgs &a) {
   const unsigned long long nfl = a.tot_seg ? a.tot_seg->nflds : 0ull;
   return a.emit_k == (uint32_t)SPARSE_K || (a.emit_k == 0u && a.len >= 32ull * (nfl + 1ull));
 }
-template <bool TS, bool SK>
 #ifndef PARPA_SPARSE_MINB
 #define PARPA_SPARSE_MINB PARPA_EMIT_MINB
 #endif
-__global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_SPARSE_MINB) k_emit_sparse(const KArgs a, const ColsK colsk) {
+#ifndef PARPA_SPARSE_WARPS
+#define PARPA_SPARSE_WARPS PARPA_EMIT_WARPS
+#endif
+constexpr int SPARSE_WARPS = PARPA_SPARSE_WARPS;
+constexpr size_t SPARSE_SMEM = SPARSE_WARPS * sizeof(WarpScratchT<SPARSE_K>);
+template <bool TS, bool SK>
+__global__ void __launch_bounds__(SPARSE_WARPS * 32, PARPA_SPARSE_MINB) k_emit_sparse(const KArgs a, const ColsK colsk) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ ColDesc s_cols[MAX_COLS];
   PdlTrigger pdl_trigger;
@@ -1402,7 +1407,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_SPARSE_MINB) k_emit_spa
   __syncthreads();
   pdl_wait();
   if (!emit_is_sparse(a)) return;
-  const uint32_t nw = gridDim.x * EMIT_WARPS;
+  const uint32_t nw = gridDim.x * SPARSE_WARPS;
   WarpScratchT<SPARSE_K> *ws4 = reinterpret_cast<WarpScratchT<SPARSE_K> *>(smem) + warp;
   const uint32_t nunits = (a.ntiles + SPARSE_K - 1) / SPARSE_K;
   while (true) {
