@@ -1392,8 +1392,8 @@ __device__ __forceinline__ bool emit_is_sparse(const KArgs &a) {
 #define PARPA_SPARSE_MINB PARPA_EMIT_MINB
 #endif
 #ifndef PARPA_SPARSE_WARPS
-#define PARPA_SPARSE_WARPS PARPA_EMIT_WARPS
-#endif
+#define PARPA_SPARSE_WARPS 14     // 2 x 14 warps per SM, 72 registers: at 16 x 2 (64 registers) the 4-chunk masks
+#endif                            // spill (measured on yelp: 16 -> 2.06 ms, 14 -> 1.81, 12 -> 1.85, 10 -> 1.82)
 constexpr int SPARSE_WARPS = PARPA_SPARSE_WARPS;
 constexpr size_t SPARSE_SMEM = SPARSE_WARPS * sizeof(WarpScratchT<SPARSE_K>);
 template <bool TS, bool SK>
