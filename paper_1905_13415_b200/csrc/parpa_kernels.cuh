@@ -1024,6 +1024,56 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratchT<K> *
       if (act) ws->dlist[k] = (uint16_t)(pos | (isrec << 15));
       if (isrec) ws->rows[__popc(recm & lt)] = (k + 1u) | (pos << 16);
     }
+  } else if (K > 1) {
+    // Super tiles: the warp selects delimiters cooperatively instead of each lane walking its 256 bytes (the
+    // walk ran at ~3 active lanes of 32 on yelp).  The lanes' delimiter / record words and the exclusive
+    // delimiter count of each 32-bit segment go to the (not yet used) mask arrays; then lane t takes the
+    // unit's delimiters t, t + 32, ...: owning lane by a shuffle binary search over the lanes' exclusive
+    // counts, segment by a binary search over that lane's 2K segment counts, bit by a popcount search.
+    constexpr int NS = 2 * K;                                   // 32-bit segments per lane
+    uint32_t seg = 0;
+#pragma unroll
+    for (int j = 0; j < K; j++) {
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const uint32_t si = (uint32_t)lane * NS + (uint32_t)(2 * j + h);
+        const uint32_t fw = (uint32_t)(m.F[j] >> (32 * h));
+        ws->dmask[si] = fw;
+        ws->kmask[si] = (uint32_t)(m.R[j] >> (32 * h));
+        ws->kpre[si] = (uint16_t)seg;
+        seg += (uint32_t)__popc(fw);
+      }
+    }
+    __syncwarp();
+    const uint32_t ex = (inc - mine) >> 16;                   // this lane's first delimiter index
+    const unsigned lt = (1u << lane) - 1u;
+    uint32_t jcarry = 0;
+    for (uint32_t kb = 0; kb < nf; kb += 32) {                 // warp-uniform rounds
+      const uint32_t k = kb + (uint32_t)lane;
+      uint32_t o = 0;
+#pragma unroll
+      for (uint32_t st = 16; st; st >>= 1)
+        if (__shfl_sync(0xffffffffu, ex, o + st) <= k) o += st;
+      const uint32_t r = k - __shfl_sync(0xffffffffu, ex, o);
+      const bool act = k < nf;
+      uint32_t s = 0;                                           // segment of lane o holding rank r
+#pragma unroll
+      for (uint32_t st = NS / 2; st; st >>= 1)
+        if (act && ws->kpre[o * NS + s + st] <= r) s += st;
+      uint32_t word = act ? ws->dmask[o * NS + s] : 0u, rr = act ? r - ws->kpre[o * NS + s] : 0u, q = 0;
+#pragma unroll
+      for (uint32_t sh = 16; sh; sh >>= 1) {
+        const uint32_t c = (uint32_t)__popc(word & ((1u << sh) - 1u));
+        if (rr >= c) { rr -= c; word >>= sh; q += sh; }
+      }
+      const uint32_t pos = (o * K + (s >> 1)) * CHUNK + (s & 1u) * 32u + q;
+      const uint32_t isrec = act ? ((ws->kmask[o * NS + s] >> q) & 1u) : 0u;
+      const unsigned recm = __ballot_sync(0xffffffffu, isrec != 0u);
+      if (act) ws->dlist[k] = (uint16_t)(pos | (isrec << 15));
+      if (isrec) ws->rows[jcarry + __popc(recm & lt)] = (k + 1u) | (pos << 16);
+      jcarry += (uint32_t)__popc(recm);
+    }
+    __syncwarp();                                               // the mask arrays are rewritten below
   } else {
     uint32_t k = (inc - mine) >> 16, jr = (inc - mine) & 0xFFFFu;
 #pragma unroll
@@ -1418,18 +1468,30 @@ __global__ void __launch_bounds__(SPARSE_WARPS * 32, PARPA_SPARSE_MINB) k_emit_s
     const uint32_t t0 = u * SPARSE_K;
     const unsigned long long ustart = (unsigned long long)t0 * WT;
     Masks<SPARSE_K> mm;
+    // chunk lane * K + j of the unit: tile t0 + (lane * K + j) / 32, lane (lane * K + j) % 32 of its masks
+    const unsigned long long *mk0 = a.masks + (unsigned long long)t0 * 96;
+    if (ustart + (unsigned long long)SPARSE_K * WT <= a.len) {   // every unit but the last: all chunks full
 #pragma unroll
-    for (int j = 0; j < SPARSE_K; j++) {                 // chunk lane * K + j of the unit
-      const unsigned long long ch = (unsigned long long)t0 * 32 + (unsigned long long)lane * SPARSE_K + j;
-      const unsigned long long cs = ch * CHUNK;
-      const int nv = cs >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cs);
-      if (nv > 0) {
-        const unsigned long long *mk = a.masks + (ch >> 5) * 96 + (ch & 31);
+      for (int j = 0; j < SPARSE_K; j++) {
+        const uint32_t ci = (uint32_t)lane * SPARSE_K + (uint32_t)j;
+        const unsigned long long *mk = mk0 + (ci >> 5) * 96 + (ci & 31u);
         mm.D[j] = mk[0]; mm.F[j] = mk[32]; mm.R[j] = mk[64];
-      } else {
-        mm.D[j] = mm.F[j] = mm.R[j] = 0ull;
+        mm.V[j] = ~0ull;
       }
-      mm.V[j] = nv >= 64 ? ~0ull : ((1ull << nv) - 1ull);
+    } else {
+#pragma unroll
+      for (int j = 0; j < SPARSE_K; j++) {
+        const uint32_t ci = (uint32_t)lane * SPARSE_K + (uint32_t)j;
+        const unsigned long long cs = ustart + (unsigned long long)ci * CHUNK;
+        const int nv = cs >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cs);
+        if (nv > 0) {
+          const unsigned long long *mk = mk0 + (ci >> 5) * 96 + (ci & 31u);
+          mm.D[j] = mk[0]; mm.F[j] = mk[32]; mm.R[j] = mk[64];
+        } else {
+          mm.D[j] = mm.F[j] = mm.R[j] = 0ull;
+        }
+        mm.V[j] = nv >= 64 ? ~0ull : ((1ull << nv) - 1ull);
+      }
     }
     emit_tile<TS, 1, SK, SPARSE_K>(a, s_cols, ws4, seg_op(a.seed, a.tinfo[t0].excl), mm, a.base + ustart,
                                    a.base + ustart + (unsigned long long)lane * SPARSE_K * CHUNK, cnt);
