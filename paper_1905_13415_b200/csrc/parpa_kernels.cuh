@@ -780,6 +780,7 @@ struct alignas(16) WarpScratchT {
   uint16_t dlist[FCAP];                     // delimiter positions (unit-local) | record bit << 15
   uint32_t dmask[WT * K / 32], kmask[WT * K / 32];  // DATA / CTRL bits of the unit, 32 per word
   uint16_t kpre[WT * K / 32];               // CTRL bits before each word
+  uint16_t segpre[K == 1 ? 2 : WT * K / 32];  // super tiles, E1a: delimiters before each lane's 32-bit segments
   uint32_t e1_nf, e1_nrec, e1_plain;        // E1 -> E2 when several warps share a tile (k_small)
 };
 using WarpScratch = WarpScratchT<1>;
@@ -942,7 +943,7 @@ __device__ __forceinline__ uint32_t kcount(const WS *ws, uint32_t x) {   // CTRL
 // (bar, NP warps) publishes it, and every part writes the columns c = part, part + NP, ... in E2 (the
 // column-uniform path) or every NP-th item (the flattened path).  NP == 1 is the one-warp-per-tile path.
 template <bool TS, int NP = 1, bool SK = true, int K = 1>
-__device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratchT<K> *ws, const Seg &prefix,
+__device__ __forceinline__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratchT<K> *ws, const Seg &prefix,
                           const Masks<K> &m, unsigned long long tbase_g, unsigned long long cbase,
                           EmitCounters &cnt, uint32_t part = 0, int bar = 0) {
   static_assert(K == 1 || NP == 1, "super tiles are one warp per unit");
@@ -1026,21 +1027,26 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratchT<K> *
     }
   } else if (K > 1) {
     // Super tiles: the warp selects delimiters cooperatively instead of each lane walking its 256 bytes (the
-    // walk ran at ~3 active lanes of 32 on yelp).  The lanes' delimiter / record words and the exclusive
-    // delimiter count of each 32-bit segment go to the (not yet used) mask arrays; then lane t takes the
-    // unit's delimiters t, t + 32, ...: owning lane by a shuffle binary search over the lanes' exclusive
-    // counts, segment by a binary search over that lane's 2K segment counts, bit by a popcount search.
+    // walk ran at ~3 active lanes of 32 on yelp).  The DATA / CTRL words go to shared memory first (the masks
+    // then die: register pressure), the lanes' delimiter / record words to `fields` (free until E1b) and the
+    // delimiters before each 32-bit segment to `segpre`; lane t then takes the unit's delimiters t, t + 32, ...:
+    // owning lane by a shuffle binary search over the lanes' exclusive counts, segment by a binary search over
+    // that lane's 2K segment counts, bit by a popcount search.
     constexpr int NS = 2 * K;                                   // 32-bit segments per lane
-    uint32_t seg = 0;
+    uint32_t kex = kinc - kmine, seg = 0;
 #pragma unroll
     for (int j = 0; j < K; j++) {
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const uint32_t si = (uint32_t)lane * NS + (uint32_t)(2 * j + h);
-        const uint32_t fw = (uint32_t)(m.F[j] >> (32 * h));
-        ws->dmask[si] = fw;
-        ws->kmask[si] = (uint32_t)(m.R[j] >> (32 * h));
-        ws->kpre[si] = (uint16_t)seg;
+        const uint32_t kw = (uint32_t)(Kmj[j] >> (32 * h)), fw = (uint32_t)(m.F[j] >> (32 * h));
+        ws->dmask[si] = (uint32_t)(m.D[j] >> (32 * h));
+        ws->kmask[si] = kw;
+        ws->kpre[si] = (uint16_t)kex;
+        kex += (uint32_t)__popc(kw);
+        ws->fields[si] = fw;
+        ws->fields[WT * K / 32 + si] = (uint32_t)(m.R[j] >> (32 * h));
+        ws->segpre[si] = (uint16_t)seg;
         seg += (uint32_t)__popc(fw);
       }
     }
@@ -1059,21 +1065,22 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratchT<K> *
       uint32_t s = 0;                                           // segment of lane o holding rank r
 #pragma unroll
       for (uint32_t st = NS / 2; st; st >>= 1)
-        if (act && ws->kpre[o * NS + s + st] <= r) s += st;
-      uint32_t word = act ? ws->dmask[o * NS + s] : 0u, rr = act ? r - ws->kpre[o * NS + s] : 0u, q = 0;
+        if (act && ws->segpre[o * NS + s + st] <= r) s += st;
+      const uint32_t wi = o * NS + s;
+      uint32_t word = act ? ws->fields[wi] : 0u, rr = act ? r - ws->segpre[wi] : 0u, q = 0;
 #pragma unroll
       for (uint32_t sh = 16; sh; sh >>= 1) {
         const uint32_t c = (uint32_t)__popc(word & ((1u << sh) - 1u));
         if (rr >= c) { rr -= c; word >>= sh; q += sh; }
       }
       const uint32_t pos = (o * K + (s >> 1)) * CHUNK + (s & 1u) * 32u + q;
-      const uint32_t isrec = act ? ((ws->kmask[o * NS + s] >> q) & 1u) : 0u;
+      const uint32_t isrec = act ? ((ws->fields[WT * K / 32 + wi] >> q) & 1u) : 0u;
       const unsigned recm = __ballot_sync(0xffffffffu, isrec != 0u);
       if (act) ws->dlist[k] = (uint16_t)(pos | (isrec << 15));
       if (isrec) ws->rows[jcarry + __popc(recm & lt)] = (k + 1u) | (pos << 16);
       jcarry += (uint32_t)__popc(recm);
     }
-    __syncwarp();                                               // the mask arrays are rewritten below
+    __syncwarp();                                               // `fields` is rewritten by E1b
   } else {
     uint32_t k = (inc - mine) >> 16, jr = (inc - mine) & 0xFFFFu;
 #pragma unroll
@@ -1093,7 +1100,9 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratchT<K> *
       }
     }
   }
-  if constexpr (K == 1) {
+  if constexpr (K > 1) {
+    // (written before the select above)
+  } else if constexpr (K == 1) {
     ws->dmask[2 * lane] = (uint32_t)m.D[0];
     ws->dmask[2 * lane + 1] = (uint32_t)(m.D[0] >> 32);
     ws->kmask[2 * lane] = (uint32_t)Kmj[0];
@@ -1207,6 +1216,12 @@ __device__ void emit_tile(const KArgs &a, const ColDesc *cols, WarpScratchT<K> *
           }
         }
         uint32_t e = fd < 0 ? p : ((uint32_t)fd | ((uint32_t)(ld + 1 - fd) << LSH) | ic);  // empty: (delim, 0)
+        if (K > 1 && typed && fd >= 0)    // super tiles read typed bytes from global memory in E2: start the load now
+#ifdef PARPA_PREF_L2
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in + (tbase_g - a.base) + (unsigned)fd));
+#else
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.in + (tbase_g - a.base) + (unsigned)fd));
+#endif
         if (k == 0) {                                         // may continue a field of an earlier tile
           uint32_t fl = ic ? F_IC : 0u;
           if (ktot && typed) {
