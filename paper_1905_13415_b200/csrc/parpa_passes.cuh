@@ -250,15 +250,20 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, con
   uint32_t t = blockIdx.x * PASS_WARPS + warp;
   if (t < a.ntiles) stage_chunk(a, bufs, t, lane, nfull);
   cp_async_commit();
+  // each tile's lane-exclusive τ and tile prefix are loaded one iteration ahead (their latency was exposed
+  // right before the re-simulation: -3 to -4% on pass 2)
+  uint32_t lex_n = t < a.ntiles ? a.lex[(unsigned long long)t * 32 + lane] : 0u, wpre_n = t < a.ntiles ? a.wpre[t] : 0u;
   for (uint32_t i = 0; t < a.ntiles; t += nw, i ^= 1u) {
     if (t + nw < a.ntiles) stage_chunk(a, bufs + (i ^ 1u) * (WT / 16), t + nw, lane, nfull);
     cp_async_commit();
+    const uint32_t lex_c = lex_n, wpre_c = wpre_n;
+    if (t + nw < a.ntiles) { lex_n = a.lex[(unsigned long long)(t + nw) * 32 + lane]; wpre_n = a.wpre[t + nw]; }
     cp_async_wait1();
     const unsigned long long cstart = (unsigned long long)t * WT + (unsigned long long)lane * CHUNK;
     const int nv = t < nfull ? CHUNK : chunk_valid(a, cstart);
     uint32_t v[16];
     read_chunk(bufs + i * (WT / 16), lane, v);
-    const uint32_t entry = nib_at(a.lex[(unsigned long long)t * 32 + lane], nib_at(a.wpre[t], a.seed_dev));
+    const uint32_t entry = nib_at(lex_c, nib_at(wpre_c, a.seed_dev));
     a.chunk_state[(unsigned long long)t * 32 + lane] = (uint8_t)entry;
     unsigned long long Dm, Fm, Rm;
     uint32_t fin, xprev;
@@ -274,12 +279,13 @@ __global__ void __launch_bounds__(PASS_WARPS * 32, 1) k_pass2(const KArgs a, con
       int p = first_inv_in_chunk(ps.lut, a.in + cstart, nv, ps.laneoff, entry, STEP_ROW_DP);
       if (p >= 0) atomicMax(&a.ctrl->inv_neg, ~(a.base + cstart + (unsigned)p));
     }
-    if (nv > 0 && cstart + (unsigned)nv == a.len) a.ctrl->last_cls = 0x100u | (xprev & 0xFu);   // for the EOI action
+    if (t + 1u == a.ntiles && nv > 0 && cstart + (unsigned)nv == a.len)
+      a.ctrl->last_cls = 0x100u | (xprev & 0xFu);                            // for the EOI action
     unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;   // for k_emit
     mk[0] = Dm;
     mk[32] = Fm;
     mk[64] = Rm;
-    const unsigned long long Vm = nv >= 64 ? ~0ull : ((1ull << nv) - 1ull);
+    const unsigned long long Vm = t < nfull ? ~0ull : nv >= 64 ? ~0ull : ((1ull << nv) - 1ull);
     const SegT s = warp_tile_segt(Dm, Fm, Rm, Vm);
     if (lane == 0) a.wseg[t] = make_uint4(s.cnt, s.colf, s.pos, 0u);
   }
