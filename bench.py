@@ -484,6 +484,17 @@ def run_config(args, config, ctx, main=True):
                 "share_of_step": round(kms / ms_step, 4),
                 "step_achieved": round(alg_bytes * (total_bytes / n) / (ms_step * 1e-3) / 1e9, 1),
                 "step_frac": round(alg_bytes * (total_bytes / n) / (ms_step * 1e-3) / 1e9 / peak, 4)}
+        # every kernel's share of the step and its own algorithmic fraction: the passes each read the input once
+        # (N bytes; their masks / transition vectors are intermediates), the emission kernel moves bytes_alg
+        kk = {}
+        for name, v in per_kernel.items():
+            m = statistics.mean(v)
+            ab = alg_bytes if name in ("k_emit", "k_emit_sparse") else (n if name in ("k_pass1", "k_pass2") else None)
+            kk[name] = {"ms": round(m, 4), "share": round(m / ms_step, 4)}
+            if ab is not None and m > 0.05:
+                kk[name].update({"alg_bytes": int(ab), "frac": round(ab / (m * 1e-3) / 1e9 / peak, 4)})
+        roof["kernels"] = kk
+        roof["largest_share"] = max(kk, key=lambda k: kk[k]["share"])
 
     parity = None
     if world == 1 and args.parity == "full":
