@@ -910,8 +910,10 @@ __device__ __forceinline__ void write_value_tile(const KArgs &a, const ColDesc *
 #pragma unroll
       for (int k = 0; k < 7; k++) x[k] = __funnelshift_r(w[k], w[k + 1], sh);
       res = conv_timestamp_words(x, (int)len, v);
+#ifndef PARPA_CONV8_ONLY
     } else if (len <= 4u) {
       res = conv_window4(__funnelshift_r(w[0], w[1], sh), len, isf, v);
+#endif
     } else {
       const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
       const unsigned long long x8 = (unsigned long long)__funnelshift_r(w0, w1, sh) |
