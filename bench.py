@@ -103,13 +103,26 @@ class Clocks:
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "25"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-            time.sleep(0.2)
+            t0 = time.time()                       # nvidia-smi's start-up can exceed 0.2 s on a busy host:
+            while time.time() - t0 < 3.0:          # wait for its first sample before the timed region
+                time.sleep(0.05)
+                if os.path.getsize(self.path) > 0:
+                    break
         except Exception:
             self.proc = None
 
     def stop(self):
         if not self.proc:
             return None
+        t0 = time.time()                           # short timed regions (cfg1: ~10 ms): let the 25 ms sampler
+        while time.time() - t0 < 0.5:              # record at least three samples around the region
+            try:
+                with open(self.path) as f:
+                    if sum(1 for _ in f) >= 3:
+                        break
+            except OSError:
+                break
+            time.sleep(0.025)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)

@@ -951,96 +951,8 @@ __device__ __forceinline__ void emit_tile(const KArgs &a, const ColDesc *cols, W
   static_assert(K == 1 || NP == 1, "super tiles are one warp per unit");
   constexpr uint32_t POSM = UnitBits<K>::POS_MASK, LSH = UnitBits<K>::POS_BITS, LENM = UnitBits<K>::LEN_MASK;
   const int lane = threadIdx.x & 31;
-  uint32_t nf = 0, nrec = 0, ktot_s = 0;
+  uint32_t nf = 0, nrec = 0;
   bool plain = false, need_e1b = false;
-  // (one block of 32 fields [kb, kb + 32); jcarry / lastrec = records before kb and the last of them)
-  auto e1b_block = [&](uint32_t kb, uint32_t &jcarry, int &lastrec, uint32_t &extra) {
-    const uint32_t c0 = prefix.col;
-    const unsigned lt = (1u << lane) - 1u;
-      const uint32_t k = kb + (uint32_t)lane;
-      const bool act = k < nf;
-      const uint32_t dl = act ? ws->dlist[k] : 0u;
-      const uint32_t p = dl & POSM;
-      const bool isrec = act && (dl >> 15);
-      const unsigned recm = __ballot_sync(0xffffffffu, isrec);
-      const uint32_t jr = jcarry + __popc(recm & lt);
-      const unsigned before = recm & lt;
-      const int lr = before ? (int)(kb + 31u - __clz(before)) : lastrec;
-      const uint32_t c = lr >= 0 ? k - (uint32_t)lr - 1u : c0 + k;
-      extra += (uint32_t)__popc(__ballot_sync(0xffffffffu, act && c >= a.C));
-      if (act) {
-        const uint32_t x = k ? (ws->dlist[k - 1] & POSM) + 1u : 0u;   // field bytes [x, p)
-        // inner / surrounding control bytes only matter for converted columns (a span is [first, last DATA])
-        const uint32_t ty = c < a.C ? cols[c].type : (uint32_t)T_SKIP;
-        const bool typed = ty != T_SPAN && ty != T_SKIP;
-        int fd = -1, ld = -1;
-        uint32_t ic = 0;
-        if (ktot_s == 0u) {                                     // no CTRL byte: [x, p) is all DATA
-          if (x < p) { fd = (int)x; ld = (int)p - 1; }
-        } else {
-          if (x < p) {
-            uint32_t w = x >> 5;
-            uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu << (x & 31u));
-            const uint32_t wp = p >> 5;
-            while (!bits && w < wp) bits = ws->dmask[++w];
-            if (bits) {
-              const uint32_t f = (w << 5) + (uint32_t)__ffs(bits) - 1u;
-              if (f < p) fd = (int)f;
-            }
-          }
-          if (fd >= 0) {
-            const uint32_t y = p - 1u;
-            uint32_t w = y >> 5;
-            uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu >> (31u - (y & 31u)));
-            while (!bits) bits = ws->dmask[--w];
-            ld = (int)((w << 5) + 31u - (uint32_t)__clz(bits));
-            if (typed && ld > fd && kcount(ws, (uint32_t)ld) > kcount(ws, (uint32_t)fd + 1u)) ic = 0x80000000u;
-          }
-        }
-        uint32_t e = fd < 0 ? p : ((uint32_t)fd | ((uint32_t)(ld + 1 - fd) << LSH) | ic);  // empty: (delim, 0)
-        if (K > 1 && typed && fd >= 0)    // super tiles read typed bytes from global memory in E2: start the load now
-#ifdef PARPA_PREF_L2
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in + (tbase_g - a.base) + (unsigned)fd));
-#else
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.in + (tbase_g - a.base) + (unsigned)fd));
-#endif
-        if (k == 0) {                                         // may continue a field of an earlier tile
-          uint32_t fl = ic ? F_IC : 0u;
-          if (ktot_s && typed) {
-            if (fd >= 0) {
-              if (kcount(ws, (uint32_t)fd) > 0u) fl |= F_PRE;
-              if (kcount(ws, p) > kcount(ws, (uint32_t)ld + 1u)) fl |= F_PC;
-            } else if (kcount(ws, p) > 0u) {
-              fl |= F_PRE;
-            }
-          }
-          unsigned long long cfd = prefix.fd, cld = prefix.ld;
-          uint32_t cfl = prefix.flags & (F_IC | F_PC | F_PRE);
-          open_combine(cfd, cld, cfl, fd >= 0 ? tbase_g + (unsigned)fd : NONE, fd >= 0 ? tbase_g + (unsigned)ld : NONE,
-                       fl);
-          if (cfd == NONE) {
-            e = p;
-          } else {
-            const unsigned long long L = cld + 1 - cfd;
-            const long long rel = (long long)cfd - (long long)tbase_g;
-            const uint32_t icf = (cfl & F_IC) ? 0x80000000u : 0u;
-            if (rel >= 0 && L <= (unsigned long long)WT * K) {
-              e = (uint32_t)rel | ((uint32_t)L << LSH) | icf;
-            } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
-              emit_field<TS, SK>(a, cols, prefix.recs + jr, c, cfd, cld, cfl, tbase_g + p, cnt);
-              e = FIELD_WRITTEN;
-              if (c >= a.C) cnt.extra--;                      // emit_field counted it already
-            } else {
-              ws->f0 = make_uint2((uint32_t)(int32_t)rel, (uint32_t)L | icf);
-              e = FIELD_FAR;
-            }
-          }
-        }
-        ws->fields[k] = e;
-      }
-      jcarry += (uint32_t)__popc(recm);
-      if (recm) lastrec = (int)(kb + 31u - __clz(recm));
-  };
   if (NP == 1 || part == 0) {
   unsigned long long Kmj[K];
   // per-lane (delimiters << 16 | records) and CTRL counts -> exclusive offsets, tile totals
@@ -1217,7 +1129,6 @@ __device__ __forceinline__ void emit_tile(const KArgs &a, const ColDesc *cols, W
   }
   __syncwarp();
   const uint32_t ktot = __shfl_sync(0xffffffffu, kinc, 31);    // CTRL bytes in the tile (warp-uniform)
-  ktot_s = ktot;
   plain = ktot == 0u;
   if (plain) {
     // E1b' (no CTRL byte in the tile): field k is the byte range between delimiters k-1 and k, all DATA,
@@ -1261,10 +1172,98 @@ __device__ __forceinline__ void emit_tile(const KArgs &a, const ColDesc *cols, W
   } else {
   // ---- E1b ----
   if (NP == 1) {
+  {
+    const uint32_t c0 = prefix.col;
     uint32_t jcarry = 0, extra = 0;
     int lastrec = -1;
-    for (uint32_t kb = 0; kb < nf; kb += 32) e1b_block(kb, jcarry, lastrec, extra);
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint32_t kb = 0; kb < nf; kb += 32) {
+      const uint32_t k = kb + (uint32_t)lane;
+      const bool act = k < nf;
+      const uint32_t dl = act ? ws->dlist[k] : 0u;
+      const uint32_t p = dl & POSM;
+      const bool isrec = act && (dl >> 15);
+      const unsigned recm = __ballot_sync(0xffffffffu, isrec);
+      const uint32_t jr = jcarry + __popc(recm & lt);
+      const unsigned before = recm & lt;
+      const int lr = before ? (int)(kb + 31u - __clz(before)) : lastrec;
+      const uint32_t c = lr >= 0 ? k - (uint32_t)lr - 1u : c0 + k;
+      extra += (uint32_t)__popc(__ballot_sync(0xffffffffu, act && c >= a.C));
+      if (act) {
+        const uint32_t x = k ? (ws->dlist[k - 1] & POSM) + 1u : 0u;   // field bytes [x, p)
+        // inner / surrounding control bytes only matter for converted columns (a span is [first, last DATA])
+        const uint32_t ty = c < a.C ? cols[c].type : (uint32_t)T_SKIP;
+        const bool typed = ty != T_SPAN && ty != T_SKIP;
+        int fd = -1, ld = -1;
+        uint32_t ic = 0;
+        if (ktot == 0u) {                                     // no CTRL byte: [x, p) is all DATA
+          if (x < p) { fd = (int)x; ld = (int)p - 1; }
+        } else {
+          if (x < p) {
+            uint32_t w = x >> 5;
+            uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu << (x & 31u));
+            const uint32_t wp = p >> 5;
+            while (!bits && w < wp) bits = ws->dmask[++w];
+            if (bits) {
+              const uint32_t f = (w << 5) + (uint32_t)__ffs(bits) - 1u;
+              if (f < p) fd = (int)f;
+            }
+          }
+          if (fd >= 0) {
+            const uint32_t y = p - 1u;
+            uint32_t w = y >> 5;
+            uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu >> (31u - (y & 31u)));
+            while (!bits) bits = ws->dmask[--w];
+            ld = (int)((w << 5) + 31u - (uint32_t)__clz(bits));
+            if (typed && ld > fd && kcount(ws, (uint32_t)ld) > kcount(ws, (uint32_t)fd + 1u)) ic = 0x80000000u;
+          }
+        }
+        uint32_t e = fd < 0 ? p : ((uint32_t)fd | ((uint32_t)(ld + 1 - fd) << LSH) | ic);  // empty: (delim, 0)
+        if (K > 1 && typed && fd >= 0)    // super tiles read typed bytes from global memory in E2: start the load now
+#ifdef PARPA_PREF_L2
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in + (tbase_g - a.base) + (unsigned)fd));
+#else
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.in + (tbase_g - a.base) + (unsigned)fd));
+#endif
+        if (k == 0) {                                         // may continue a field of an earlier tile
+          uint32_t fl = ic ? F_IC : 0u;
+          if (ktot && typed) {
+            if (fd >= 0) {
+              if (kcount(ws, (uint32_t)fd) > 0u) fl |= F_PRE;
+              if (kcount(ws, p) > kcount(ws, (uint32_t)ld + 1u)) fl |= F_PC;
+            } else if (kcount(ws, p) > 0u) {
+              fl |= F_PRE;
+            }
+          }
+          unsigned long long cfd = prefix.fd, cld = prefix.ld;
+          uint32_t cfl = prefix.flags & (F_IC | F_PC | F_PRE);
+          open_combine(cfd, cld, cfl, fd >= 0 ? tbase_g + (unsigned)fd : NONE, fd >= 0 ? tbase_g + (unsigned)ld : NONE,
+                       fl);
+          if (cfd == NONE) {
+            e = p;
+          } else {
+            const unsigned long long L = cld + 1 - cfd;
+            const long long rel = (long long)cfd - (long long)tbase_g;
+            const uint32_t icf = (cfl & F_IC) ? 0x80000000u : 0u;
+            if (rel >= 0 && L <= (unsigned long long)WT * K) {
+              e = (uint32_t)rel | ((uint32_t)L << LSH) | icf;
+            } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
+              emit_field<TS, SK>(a, cols, prefix.recs + jr, c, cfd, cld, cfl, tbase_g + p, cnt);
+              e = FIELD_WRITTEN;
+              if (c >= a.C) cnt.extra--;                      // emit_field counted it already
+            } else {
+              ws->f0 = make_uint2((uint32_t)(int32_t)rel, (uint32_t)L | icf);
+              e = FIELD_FAR;
+            }
+          }
+        }
+        ws->fields[k] = e;
+      }
+      jcarry += (uint32_t)__popc(recm);
+      if (recm) lastrec = (int)(kb + 31u - __clz(recm));
+    }
     if (lane == 0) cnt.extra += extra;
+  }
   } else {
     need_e1b = true;                                        // split over the NP parts after the barrier
   }
@@ -1278,8 +1277,12 @@ __device__ __forceinline__ void emit_tile(const KArgs &a, const ColDesc *cols, W
     nf = ws->e1_nf;
     nrec = ws->e1_nrec;
     plain = ws->e1_plain != 0u;
-    if (!plain && nf > 0u) {                                // E1b split over the parts: block kb by part kb/32 % NP
-      ktot_s = 1u;                                          // (not plain: the tile has CTRL bytes)
+    (void)need_e1b;
+    if (!plain && nf > 0u) {
+      // E1b split over the NP parts (k_small: the tile's E1 latency is on the critical path): part p takes the
+      // 32-field blocks p, p + NP, ..., its record / column carries recomputed from the delimiter list
+      const uint32_t c0 = prefix.col;
+      const unsigned lt = (1u << lane) - 1u;
       uint32_t extra = 0;
       for (uint32_t kb = 32u * part; kb < nf; kb += 32u * NP) {
         uint32_t jcarry = 0;                                // records before kb, and the last of them
@@ -1290,7 +1293,87 @@ __device__ __forceinline__ void emit_tile(const KArgs &a, const ColDesc *cols, W
           jcarry += (uint32_t)__popc(mr);
           if (mr) lastrec = (int)(b + 31u - __clz(mr));
         }
-        e1b_block(kb, jcarry, lastrec, extra);
+      const uint32_t k = kb + (uint32_t)lane;
+      const bool act = k < nf;
+      const uint32_t dl = act ? ws->dlist[k] : 0u;
+      const uint32_t p = dl & POSM;
+      const bool isrec = act && (dl >> 15);
+      const unsigned recm = __ballot_sync(0xffffffffu, isrec);
+      const uint32_t jr = jcarry + __popc(recm & lt);
+      const unsigned before = recm & lt;
+      const int lr = before ? (int)(kb + 31u - __clz(before)) : lastrec;
+      const uint32_t c = lr >= 0 ? k - (uint32_t)lr - 1u : c0 + k;
+      extra += (uint32_t)__popc(__ballot_sync(0xffffffffu, act && c >= a.C));
+      if (act) {
+        const uint32_t x = k ? (ws->dlist[k - 1] & POSM) + 1u : 0u;   // field bytes [x, p)
+        // inner / surrounding control bytes only matter for converted columns (a span is [first, last DATA])
+        const uint32_t ty = c < a.C ? cols[c].type : (uint32_t)T_SKIP;
+        const bool typed = ty != T_SPAN && ty != T_SKIP;
+        int fd = -1, ld = -1;
+        uint32_t ic = 0;
+        if (false) {                                          // (the tile has CTRL bytes)                                     // no CTRL byte: [x, p) is all DATA
+          if (x < p) { fd = (int)x; ld = (int)p - 1; }
+        } else {
+          if (x < p) {
+            uint32_t w = x >> 5;
+            uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu << (x & 31u));
+            const uint32_t wp = p >> 5;
+            while (!bits && w < wp) bits = ws->dmask[++w];
+            if (bits) {
+              const uint32_t f = (w << 5) + (uint32_t)__ffs(bits) - 1u;
+              if (f < p) fd = (int)f;
+            }
+          }
+          if (fd >= 0) {
+            const uint32_t y = p - 1u;
+            uint32_t w = y >> 5;
+            uint32_t bits = ws->dmask[w] & (0xFFFFFFFFu >> (31u - (y & 31u)));
+            while (!bits) bits = ws->dmask[--w];
+            ld = (int)((w << 5) + 31u - (uint32_t)__clz(bits));
+            if (typed && ld > fd && kcount(ws, (uint32_t)ld) > kcount(ws, (uint32_t)fd + 1u)) ic = 0x80000000u;
+          }
+        }
+        uint32_t e = fd < 0 ? p : ((uint32_t)fd | ((uint32_t)(ld + 1 - fd) << LSH) | ic);  // empty: (delim, 0)
+        if (K > 1 && typed && fd >= 0)    // super tiles read typed bytes from global memory in E2: start the load now
+#ifdef PARPA_PREF_L2
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in + (tbase_g - a.base) + (unsigned)fd));
+#else
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.in + (tbase_g - a.base) + (unsigned)fd));
+#endif
+        if (k == 0) {                                         // may continue a field of an earlier tile
+          uint32_t fl = ic ? F_IC : 0u;
+          if (typed) {
+            if (fd >= 0) {
+              if (kcount(ws, (uint32_t)fd) > 0u) fl |= F_PRE;
+              if (kcount(ws, p) > kcount(ws, (uint32_t)ld + 1u)) fl |= F_PC;
+            } else if (kcount(ws, p) > 0u) {
+              fl |= F_PRE;
+            }
+          }
+          unsigned long long cfd = prefix.fd, cld = prefix.ld;
+          uint32_t cfl = prefix.flags & (F_IC | F_PC | F_PRE);
+          open_combine(cfd, cld, cfl, fd >= 0 ? tbase_g + (unsigned)fd : NONE, fd >= 0 ? tbase_g + (unsigned)ld : NONE,
+                       fl);
+          if (cfd == NONE) {
+            e = p;
+          } else {
+            const unsigned long long L = cld + 1 - cfd;
+            const long long rel = (long long)cfd - (long long)tbase_g;
+            const uint32_t icf = (cfl & F_IC) ? 0x80000000u : 0u;
+            if (rel >= 0 && L <= (unsigned long long)WT * K) {
+              e = (uint32_t)rel | ((uint32_t)L << LSH) | icf;
+            } else if (L >= 0x7FFFFFFFull || rel < -0x7FFFFFFFll) {   // huge / far-away: write it here
+              emit_field<TS, SK>(a, cols, prefix.recs + jr, c, cfd, cld, cfl, tbase_g + p, cnt);
+              e = FIELD_WRITTEN;
+              if (c >= a.C) cnt.extra--;                      // emit_field counted it already
+            } else {
+              ws->f0 = make_uint2((uint32_t)(int32_t)rel, (uint32_t)L | icf);
+              e = FIELD_FAR;
+            }
+          }
+        }
+        ws->fields[k] = e;
+      }
       }
       if (lane == 0) cnt.extra += extra;
       __syncwarp();
