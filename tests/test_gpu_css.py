@@ -101,3 +101,47 @@ def test_result_accessors_and_allocator_hook():
         torch.cuda.synchronize()
     finally:
         parpa.use_torch_allocator(False)
+
+
+def test_error_paths_of_the_round2_entry_points():
+    """EINVAL / ENOMEM of the plan-strings, CSS-index, workspace and allocator entry points (include/parpa.h)"""
+    import ctypes
+    from paper_1905_13415_b200 import _lib
+    L = _lib.load()
+    data = b"1,a\n2,b\n" * 1000
+    d = dev(data)
+    with parpa.Plan(parpa.Dfa.dialect("csv"), d) as plan:
+        res = plan.emit(parpa.Schema([oracle.INT64, oracle.SPAN]))
+        col = res.columns[1].struct()
+        offs = torch.empty(res.records + 1, dtype=torch.int64, device="cuda")
+        total = ctypes.c_uint64()
+        assert L.parpa_plan_strings_size(plan._plan, ctypes.byref(col), res.records, 3, ctypes.c_void_p(offs.data_ptr()),
+                                         ctypes.byref(total), None) == parpa.EINVAL          # mode > 2
+        assert L.parpa_plan_strings_copy(plan._plan, ctypes.byref(col), res.records, parpa.CSS_VECTOR, 0x1F,
+                                         ctypes.c_void_p(offs.data_ptr()), ctypes.c_void_p(offs.data_ptr()), None,
+                                         None) == parpa.EINVAL                               # VECTOR without aux
+    cnt = ctypes.c_uint64(7)
+    assert L.parpa_css_index(parpa.CSS_INLINE, 0x1F, None, None, 0, None, ctypes.byref(cnt), None) == 0 and cnt.value == 0
+    assert L.parpa_css_index(parpa.CSS_ARROW, 0x1F, None, None, 0, None, ctypes.byref(cnt), None) == parpa.EINVAL
+    ws = parpa.Workspace(1 << 20)
+    mis = torch.empty(len(data) + 16, dtype=torch.uint8, device="cuda")[1:1 + len(data)]
+    mis.copy_(d)
+    schema = parpa.Schema([oracle.INT64, oracle.SPAN])
+    cols = parpa.alloc_columns(schema, 2100)
+    with pytest.raises(parpa.ParpaError):                                                  # misaligned input
+        parpa.parse_into(parpa.Dfa.dialect("csv"), schema, mis, cols, 2100, parpa.new_stats_tensor(), workspace=ws)
+    ws.close()
+    # an allocator that fails: parpa_parse reports ENOMEM and leaves nothing behind
+    fail = parpa._ALLOC_FN(lambda n, s, c: None)
+    free = parpa._FREE_FN(lambda p, s, c: None)
+    assert L.parpa_set_allocator(ctypes.cast(fail, ctypes.c_void_p), None, None) == parpa.EINVAL   # one of two NULL
+    assert L.parpa_set_allocator(ctypes.cast(fail, ctypes.c_void_p), ctypes.cast(free, ctypes.c_void_p), None) == 0
+    try:
+        r = ctypes.c_void_p()
+        sch = schema.struct()
+        dfa_csv = parpa.Dfa.dialect("csv")                # (kept alive across the call)
+        rc = L.parpa_parse(dfa_csv.handle, ctypes.byref(sch), ctypes.c_void_p(d.data_ptr()), d.numel(), None,
+                           ctypes.byref(r))
+        assert rc == parpa.ENOMEM, rc
+    finally:
+        assert L.parpa_set_allocator(None, None, None) == 0
