@@ -801,11 +801,14 @@ template <int K> struct Masks {             // a lane's K chunks (chunk lane * K
 #define PARPA_E2_ROWS_MIN 16
 #endif
 constexpr uint32_t E2_ROWS_MIN = PARPA_E2_ROWS_MIN;  // tiles with at least this many rows: column-uniform E2
-constexpr int E2_ROWS_MIN_MAX = 16;
-static_assert(E2_ROWS_MIN <= E2_ROWS_MIN_MAX, "c_rcp16 covers nrows < 16");
+constexpr int E2_ROWS_MIN_MAX = 32;
+static_assert(E2_ROWS_MIN <= E2_ROWS_MIN_MAX, "c_rcp16 covers nrows < 32");
 constexpr uint32_t E1A_SELECT_MAX = 32;              // tiles with at most this many delimiters: one select round
+// 65536/d + 1: (n * c_rcp16[d]) >> 16 == n / d exactly for every d < 32 and n < 1024 (the numerators are < 128)
 __constant__ uint32_t c_rcp16[E2_ROWS_MIN_MAX] = {0u, 65537u, 32769u, 21846u, 16385u, 13108u, 10923u, 9363u, 8193u,
-                                                   7282u, 6554u, 5958u, 5462u, 5042u, 4682u, 4370u};   // 65536/d + 1
+                                                   7282u, 6554u, 5958u, 5462u, 5042u, 4682u, 4370u, 4097u, 3856u, 3641u,
+                                                   3450u, 3277u, 3121u, 2979u, 2850u, 2731u, 2622u, 2521u, 2428u, 2341u,
+                                                   2260u, 2185u, 2115u};
 constexpr uint32_t FIELD_WRITTEN = 0xFFFFFFFFu;   // E1 already wrote this field
 constexpr uint32_t FIELD_FAR = 0xFFFFFFFEu;       // field 0 began before the tile: see WarpScratch::f0
 
@@ -1477,7 +1480,7 @@ __device__ __forceinline__ void emit_tile(const KArgs &a, const ColDesc *cols, W
   // columns share one converter, so mixed int / float steps do not diverge.
   const uint32_t total = a.C * nrows;
   const uint32_t it0 = (uint32_t)lane + 32u * (NP == 1 ? 0u : part), step = 32u * NP;
-  // division by nrows (1..15 here) as a multiply by a 16-bit reciprocal: exact for numerators < 4096
+  // division by nrows (< E2_ROWS_MIN here) as a multiply by a 16-bit reciprocal (exact, see c_rcp16)
   const uint32_t rcp = c_rcp16[nrows];
   uint32_t c = (it0 * rcp) >> 16, jr = it0 - c * nrows;
   const uint32_t dc = (step * rcp) >> 16, djr = step - dc * nrows;
