@@ -1593,6 +1593,16 @@ __global__ void __launch_bounds__(SPARSE_WARPS * 32, PARPA_SPARSE_MINB) k_emit_s
     if (u >= nunits) break;
     const uint32_t t0 = u * SPARSE_K;
     const unsigned long long ustart = (unsigned long long)t0 * WT;
+#ifndef PARPA_NO_SPARSE_PREFETCH
+    {                                                    // the unit this warp will take about one round later:
+      const uint32_t un = u + nw;                        // its masks (3 KB) and tile prefixes into L2
+      if (un < nunits) {
+        const unsigned long long tn = (unsigned long long)un * SPARSE_K;
+        if (lane < 24) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.masks + tn * 96 + (unsigned)lane * 16));
+        else if (lane == 24) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.tinfo + tn));
+      }
+    }
+#endif
     Masks<SPARSE_K> mm;
     // chunk lane * K + j of the unit: tile t0 + (lane * K + j) / 32, lane (lane * K + j) % 32 of its masks
     const unsigned long long *mk0 = a.masks + (unsigned long long)t0 * 96;
