@@ -172,7 +172,7 @@ int work_alloc(Work &w, uint64_t len, uint32_t /*C*/, bool need_aligned_copy, cu
   uint64_t nt64 = (len + WT - 1) / WT;
   if (nt64 > 0x07FFFFFFull) return PARPA_EUNSUPPORTED;       // chunk index must fit 32 bits
   w.ntiles = (uint32_t)nt64;
-  w.nblk = (uint32_t)((nt64 + SCAN_TILE - 1) / SCAN_TILE);
+  w.nblk = (uint32_t)((nt64 + SEG_TILE - 1) / SEG_TILE);     // k_seg_scan's blocks (>= k_tau_scan's)
   size_t nt = std::max<size_t>(w.ntiles, 1), nb = std::max<size_t>(w.nblk, 1);
   w.dq_cap = (uint32_t)std::min<uint64_t>(std::max<uint64_t>(4096, len / 512), 1u << 24);
   size_t o = 0;
@@ -395,7 +395,7 @@ int launch_half2(const KArgs &a, const DfaK &k0, cudaStream_t s, uint32_t *launc
   DevCfg *dc;
   int rc = dev_cfg(&dc);
   if (rc) return rc;
-  const uint32_t nblk = (a.ntiles + SCAN_TILE - 1) / SCAN_TILE;
+  const uint32_t nblk = (a.ntiles + SEG_TILE - 1) / SEG_TILE;
   {
     Launch L(s, "k_pass2");
     CK(launch_k(k_pass2, grid_for(dc->occ_pass2, dc->sms, a.ntiles, PASS_WARPS), PASS_WARPS * 32, PASS_SMEM, s, true, a, k));

@@ -46,8 +46,19 @@ __device__ __forceinline__ PassSmem pass_smem(uint8_t *smem, int warp, int lane)
   p.laneaddr = p.laneoff | (((sb + lut_off) >> 16) << 16);   // PRMT layout (pass 1)
   return p;
 }
-constexpr int SCAN_THREADS = 256, SCAN_ITEMS = 8;
-constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS; // warp tiles per scan block (4 MB of input)
+#ifndef PARPA_SCAN_ITEMS
+#define PARPA_SCAN_ITEMS 8
+#endif
+constexpr int SCAN_THREADS = 256, SCAN_ITEMS = PARPA_SCAN_ITEMS;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS; // warp tiles per scan block (4 MB of input at 8 items)
+// k_seg_scan: fewer items per thread (more, shorter blocks: its look-back chain is the cost; measured 4 vs 8
+// items: 0.162 -> 0.143 ms on yelp 4.8 GB).  The look-back arrays are sized by its (larger) block count.
+#ifndef PARPA_SEG_ITEMS
+#define PARPA_SEG_ITEMS 4
+#endif
+constexpr int SEG_ITEMS = PARPA_SEG_ITEMS;
+constexpr int SEG_TILE = SCAN_THREADS * SEG_ITEMS;
+static_assert(SEG_TILE <= SCAN_TILE, "the workspace's look-back arrays are sized by k_seg_scan's blocks");
 
 __device__ __forceinline__ int chunk_valid(const KArgs &a, unsigned long long cstart) {
   return cstart >= a.len ? 0 : (int)min((unsigned long long)CHUNK, a.len - cstart);
@@ -350,10 +361,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_seg_scan(const KArgs a) {
   if (threadIdx.x == 0) s_bid = atomicAdd(&a.ctrl->ticket2, 1u);
   __syncthreads();
   const uint32_t b = s_bid;
-  const unsigned long long t0 = (unsigned long long)b * SCAN_TILE + (unsigned long long)threadIdx.x * SCAN_ITEMS;
+  const unsigned long long t0 = (unsigned long long)b * SEG_TILE + (unsigned long long)threadIdx.x * SEG_ITEMS;
   Seg loc = seg_ident();
 #pragma unroll
-  for (int k = 0; k < SCAN_ITEMS; k++)
+  for (int k = 0; k < SEG_ITEMS; k++)
     if (t0 + k < a.ntiles) loc = seg_op(loc, wseg_at(a, t0 + k));
   Seg inc = loc;
 #pragma unroll
@@ -394,13 +405,13 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_seg_scan(const KArgs a) {
     }
     if (lane == 0) {
       s_prefix = prefix;
-      if ((unsigned long long)(b + 1) * SCAN_TILE >= a.ntiles) *a.tot_seg = seg_op(prefix, bagg);
+      if ((unsigned long long)(b + 1) * SEG_TILE >= a.ntiles) *a.tot_seg = seg_op(prefix, bagg);
     }
   }
   __syncthreads();
   Seg cur = seg_op(seg_op(s_prefix, s_warp[warp]), wex);
 #pragma unroll
-  for (int k = 0; k < SCAN_ITEMS; k++) {
+  for (int k = 0; k < SEG_ITEMS; k++) {
     if (t0 + k >= a.ntiles) break;
     a.tinfo[t0 + k].excl = cur;
     cur = seg_op(cur, wseg_at(a, t0 + k));
