@@ -1698,6 +1698,7 @@ __global__ void __launch_bounds__(EMIT_WARPS * 32, PARPA_EMIT_MINB) k_emit(const
       const unsigned long long tn = (unsigned long long)(t + nw);   // its loads then wait on L2, not DRAM
       asm volatile("prefetch.global.L2 [%0];" ::"l"(a.in + tn * WT + (unsigned long long)lane * CHUNK));
       if (lane < 6) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.masks + tn * 96 + lane * 16));
+      else if (lane == 6) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.tinfo + tn));   // and its prefix
     }
 #endif
     const unsigned long long *mk = a.masks + (unsigned long long)t * 96 + lane;
